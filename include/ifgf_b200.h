@@ -1,0 +1,194 @@
+/* ifgf_b200.h -- C ABI of the B200-native IFGF matvec (libifgf_b200.so).
+ *
+ * Drop-in boundary for the reference's operator path (paths relative to
+ * /root/reference/proj).  The reference is a C++ static library with no FFI;
+ * each entry point below names the C++ interface it replaces:
+ *
+ *   ifgf_apply               ifgf::apply(PointCloud&, const KernelConfig&,
+ *                                        const EngineParams&)   engine.hpp:112-114
+ *   ifgf_plan_create         ifgf::Problem::build                engine.hpp:54-55
+ *   ifgf_plan_apply          apply() minus the rebuild           engine.cpp:270-315
+ *   ifgf_plan_*_pass         singular_pass / eval_level_d /
+ *                            propagation_pass / interpolation_pass engine.hpp:91-110
+ *   ifgf_direct_eval         ifgf::direct_eval                   engine.hpp:117
+ *   ifgf_sample_indices      ifgf::sample_indices                engine.hpp:120
+ *   ifgf_error_at_indices    ifgf::error_at_indices              engine.hpp:123-124
+ *   ifgf_choose_depth        ifgf::choose_depth                  engine.hpp:21
+ *   ifgf_plan_partition      ifgf::dist::partition               dist.hpp:23
+ *
+ * Conventions: plain pointers and sizes, no CUDA or C++ types.  Functions
+ * return 0 on success or an IFGF_E* code mirroring the reference's exception
+ * classes (invalid_argument, domain_error, logic_error, runtime_error);
+ * ifgf_last_error() returns the thread-local message.  Host-pointer entry
+ * points are blocking.  "_device" entry points take device pointers and a
+ * cudaStream_t passed as void* (NULL = legacy default stream); they order
+ * themselves after that stream and make it wait for their completion.
+ * There is no CPU fallback: without a usable sm_100 device every compute
+ * entry point fails with IFGF_ERUNTIME.
+ */
+#ifndef IFGF_B200_H
+#define IFGF_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define IFGF_B200_ABI_VERSION 1
+
+enum {
+  IFGF_OK = 0,
+  IFGF_EINVAL = 1,   /* std::invalid_argument */
+  IFGF_EDOMAIN = 2,  /* std::domain_error     */
+  IFGF_ELOGIC = 3,   /* std::logic_error      */
+  IFGF_ERUNTIME = 4  /* std::runtime_error (CUDA, memory, device) */
+};
+
+enum { IFGF_HELMHOLTZ = 0, IFGF_LAPLACE = 1 }; /* KernelKind, kernel.hpp:13 */
+
+/* EngineParams (engine.hpp:12-19) + InterpOrders (interp.hpp:11-14). */
+typedef struct ifgf_params {
+  int depth;          /* 0 = choose_depth */
+  double box_lambda;  /* 0.25 */
+  int points_per_box; /* 64 */
+  int base_s, base_theta, base_phi; /* 1, 2, 4 */
+  int p_s, p_theta, p_phi;          /* 3, 5, 5 */
+  int device;                       /* CUDA ordinal (replaces `threads`) */
+} ifgf_params;
+
+#define IFGF_MAX_LEVELS 22
+
+/* ApplyReport (engine.hpp:23-42).  Seconds: setup is host wall clock around
+ * the device setup; the pass times are CUDA-event durations. */
+typedef struct ifgf_report {
+  double setup, singular, level_d, interpolation, propagation, total;
+  int depth;
+  size_t n;
+  double h_level_d;
+  int n_levels;                           /* levels d = 3..depth */
+  size_t level_boxes[IFGF_MAX_LEVELS];    /* index d - 3 */
+  size_t level_cones[IFGF_MAX_LEVELS];
+  size_t peak_live_blocks;
+  size_t gpu_launches;                    /* kernels launched by this call */
+} ifgf_report;
+
+typedef struct ifgf_plan ifgf_plan;
+
+void ifgf_default_params(ifgf_params* p);
+const char* ifgf_last_error(void);
+int ifgf_abi_version(void);
+/* 1 if a usable sm_100 device is visible, else 0 (message in last_error). */
+int ifgf_device_ok(void);
+
+int ifgf_choose_depth(size_t n, double cube_side, double kappa, const ifgf_params* p,
+                      int* depth_out);
+
+/* ---- plan = Problem::build on the device ---- */
+int ifgf_plan_create(const double* x1, const double* x2, const double* x3, size_t n,
+                     int kernel_kind, double wavenumber, const ifgf_params* p,
+                     ifgf_plan** out);
+int ifgf_plan_create_device(const double* d_x1, const double* d_x2, const double* d_x3,
+                            size_t n, int kernel_kind, double wavenumber,
+                            const ifgf_params* p, void* stream, ifgf_plan** out);
+void ifgf_plan_destroy(ifgf_plan* plan);
+
+/* Plan options.  IFGF_OPT_SERIAL = 1 runs every apply kernel on one stream
+ * (no near-field / interpolation overlap) so per-pass event times are
+ * exclusive; used for per-kernel roofline measurement. */
+enum { IFGF_OPT_SERIAL = 1 };
+int ifgf_plan_set_option(ifgf_plan* plan, int option, int value);
+
+/* ---- operator application; i_* in the caller's original point order ---- */
+int ifgf_plan_apply(ifgf_plan* plan, const double* a_re, const double* a_im, double* i_re,
+                    double* i_im, ifgf_report* rep);
+int ifgf_plan_apply_device(ifgf_plan* plan, const double* d_a_re, const double* d_a_im,
+                           double* d_i_re, double* d_i_im, void* stream, ifgf_report* rep);
+/* create + apply + destroy: the exact contract of ifgf::apply (a_im may be
+ * NULL for a real density). */
+int ifgf_apply(size_t n, const double* x1, const double* x2, const double* x3,
+               const double* a_re, const double* a_im, int kernel_kind, double wavenumber,
+               const ifgf_params* p, double* i_re, double* i_im, ifgf_report* rep);
+
+/* ---- structure export (parity against Problem::build) ---- */
+typedef struct ifgf_plan_info {
+  size_t n;
+  int depth;
+  double cube_origin[3], cube_side;
+  double kappa;
+  int p_s, p_theta, p_phi, P;
+  size_t boxes[IFGF_MAX_LEVELS];   /* index d (1..depth) */
+  size_t cones[IFGF_MAX_LEVELS];   /* index d (3..depth) */
+  size_t nbr_entries[IFGF_MAX_LEVELS];
+  size_t cousin_entries[IFGF_MAX_LEVELS];
+  double h[IFGF_MAX_LEVELS];
+  double setup_seconds;
+  size_t device_bytes;
+} ifgf_plan_info;
+
+int ifgf_plan_get_info(const ifgf_plan* plan, ifgf_plan_info* info);
+int ifgf_plan_export_perm(const ifgf_plan* plan, uint32_t* perm);
+/* Any pointer may be NULL.  Arrays are sized from ifgf_plan_info; child_begin
+ * has boxes+1 entries for d < depth, CSR offsets have boxes+1 entries, and
+ * cone arrays exist for d >= 3 (OctreeLevel octree.hpp:23-38, LevelConeSet
+ * cones.hpp:97-104). */
+int ifgf_plan_export_level(const ifgf_plan* plan, int d, uint64_t* codes, uint32_t* first,
+                           uint32_t* count, double* centers3, uint32_t* parent,
+                           uint32_t* child_begin, uint32_t* nbr_off, uint32_t* nbr,
+                           uint32_t* cousin_off, uint32_t* cousin, uint32_t* cone_box,
+                           uint64_t* cone_gamma, uint32_t* box_cone_begin);
+
+/* ---- pass-level API (engine.hpp:91-110) over plan-owned device state ----
+ * set_density takes host arrays in the caller's order; the result buffer is
+ * in sorted order until read back.  Blocks are the reference BlockStore
+ * layout on the host side: planar re and im, [cones][P]. */
+int ifgf_plan_set_density(ifgf_plan* plan, const double* a_re, const double* a_im);
+int ifgf_plan_zero_result(ifgf_plan* plan);
+int ifgf_plan_singular_pass(ifgf_plan* plan, size_t pt_begin, size_t pt_end);
+int ifgf_plan_level_d_pass(ifgf_plan* plan, uint32_t cone_begin, uint32_t cone_end);
+int ifgf_plan_propagation_pass(ifgf_plan* plan, int d, uint32_t pcone_begin,
+                               uint32_t pcone_end);
+int ifgf_plan_interpolation_pass(ifgf_plan* plan, int d, size_t pt_begin, size_t pt_end);
+int ifgf_plan_read_blocks(ifgf_plan* plan, int d, double* re, double* im);
+int ifgf_plan_write_blocks(ifgf_plan* plan, int d, const double* re, const double* im);
+int ifgf_plan_read_result(ifgf_plan* plan, int sorted_order, double* i_re, double* i_im);
+/* Device-side block exchange for multi-GPU: pack/unpack the blocks of the
+ * listed cone ordinals (device u32 array) to/from a contiguous device buffer
+ * of m * 2P doubles. */
+int ifgf_plan_pack_blocks(ifgf_plan* plan, int d, const uint32_t* d_cones, size_t m,
+                          double* d_buf, void* stream);
+int ifgf_plan_unpack_blocks(ifgf_plan* plan, int d, const uint32_t* d_cones, size_t m,
+                            const double* d_buf, void* stream);
+/* Rank layout (dist.cpp:78-130): box_begin and point_begin have n_ranks+1
+ * entries, cone_begin has (depth-2)*(n_ranks+1), level-major from d = 3. */
+int ifgf_plan_partition(const ifgf_plan* plan, int n_ranks, uint32_t* box_begin,
+                        uint32_t* point_begin, uint32_t* cone_begin);
+/* Deduplicated foreign cones rank `rank` needs at level d (kind 0:
+ * interpolation data, dist.cpp:179-201; kind 1: propagation data,
+ * dist.cpp:206-237), sorted.  Call with cones == NULL to get the count. */
+int ifgf_plan_exchange_set(ifgf_plan* plan, int n_ranks, int rank, int d, int kind,
+                           uint32_t* cones, size_t* count);
+
+/* ---- oracle side (engine.hpp:117-128), computed on the device ---- */
+/* o_* = exact sums at the m listed targets (all points if targets == NULL). */
+int ifgf_direct_eval(size_t n, const double* x1, const double* x2, const double* x3,
+                     const double* a_re, const double* a_im, int kernel_kind,
+                     double wavenumber, const uint32_t* targets, size_t m, int device,
+                     double* o_re, double* o_im);
+int ifgf_sample_indices(size_t n, size_t m, uint64_t seed, uint32_t* out);
+int ifgf_error_at_indices(size_t n, const double* x1, const double* x2, const double* x3,
+                          const double* a_re, const double* a_im, const double* i_re,
+                          const double* i_im, int kernel_kind, double wavenumber,
+                          const uint32_t* idx, size_t m, int device, double* eps);
+
+/* ---- seeded synthetic inputs; host only ----
+ * shape 0: unit sphere (normalised Gaussians); 1: spheroid (1,1,c), area
+ * uniform by rejection.  dens 0: complex U(-1,1); 1: real N(0,1), a_im = 0. */
+int ifgf_generate(size_t n, int shape, double c, int dens, uint64_t seed, double* x1,
+                  double* x2, double* x3, double* a_re, double* a_im);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* IFGF_B200_H */

@@ -1,0 +1,357 @@
+// C-ABI shim over the UNMODIFIED reference library (test infrastructure only).
+//
+// Compiled by oracle/Makefile together with the reference sources where they
+// lie under /root/reference/proj/src into oracle/_ref/libifgf_ref.so.  Only
+// tests/, __graft_entry__.smoke() and bench.py's reference / cpu_baseline legs
+// may load it: it is the checker and the CPU baseline, never the product.
+//
+// Every entry point forwards to the reference's own public API:
+//   apply / direct_eval / sample_indices / error_at_indices  (engine.hpp:112-128)
+//   Problem::build and the four passes                        (engine.hpp:46-110)
+//   dist::partition / dist::run_distributed                   (dist.hpp:23, 90)
+// and maps the reference's exception classes onto the return codes of
+// include/ifgf_b200.h (0 ok, 1 invalid_argument, 2 domain_error,
+// 3 logic_error, 4 runtime_error).
+
+#include <cstdint>
+#include <cstring>
+#include <exception>
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "ifgf/dist.hpp"
+#include "ifgf/engine.hpp"
+#include "ifgf/simd_kernels.hpp"
+
+using namespace ifgf;
+
+namespace {
+
+thread_local std::string g_err;
+
+template <class F>
+int guarded(F&& f) {
+  try {
+    f();
+    return 0;
+  } catch (const std::invalid_argument& e) {
+    g_err = e.what();
+    return 1;
+  } catch (const std::domain_error& e) {
+    g_err = e.what();
+    return 2;
+  } catch (const std::logic_error& e) {
+    g_err = e.what();
+    return 3;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return 4;
+  }
+}
+
+PointCloud make_cloud(std::size_t n, const double* x1, const double* x2, const double* x3,
+                      const double* a_re, const double* a_im) {
+  PointCloud pc;
+  pc.resize(n);
+  for (std::size_t i = 0; i < n; ++i) {
+    pc.x1[i] = x1[i];
+    pc.x2[i] = x2[i];
+    pc.x3[i] = x3[i];
+    pc.a_re[i] = a_re ? a_re[i] : 0.0;
+    pc.a_im[i] = a_im ? a_im[i] : 0.0;
+  }
+  return pc;
+}
+
+KernelConfig make_cfg(int kind, double k) {
+  return {kind == 1 ? KernelKind::Laplace : KernelKind::Helmholtz, k};
+}
+
+// ip = {depth, points_per_box, base_s, base_theta, base_phi, p_s, p_theta, p_phi, threads}
+EngineParams make_params(const int* ip, double box_lambda) {
+  EngineParams p;
+  p.depth = ip[0];
+  p.points_per_box = ip[1];
+  p.base_s = ip[2];
+  p.base_theta = ip[3];
+  p.base_phi = ip[4];
+  p.orders = {ip[5], ip[6], ip[7]};
+  p.threads = ip[8];
+  p.box_lambda = box_lambda;
+  return p;
+}
+
+struct RefProblem {
+  Problem prob;
+  KernelConfig cfg;
+  EngineParams params;
+};
+
+}  // namespace
+
+extern "C" {
+
+const char* ref_last_error(void) { return g_err.c_str(); }
+const char* ref_simd_variant(void) { return simd::active_variant_name(); }
+
+int ref_choose_depth(std::size_t n, double side, double kappa, const int* ip, double box_lambda,
+                     int* out) {
+  return guarded([&] { *out = choose_depth(n, side, kappa, make_params(ip, box_lambda)); });
+}
+
+// seconds6 = {setup, singular, level_d, interpolation, propagation, total}
+int ref_apply(std::size_t n, const double* x1, const double* x2, const double* x3,
+              const double* a_re, const double* a_im, int kind, double k, const int* ip,
+              double box_lambda, double* i_re, double* i_im, double* seconds6, int* depth,
+              std::size_t* peak_blocks) {
+  return guarded([&] {
+    PointCloud pc = make_cloud(n, x1, x2, x3, a_re, a_im);
+    const ApplyReport rep = apply(pc, make_cfg(kind, k), make_params(ip, box_lambda));
+    std::memcpy(i_re, pc.i_re.data(), n * sizeof(double));
+    std::memcpy(i_im, pc.i_im.data(), n * sizeof(double));
+    if (seconds6) {
+      seconds6[0] = rep.seconds.setup;
+      seconds6[1] = rep.seconds.singular;
+      seconds6[2] = rep.seconds.level_d;
+      seconds6[3] = rep.seconds.interpolation;
+      seconds6[4] = rep.seconds.propagation;
+      seconds6[5] = rep.seconds.total;
+    }
+    if (depth) *depth = rep.depth;
+    if (peak_blocks) *peak_blocks = rep.peak_live_blocks;
+  });
+}
+
+// comm: per level d=3..D (index d-3): {interp_fetched, prop_fetched,
+// max_interp_fanout, max_prop_fanout, owned_blocks, peak_rank_cache_blocks,
+// max_rank_owned_blocks}; caller provides 7*19 slots.
+int ref_run_distributed(std::size_t n, const double* x1, const double* x2, const double* x3,
+                        const double* a_re, const double* a_im, int kind, double k,
+                        const int* ip, double box_lambda, int n_ranks, double* i_re,
+                        double* i_im, std::uint64_t* comm, int* n_levels) {
+  return guarded([&] {
+    PointCloud pc = make_cloud(n, x1, x2, x3, a_re, a_im);
+    const dist::DistReport rep =
+        dist::run_distributed(pc, make_cfg(kind, k), make_params(ip, box_lambda), n_ranks);
+    std::memcpy(i_re, pc.i_re.data(), n * sizeof(double));
+    std::memcpy(i_im, pc.i_im.data(), n * sizeof(double));
+    if (n_levels) *n_levels = static_cast<int>(rep.comm.levels.size());
+    if (comm) {
+      for (std::size_t l = 0; l < rep.comm.levels.size(); ++l) {
+        const auto& s = rep.comm.levels[l];
+        std::uint64_t* o = comm + 7 * l;
+        o[0] = s.interp_fetched;
+        o[1] = s.prop_fetched;
+        o[2] = s.max_interp_fanout;
+        o[3] = s.max_prop_fanout;
+        o[4] = s.owned_blocks;
+        o[5] = s.peak_rank_cache_blocks;
+        o[6] = s.max_rank_owned_blocks;
+      }
+    }
+  });
+}
+
+int ref_direct_eval(std::size_t n, const double* x1, const double* x2, const double* x3,
+                    const double* a_re, const double* a_im, int kind, double k, int threads,
+                    double* i_re, double* i_im) {
+  return guarded([&] {
+    PointCloud pc = make_cloud(n, x1, x2, x3, a_re, a_im);
+    direct_eval(pc, make_cfg(kind, k), threads);
+    std::memcpy(i_re, pc.i_re.data(), n * sizeof(double));
+    std::memcpy(i_im, pc.i_im.data(), n * sizeof(double));
+  });
+}
+
+int ref_sample_indices(std::size_t n, std::size_t m, std::uint64_t seed, std::uint32_t* out) {
+  return guarded([&] {
+    const auto idx = sample_indices(n, m, seed);
+    std::memcpy(out, idx.data(), m * sizeof(std::uint32_t));
+  });
+}
+
+int ref_error_at_indices(std::size_t n, const double* x1, const double* x2, const double* x3,
+                         const double* a_re, const double* a_im, const double* i_re,
+                         const double* i_im, int kind, double k, const std::uint32_t* idx,
+                         std::size_t m, int threads, double* eps) {
+  return guarded([&] {
+    PointCloud pc = make_cloud(n, x1, x2, x3, a_re, a_im);
+    std::memcpy(pc.i_re.data(), i_re, n * sizeof(double));
+    std::memcpy(pc.i_im.data(), i_im, n * sizeof(double));
+    *eps = error_at_indices(pc, make_cfg(kind, k), std::span<const std::uint32_t>(idx, m),
+                            threads);
+  });
+}
+
+// ---------------------------------------------------------------- Problem --
+
+void* ref_problem_build(std::size_t n, const double* x1, const double* x2, const double* x3,
+                        const double* a_re, const double* a_im, int kind, double k,
+                        const int* ip, double box_lambda) {
+  RefProblem* h = nullptr;
+  const int rc = guarded([&] {
+    auto p = std::make_unique<RefProblem>();
+    p->cfg = make_cfg(kind, k);
+    p->params = make_params(ip, box_lambda);
+    p->prob = Problem::build(make_cloud(n, x1, x2, x3, a_re, a_im), p->cfg, p->params);
+    h = p.release();
+  });
+  return rc == 0 ? h : nullptr;
+}
+
+void ref_problem_free(void* h) { delete static_cast<RefProblem*>(h); }
+
+int ref_problem_depth(void* h) { return static_cast<RefProblem*>(h)->prob.depth; }
+
+void ref_problem_cube(void* h, double* out4) {
+  const auto& c = static_cast<RefProblem*>(h)->prob.cube;
+  out4[0] = c.origin.x;
+  out4[1] = c.origin.y;
+  out4[2] = c.origin.z;
+  out4[3] = c.side;
+}
+
+void ref_problem_sorted(void* h, std::uint32_t* perm, double* x1, double* x2, double* x3,
+                        double* a_re, double* a_im) {
+  const Problem& p = static_cast<RefProblem*>(h)->prob;
+  const std::size_t n = p.cloud.size();
+  std::memcpy(perm, p.perm.data(), n * sizeof(std::uint32_t));
+  std::memcpy(x1, p.cloud.x1.data(), n * sizeof(double));
+  std::memcpy(x2, p.cloud.x2.data(), n * sizeof(double));
+  std::memcpy(x3, p.cloud.x3.data(), n * sizeof(double));
+  std::memcpy(a_re, p.cloud.a_re.data(), n * sizeof(double));
+  std::memcpy(a_im, p.cloud.a_im.data(), n * sizeof(double));
+}
+
+// sizes = {boxes, cones, nbr_entries, cousin_entries, h as bits}
+void ref_problem_level_sizes(void* h, int d, std::uint64_t* sizes) {
+  const Problem& p = static_cast<RefProblem*>(h)->prob;
+  const OctreeLevel& l = p.tree.level(d);
+  sizes[0] = l.size();
+  sizes[1] = d >= 3 ? p.cones.level(d).size() : 0;
+  sizes[2] = l.nbr.size();
+  sizes[3] = l.cousin.size();
+  std::memcpy(&sizes[4], &l.h, sizeof(double));
+}
+
+void ref_problem_level_boxes(void* h, int d, std::uint64_t* codes, std::uint32_t* first,
+                             std::uint32_t* count, double* centers3, std::uint32_t* parent,
+                             std::uint32_t* child_begin) {
+  const Problem& p = static_cast<RefProblem*>(h)->prob;
+  const OctreeLevel& l = p.tree.level(d);
+  for (std::size_t b = 0; b < l.size(); ++b) {
+    codes[b] = l.codes[b];
+    first[b] = l.boxes[b].first_point;
+    count[b] = l.boxes[b].point_count;
+    centers3[3 * b] = l.boxes[b].center.x;
+    centers3[3 * b + 1] = l.boxes[b].center.y;
+    centers3[3 * b + 2] = l.boxes[b].center.z;
+    if (parent) parent[b] = d >= 2 ? l.parent[b] : 0;
+  }
+  if (child_begin && d < p.depth)
+    std::memcpy(child_begin, l.child_begin.data(), (l.size() + 1) * sizeof(std::uint32_t));
+}
+
+void ref_problem_level_adjacency(void* h, int d, std::uint32_t* nbr_off, std::uint32_t* nbr,
+                                 std::uint32_t* cousin_off, std::uint32_t* cousin) {
+  const Problem& p = static_cast<RefProblem*>(h)->prob;
+  const OctreeLevel& l = p.tree.level(d);
+  std::memcpy(nbr_off, l.nbr_off.data(), l.nbr_off.size() * sizeof(std::uint32_t));
+  std::memcpy(nbr, l.nbr.data(), l.nbr.size() * sizeof(std::uint32_t));
+  if (d >= 3) {
+    std::memcpy(cousin_off, l.cousin_off.data(), l.cousin_off.size() * sizeof(std::uint32_t));
+    std::memcpy(cousin, l.cousin.data(), l.cousin.size() * sizeof(std::uint32_t));
+  }
+}
+
+void ref_problem_level_cones(void* h, int d, std::uint32_t* cone_box, std::uint64_t* gamma,
+                             std::uint32_t* box_cone_begin) {
+  const Problem& p = static_cast<RefProblem*>(h)->prob;
+  const LevelConeSet& cs = p.cones.level(d);
+  std::memcpy(cone_box, cs.cone_box.data(), cs.size() * sizeof(std::uint32_t));
+  std::memcpy(gamma, cs.cone_gamma.data(), cs.size() * sizeof(std::uint64_t));
+  std::memcpy(box_cone_begin, cs.box_cone_begin.data(),
+              cs.box_cone_begin.size() * sizeof(std::uint32_t));
+}
+
+// Passes over the sorted problem; outputs in sorted order / cone order.
+int ref_problem_singular(void* h, std::size_t b, std::size_t e, int threads, double* i_re,
+                         double* i_im) {
+  auto* P = static_cast<RefProblem*>(h);
+  return guarded([&] {
+    const std::size_t n = P->prob.cloud.size();
+    std::vector<double> re(i_re, i_re + n), im(i_im, i_im + n);
+    singular_pass(P->prob, P->cfg, b, e, threads, re, im);
+    std::memcpy(i_re, re.data(), n * sizeof(double));
+    std::memcpy(i_im, im.data(), n * sizeof(double));
+  });
+}
+
+int ref_problem_level_d(void* h, int threads, double* blk_re, double* blk_im) {
+  auto* P = static_cast<RefProblem*>(h);
+  return guarded([&] {
+    const int D = P->prob.depth;
+    const std::size_t nc = P->prob.cones.level(D).size();
+    BlockStore st;
+    st.allocate(nc, P->params.orders.total());
+    eval_level_d(P->prob, P->cfg, 0, static_cast<std::uint32_t>(nc), threads, st);
+    std::memcpy(blk_re, st.re.data(), st.re.size() * sizeof(double));
+    std::memcpy(blk_im, st.im.data(), st.im.size() * sizeof(double));
+  });
+}
+
+int ref_problem_propagation(void* h, int d, int threads, const double* child_re,
+                            const double* child_im, double* par_re, double* par_im) {
+  auto* P = static_cast<RefProblem*>(h);
+  return guarded([&] {
+    const int Pn = P->params.orders.total();
+    const std::size_t nc = P->prob.cones.level(d).size();
+    const std::size_t np = P->prob.cones.level(d - 1).size();
+    BlockStore child;
+    child.allocate(nc, Pn);
+    std::memcpy(child.re.data(), child_re, nc * Pn * sizeof(double));
+    std::memcpy(child.im.data(), child_im, nc * Pn * sizeof(double));
+    BlockStore par;
+    par.allocate(np, Pn);
+    propagation_pass(P->prob, P->cfg, d, BlockTable::all_of(child, nc), 0,
+                     static_cast<std::uint32_t>(np), threads, par);
+    std::memcpy(par_re, par.re.data(), par.re.size() * sizeof(double));
+    std::memcpy(par_im, par.im.data(), par.im.size() * sizeof(double));
+  });
+}
+
+int ref_problem_interpolation(void* h, int d, int threads, const double* blk_re,
+                              const double* blk_im, double* i_re, double* i_im) {
+  auto* P = static_cast<RefProblem*>(h);
+  return guarded([&] {
+    const int Pn = P->params.orders.total();
+    const std::size_t nc = P->prob.cones.level(d).size();
+    const std::size_t n = P->prob.cloud.size();
+    BlockStore st;
+    st.allocate(nc, Pn);
+    std::memcpy(st.re.data(), blk_re, nc * Pn * sizeof(double));
+    std::memcpy(st.im.data(), blk_im, nc * Pn * sizeof(double));
+    std::vector<double> re(i_re, i_re + n), im(i_im, i_im + n);
+    interpolation_pass(P->prob, P->cfg, d, BlockTable::all_of(st, nc), 0, n, threads, re, im);
+    std::memcpy(i_re, re.data(), n * sizeof(double));
+    std::memcpy(i_im, im.data(), n * sizeof(double));
+  });
+}
+
+// box_begin / point_begin: n_ranks+1 each; cone_begin: (D-2)*(n_ranks+1), level-major.
+int ref_problem_partition(void* h, int n_ranks, std::uint32_t* box_begin,
+                          std::uint32_t* point_begin, std::uint32_t* cone_begin) {
+  auto* P = static_cast<RefProblem*>(h);
+  return guarded([&] {
+    const dist::RankLayout L = dist::partition(P->prob.tree, P->prob.cones, n_ranks);
+    std::memcpy(box_begin, L.box_begin.data(), (n_ranks + 1) * sizeof(std::uint32_t));
+    std::memcpy(point_begin, L.point_begin.data(), (n_ranks + 1) * sizeof(std::uint32_t));
+    for (std::size_t l = 0; l < L.cone_begin.size(); ++l)
+      std::memcpy(cone_begin + l * (n_ranks + 1), L.cone_begin[l].data(),
+                  (n_ranks + 1) * sizeof(std::uint32_t));
+  });
+}
+
+}  // extern "C"

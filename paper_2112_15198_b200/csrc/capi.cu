@@ -1,0 +1,916 @@
+// capi.cu -- the C ABI (include/ifgf_b200.h): plan lifecycle, the apply
+// orchestration (engine.cpp:260-325) on two CUDA streams, the pass-level API
+// (engine.hpp:91-110), structure export, rank layout and exchange sets
+// (dist.cpp:78-237), and the device-side direct sums.
+//
+// Apply schedule (one plan, one GPU):
+//   s_main: gather densities -> K2 level-D blocks -> K3(D) -> K3(D-1) -> ... -> K3(4)
+//   s_aux : K1 near field -> K4(D) -> K4(D-1) -> ... -> K4(3)        (all += into i)
+//   K4(d) waits for "blocks of level d ready"; K3(d) overwrites the slot of
+//   level d-1+n_slots and therefore waits for K4 of that level.  With one slot
+//   per level (the default whenever the blocks fit) K3 never waits on K4, so
+//   propagation and interpolation of a level overlap.
+#include <cub/cub.cuh>
+
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstring>
+#include <memory>
+#include <new>
+#include <random>
+#include <string>
+#include <vector>
+
+#include "plan.hpp"
+
+using namespace ifgf_b200;
+
+namespace {
+
+thread_local std::string g_err;
+
+template <class F>
+int guarded(F&& f) {
+  try {
+    f();
+    return IFGF_OK;
+  } catch (const Error& e) {
+    g_err = e.what();
+    return e.code;
+  } catch (const std::bad_alloc&) {
+    g_err = "host allocation failed";
+    return IFGF_ERUNTIME;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return IFGF_ERUNTIME;
+  }
+}
+
+using clk = std::chrono::steady_clock;
+double since(clk::time_point t0) { return std::chrono::duration<double>(clk::now() - t0).count(); }
+
+void require_device(int device) {
+  int count = 0;
+  const cudaError_t e = cudaGetDeviceCount(&count);
+  if (e != cudaSuccess || count == 0)
+    throw Error(IFGF_ERUNTIME, std::string("no CUDA device visible (") +
+                                   (e == cudaSuccess ? "0 devices" : cudaGetErrorString(e)) +
+                                   "); libifgf_b200 has no CPU path");
+  if (device < 0 || device >= count) throw Error(IFGF_EINVAL, "device ordinal out of range");
+  cudaDeviceProp prop;
+  IFGF_CUDA(cudaGetDeviceProperties(&prop, device));
+  if (prop.major != 10)
+    throw Error(IFGF_ERUNTIME, std::string("device ") + prop.name +
+                                   " is not sm_100 (this build targets sm_100a only)");
+  IFGF_CUDA(cudaSetDevice(device));
+  static bool pool_tuned = false;
+  if (!pool_tuned) {
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+      uint64_t thr = UINT64_MAX;
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
+    pool_tuned = true;
+  }
+}
+
+void validate_params(const ifgf_params* p) {
+  if (!p) throw Error(IFGF_EINVAL, "null params");
+  if (p->p_s < 1 || p->p_theta < 1 || p->p_phi < 1 || p->p_s > kMaxOrder ||
+      p->p_theta > kMaxOrder || p->p_phi > kMaxOrder)
+    throw Error(IFGF_EINVAL, "unsupported interpolation orders");
+  if (!orders_supported(p->p_s, p->p_theta, p->p_phi))
+    throw Error(IFGF_EINVAL, "interpolation orders (" + std::to_string(p->p_s) + "," +
+                                 std::to_string(p->p_theta) + "," + std::to_string(p->p_phi) +
+                                 ") are not instantiated in this build");
+  if (p->base_s < 1 || p->base_theta < 1 || p->base_phi < 1)
+    throw Error(IFGF_EINVAL, "cone base counts must be positive");
+}
+
+// interp.hpp:29-31 nodes and interp.cpp:19-34 transforms, host libm.
+InterpConsts make_consts(const ifgf_params* p) {
+  InterpConsts K{};
+  K.ps = p->p_s;
+  K.pt = p->p_theta;
+  K.pp = p->p_phi;
+  K.P = K.ps * K.pt * K.pp;
+  const auto fill = [](int q, double* nodes, double* M) {
+    for (int j = 0; j < q; ++j) nodes[j] = std::cos(kPi * (2.0 * j + 1.0) / (2.0 * q));
+    for (int k = 0; k < q; ++k) {
+      const double w = (k == 0 ? 1.0 : 2.0) / q;
+      for (int j = 0; j < q; ++j) M[k * q + j] = w * std::cos(k * kPi * (2.0 * j + 1.0) / (2.0 * q));
+    }
+  };
+  fill(K.ps, K.ns, K.Ms);
+  fill(K.pt, K.nt, K.Mt);
+  fill(K.pp, K.np, K.Mp);
+  return K;
+}
+
+void plan_free(ifgf_plan* P) {
+  if (!P) return;
+  cudaSetDevice(P->device);
+  if (P->s_main) cudaStreamSynchronize(P->s_main);
+  if (P->s_aux) cudaStreamSynchronize(P->s_aux);
+  for (void* a : P->allocs) cudaFree(a);
+  if (P->s_main) cudaStreamDestroy(P->s_main);
+  if (P->s_aux) cudaStreamDestroy(P->s_aux);
+  delete P;
+}
+
+ifgf_plan* new_plan(size_t n, int kind, double wavenumber, const ifgf_params* p) {
+  if (n < 1) throw Error(IFGF_EINVAL, "empty point cloud");
+  if (n > 0xffffffffull) throw Error(IFGF_EINVAL, "more than 2^32 points");
+  if (kind != IFGF_HELMHOLTZ && kind != IFGF_LAPLACE) throw Error(IFGF_EINVAL, "bad kernel kind");
+  if (!(wavenumber >= 0.0) || !std::isfinite(wavenumber))
+    throw Error(IFGF_EINVAL, "wavenumber must be finite and >= 0");
+  validate_params(p);
+  require_device(p->device);
+  auto* P = new ifgf_plan;
+  P->device = p->device;
+  P->n = n;
+  P->kind = kind;
+  P->kappa = kind == IFGF_LAPLACE ? 0.0 : wavenumber;  // KernelConfig::kappa, kernel.hpp:20
+  P->params = *p;
+  P->K = make_consts(p);
+  try {
+    IFGF_CUDA(cudaStreamCreateWithFlags(&P->s_main, cudaStreamNonBlocking));
+    IFGF_CUDA(cudaStreamCreateWithFlags(&P->s_aux, cudaStreamNonBlocking));
+    P->err = P->alloc<int>(1);
+    IFGF_CUDA(cudaMemsetAsync(P->err, 0, sizeof(int), P->s_main));
+  } catch (...) {
+    plan_free(P);
+    throw;
+  }
+  return P;
+}
+
+void finish_create(ifgf_plan* P, const double* dx, const double* dy, const double* dz) {
+  build_plan(P, dx, dy, dz);
+  P->ar = P->alloc<double>(P->n);
+  P->ai = P->alloc<double>(P->n);
+  P->ir = P->alloc<double>(P->n);
+  P->ii = P->alloc<double>(P->n);
+  IFGF_CUDA(cudaStreamSynchronize(P->s_main));
+}
+
+// Block storage for apply: one slot per level when it fits in half of the
+// free memory, else two slots sized for the largest level.
+void ensure_slots(ifgf_plan* P) {
+  if (P->n_slots) return;
+  const int D = P->depth;
+  const size_t bpc = (size_t)P->K.P * sizeof(double2);
+  size_t total = 0, mx = 0;
+  for (int d = 3; d <= D; ++d) {
+    total += P->lv[d].nc;
+    mx = std::max<size_t>(mx, P->lv[d].nc);
+  }
+  size_t fr = 0, tot = 0;
+  IFGF_CUDA(cudaMemGetInfo(&fr, &tot));
+  if (total * bpc < fr / 2) {
+    double2* base = P->alloc<double2>(total * P->K.P + 1);
+    size_t off = 0;
+    for (int d = 3; d <= D; ++d) {
+      P->slots[d] = base + off * P->K.P;
+      off += P->lv[d].nc;
+    }
+    P->n_slots = D - 2;
+  } else {
+    double2* a = P->alloc<double2>(mx * P->K.P + 1);
+    double2* b = P->alloc<double2>(mx * P->K.P + 1);
+    for (int d = 3; d <= D; ++d) P->slots[d] = (d % 2) ? a : b;
+    P->n_slots = 2;
+  }
+}
+
+struct EventPair {
+  cudaEvent_t a = nullptr, b = nullptr;
+};
+
+// The operator on device buffers (densities/results in caller order).
+void apply_device(ifgf_plan* P, const double* a_re, const double* a_im, double* i_re,
+                  double* i_im, cudaStream_t caller, ifgf_report* rep) {
+  const auto t0 = clk::now();
+  IFGF_CUDA(cudaSetDevice(P->device));
+  ensure_slots(P);
+  const int D = P->depth;
+  const size_t launches0 = P->launches;
+  cudaStream_t sm = P->s_main, sa = P->serial ? P->s_main : P->s_aux;
+
+  std::vector<cudaEvent_t> evs;
+  auto mk = [&](bool timing) {
+    cudaEvent_t e;
+    IFGF_CUDA(cudaEventCreateWithFlags(&e, timing ? cudaEventDefault : cudaEventDisableTiming));
+    evs.push_back(e);
+    return e;
+  };
+  struct Guard {
+    std::vector<cudaEvent_t>& v;
+    ~Guard() {
+      for (auto e : v) cudaEventDestroy(e);
+    }
+  } guard{evs};
+
+  cudaEvent_t start = mk(false);
+  IFGF_CUDA(cudaEventRecord(start, caller));
+  IFGF_CUDA(cudaStreamWaitEvent(sm, start, 0));
+  launch_gather_density(P, a_re, a_im, sm);
+  cudaEvent_t gathered = mk(false);
+  IFGF_CUDA(cudaEventRecord(gathered, sm));
+  IFGF_CUDA(cudaStreamWaitEvent(sa, gathered, 0));
+
+  EventPair t_sing{mk(true), mk(true)}, t_ld{mk(true), mk(true)};
+  std::vector<EventPair> t_int(D + 1), t_prop(D + 1);
+  std::vector<cudaEvent_t> blk_ready(D + 1), int_done(D + 1);
+
+  IFGF_CUDA(cudaEventRecord(t_sing.a, sa));
+  launch_singular(P, 0, P->n, sa);
+  IFGF_CUDA(cudaEventRecord(t_sing.b, sa));
+
+  IFGF_CUDA(cudaEventRecord(t_ld.a, sm));
+  launch_level_d(P, 0, P->lv[D].nc, P->slots[D], sm);
+  IFGF_CUDA(cudaEventRecord(t_ld.b, sm));
+  blk_ready[D] = t_ld.b;
+
+  for (int d = D; d >= 3; --d) {
+    IFGF_CUDA(cudaStreamWaitEvent(sa, blk_ready[d], 0));
+    t_int[d] = {mk(true), mk(true)};
+    IFGF_CUDA(cudaEventRecord(t_int[d].a, sa));
+    launch_interpolation(P, d, 0, P->n, P->slots[d], sa);
+    IFGF_CUDA(cudaEventRecord(t_int[d].b, sa));
+    int_done[d] = t_int[d].b;
+    if (d > 3) {
+      const int prev = d - 1 + P->n_slots;  // previous occupant of level d-1's slot
+      if (P->n_slots < D - 2 && prev <= D) IFGF_CUDA(cudaStreamWaitEvent(sm, int_done[prev], 0));
+      t_prop[d] = {mk(true), mk(true)};
+      IFGF_CUDA(cudaEventRecord(t_prop[d].a, sm));
+      launch_propagation(P, d, 0, P->lv[d - 1].nc, P->slots[d], P->slots[d - 1], sm);
+      IFGF_CUDA(cudaEventRecord(t_prop[d].b, sm));
+      blk_ready[d - 1] = t_prop[d].b;
+    }
+  }
+  IFGF_CUDA(cudaStreamWaitEvent(sm, int_done[3], 0));
+  launch_scatter_result(P, i_re, i_im, sm);
+  cudaEvent_t done = mk(false);
+  IFGF_CUDA(cudaEventRecord(done, sm));
+  IFGF_CUDA(cudaGetLastError());
+  IFGF_CUDA(cudaStreamWaitEvent(caller, done, 0));
+  IFGF_CUDA(cudaEventSynchronize(done));
+  check_device_error(P);
+
+  if (rep) {
+    auto ms = [](const EventPair& e) {
+      float v = 0.f;
+      if (e.a && e.b) cudaEventElapsedTime(&v, e.a, e.b);
+      return 1e-3 * v;
+    };
+    rep->singular = ms(t_sing);
+    rep->level_d = ms(t_ld);
+    rep->interpolation = rep->propagation = 0.0;
+    for (int d = 3; d <= D; ++d) {
+      rep->interpolation += ms(t_int[d]);
+      if (d > 3) rep->propagation += ms(t_prop[d]);
+    }
+    rep->total = since(t0);
+    rep->depth = D;
+    rep->n = P->n;
+    rep->h_level_d = P->lv[D].h;
+    rep->n_levels = D - 2;
+    size_t peak = P->lv[D].nc;
+    for (int d = 3; d <= D; ++d) {
+      rep->level_boxes[d - 3] = P->lv[d].nb;
+      rep->level_cones[d - 3] = P->lv[d].nc;
+      if (d > 3) peak = std::max<size_t>(peak, P->lv[d].nc + P->lv[d - 1].nc);
+    }
+    rep->peak_live_blocks = peak;  // the reference's two-level figure (engine.cpp:280-308)
+    rep->setup = 0.0;
+    rep->gpu_launches = P->launches - launches0;
+  }
+}
+
+double2* stage_blocks(ifgf_plan* P, int d) {
+  if (d < 3 || d > P->depth) throw Error(IFGF_EINVAL, "level out of range");
+  if (!P->stage_blocks[d]) {
+    P->stage_blocks[d] = P->alloc<double2>((size_t)P->lv[d].nc * P->K.P + 1);
+    IFGF_CUDA(cudaMemsetAsync(P->stage_blocks[d], 0,
+                              ((size_t)P->lv[d].nc * P->K.P + 1) * sizeof(double2), P->s_main));
+  }
+  return P->stage_blocks[d];
+}
+
+template <class T>
+std::vector<T> d2h(const T* d, size_t count, cudaStream_t s) {
+  std::vector<T> h(count);
+  if (count) IFGF_CUDA(cudaMemcpyAsync(h.data(), d, count * sizeof(T), cudaMemcpyDeviceToHost, s));
+  IFGF_CUDA(cudaStreamSynchronize(s));
+  return h;
+}
+
+// dist.cpp:78-130 (partition), on host arrays of the level-D boxes.
+void partition_host(ifgf_plan* P, int R, uint32_t* box_begin, uint32_t* point_begin,
+                    uint32_t* cone_begin) {
+  if (R < 1) throw Error(IFGF_EINVAL, "partition: need at least one rank");
+  const Level& L = P->lv[P->depth];
+  const size_t nb = L.nb;
+  if ((size_t)R > nb)
+    throw Error(IFGF_EINVAL,
+                "partition: more ranks than relevant finest-level boxes (the smallest "
+                "distribution unit)");
+  const auto first = d2h(L.first, nb, P->s_main);
+  const auto count = d2h(L.count, nb, P->s_main);
+  const size_t npts = (size_t)first[nb - 1] + count[nb - 1];
+  box_begin[0] = point_begin[0] = 0;
+  uint32_t b = 0;
+  for (int r = 0; r < R - 1; ++r) {
+    const double target = static_cast<double>(npts) * (r + 1) / R;
+    const uint32_t max_end = (uint32_t)nb - (uint32_t)(R - 1 - r);
+    uint32_t e = b + 1;
+    while (e < max_end && static_cast<double>(first[e - 1] + count[e - 1]) < target) ++e;
+    box_begin[r + 1] = e;
+    point_begin[r + 1] = first[e - 1] + count[e - 1];
+    b = e;
+  }
+  box_begin[R] = (uint32_t)nb;
+  point_begin[R] = (uint32_t)npts;
+  if (cone_begin)
+    for (int d = 3; d <= P->depth; ++d) {
+      uint32_t* cb = cone_begin + (size_t)(d - 3) * (R + 1);
+      const size_t nc = P->lv[d].nc, base = nc / R, extra = nc % R;
+      cb[0] = 0;
+      for (int r = 0; r < R; ++r) cb[r + 1] = cb[r] + (uint32_t)(base + ((size_t)r < extra ? 1 : 0));
+    }
+}
+
+__device__ __forceinline__ int cone_owner(uint32_t q, uint32_t nc, int R) {
+  const uint32_t base = nc / R, extra = nc % R;
+  const uint32_t cut = extra * (base + 1);
+  return q < cut ? (int)(q / (base + 1)) : (int)(extra + (q - cut) / base);
+}
+
+// dist.cpp:179-201: cones of level d holding (via cone_of_point) the owned
+// points as seen from their cousins; foreign ones are flagged.
+__global__ void k_need_interp(const __grid_constant__ LevelDev L, const uint32_t* __restrict__ ptbox,
+                              const double* xs, const double* ys, const double* zs, uint32_t p0,
+                              uint32_t p1, int R, int rank, uint8_t* need, int* err) {
+  const uint32_t i = p0 + blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= p1) return;
+  const uint32_t b = ptbox[i];
+  for (uint32_t k = L.cous_off[b]; k < L.cous_off[b + 1]; ++k) {
+    const uint32_t cb = L.cous[k];
+    uint32_t g;
+    const int e = cone_of_point(L, L.cx[cb], L.cy[cb], L.cz[cb], xs[i], ys[i], zs[i], g);
+    if (e) {
+      raise_err(err, e);
+      return;
+    }
+    const uint32_t q = find_cone(L, cb, g);
+    if (q == 0xffffffffu) {
+      raise_err(err, kErrInterpCover);
+      return;
+    }
+    if (cone_owner(q, L.nc, R) != rank) need[q] = 1;
+  }
+}
+
+// dist.cpp:206-237: child cones of level d hit by the nodes of the owned
+// parent cones of level d-1.
+__global__ void k_need_prop(const __grid_constant__ LevelDev L, const __grid_constant__ LevelDev U,
+                            const __grid_constant__ InterpConsts K, uint32_t q0, uint32_t q1,
+                            int R, int rank, uint8_t* need, int* err) {
+  const size_t t = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
+  if (t >= (size_t)(q1 - q0) * K.P) return;
+  const uint32_t q = q0 + (uint32_t)(t / K.P);
+  const int m = (int)(t % K.P);
+  const int jp = m % K.pp, jt = (m / K.pp) % K.pt, js = m / (K.pp * K.pt);
+  const uint32_t pb = U.cone_box[q];
+  const SegMid sg = segment_mid(U, U.cone_gamma[q]);
+  double x, y, z;
+  node_position(sg, U.rad, U.cx[pb], U.cy[pb], U.cz[pb], K.ns[js], K.nt[jt], K.np[jp], x, y, z);
+  for (uint32_t cb = U.child_begin[pb]; cb < U.child_begin[pb + 1]; ++cb) {
+    uint32_t g;
+    const int e = cone_of_point(L, L.cx[cb], L.cy[cb], L.cz[cb], x, y, z, g);
+    if (e) {
+      raise_err(err, e);
+      return;
+    }
+    const uint32_t cq = find_cone(L, cb, g);
+    if (cq == 0xffffffffu) {
+      raise_err(err, kErrPropCover);
+      return;
+    }
+    if (cone_owner(cq, L.nc, R) != rank) need[cq] = 1;
+  }
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* ifgf_last_error(void) { return g_err.c_str(); }
+int ifgf_abi_version(void) { return IFGF_B200_ABI_VERSION; }
+
+void ifgf_default_params(ifgf_params* p) {
+  if (!p) return;
+  p->depth = 0;
+  p->box_lambda = 0.25;
+  p->points_per_box = 64;
+  p->base_s = 1;
+  p->base_theta = 2;
+  p->base_phi = 4;
+  p->p_s = 3;
+  p->p_theta = 5;
+  p->p_phi = 5;
+  p->device = 0;
+}
+
+int ifgf_device_ok(void) {
+  return guarded([] { require_device(0); }) == IFGF_OK ? 1 : 0;
+}
+
+int ifgf_choose_depth(size_t n, double side, double kappa, const ifgf_params* p, int* out) {
+  return guarded([&] {
+    if (!p || !out) throw Error(IFGF_EINVAL, "null argument");
+    int d;
+    if (p->depth > 0) {
+      d = p->depth;
+    } else if (kappa > 0.0) {
+      const double lambda = 2.0 * kPi / kappa;
+      const double ratio = side / (p->box_lambda * lambda);
+      d = 1 + static_cast<int>(std::floor(std::log2(std::max(ratio, 1.0)) + 1e-4));
+    } else {
+      const double boxes = static_cast<double>(n) / std::max(1, p->points_per_box);
+      d = 1 + static_cast<int>(std::ceil(0.5 * std::log2(std::max(boxes, 1.0)) - 1e-9));
+    }
+    *out = std::clamp(d, 3, 21);
+  });
+}
+
+int ifgf_plan_create_device(const double* dx, const double* dy, const double* dz, size_t n,
+                            int kind, double k, const ifgf_params* p, void* stream,
+                            ifgf_plan** out) {
+  return guarded([&] {
+    if (!out) throw Error(IFGF_EINVAL, "null output");
+    *out = nullptr;
+    ifgf_plan* P = new_plan(n, kind, k, p);
+    try {
+      cudaEvent_t e;
+      IFGF_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+      IFGF_CUDA(cudaEventRecord(e, static_cast<cudaStream_t>(stream)));
+      IFGF_CUDA(cudaStreamWaitEvent(P->s_main, e, 0));
+      cudaEventDestroy(e);
+      finish_create(P, dx, dy, dz);
+    } catch (...) {
+      plan_free(P);
+      throw;
+    }
+    *out = P;
+  });
+}
+
+int ifgf_plan_create(const double* x1, const double* x2, const double* x3, size_t n, int kind,
+                     double k, const ifgf_params* p, ifgf_plan** out) {
+  return guarded([&] {
+    if (!out) throw Error(IFGF_EINVAL, "null output");
+    *out = nullptr;
+    if (n >= 1 && (!x1 || !x2 || !x3)) throw Error(IFGF_EINVAL, "null coordinates");
+    const auto t0 = clk::now();
+    ifgf_plan* P = new_plan(n, kind, k, p);
+    try {
+      double* tmp = P->alloc<double>(3 * n);
+      IFGF_CUDA(cudaMemcpyAsync(tmp, x1, n * sizeof(double), cudaMemcpyHostToDevice, P->s_main));
+      IFGF_CUDA(cudaMemcpyAsync(tmp + n, x2, n * sizeof(double), cudaMemcpyHostToDevice, P->s_main));
+      IFGF_CUDA(
+          cudaMemcpyAsync(tmp + 2 * n, x3, n * sizeof(double), cudaMemcpyHostToDevice, P->s_main));
+      finish_create(P, tmp, tmp + n, tmp + 2 * n);
+      P->setup_seconds = since(t0);
+    } catch (...) {
+      plan_free(P);
+      throw;
+    }
+    *out = P;
+  });
+}
+
+void ifgf_plan_destroy(ifgf_plan* plan) { plan_free(plan); }
+
+int ifgf_plan_set_option(ifgf_plan* P, int option, int value) {
+  return guarded([&] {
+    if (!P) throw Error(IFGF_EINVAL, "null plan");
+    if (option == IFGF_OPT_SERIAL) P->serial = value != 0;
+    else throw Error(IFGF_EINVAL, "unknown option");
+  });
+}
+
+int ifgf_plan_apply_device(ifgf_plan* P, const double* a_re, const double* a_im, double* i_re,
+                           double* i_im, void* stream, ifgf_report* rep) {
+  return guarded([&] {
+    if (!P || !a_re || !i_re || !i_im) throw Error(IFGF_EINVAL, "null argument");
+    if (P->n < 2) throw Error(IFGF_EINVAL, "apply: need at least two points");
+    apply_device(P, a_re, a_im, i_re, i_im, static_cast<cudaStream_t>(stream), rep);
+  });
+}
+
+int ifgf_plan_apply(ifgf_plan* P, const double* a_re, const double* a_im, double* i_re,
+                    double* i_im, ifgf_report* rep) {
+  return guarded([&] {
+    if (!P || !a_re || !i_re || !i_im) throw Error(IFGF_EINVAL, "null argument");
+    if (P->n < 2) throw Error(IFGF_EINVAL, "apply: need at least two points");
+    const auto t0 = clk::now();
+    IFGF_CUDA(cudaSetDevice(P->device));
+    const size_t n = P->n;
+    double* buf = nullptr;
+    IFGF_CUDA(cudaMallocAsync(&buf, 4 * n * sizeof(double), P->s_main));
+    struct F {
+      double* b;
+      cudaStream_t s;
+      ~F() { cudaFreeAsync(b, s); }
+    } f{buf, P->s_main};
+    IFGF_CUDA(cudaMemcpyAsync(buf, a_re, n * sizeof(double), cudaMemcpyHostToDevice, P->s_main));
+    if (a_im)
+      IFGF_CUDA(
+          cudaMemcpyAsync(buf + n, a_im, n * sizeof(double), cudaMemcpyHostToDevice, P->s_main));
+    apply_device(P, buf, a_im ? buf + n : nullptr, buf + 2 * n, buf + 3 * n, P->s_main, rep);
+    IFGF_CUDA(
+        cudaMemcpyAsync(i_re, buf + 2 * n, n * sizeof(double), cudaMemcpyDeviceToHost, P->s_main));
+    IFGF_CUDA(
+        cudaMemcpyAsync(i_im, buf + 3 * n, n * sizeof(double), cudaMemcpyDeviceToHost, P->s_main));
+    IFGF_CUDA(cudaStreamSynchronize(P->s_main));
+    if (rep) rep->total = since(t0);
+  });
+}
+
+int ifgf_apply(size_t n, const double* x1, const double* x2, const double* x3, const double* a_re,
+               const double* a_im, int kind, double k, const ifgf_params* p, double* i_re,
+               double* i_im, ifgf_report* rep) {
+  // engine.cpp:260-325: rebuild, apply, return in the caller's order
+  if (n < 2) {
+    g_err = "apply: need at least two points";
+    return IFGF_EINVAL;
+  }
+  const auto t0 = clk::now();
+  ifgf_plan* P = nullptr;
+  int rc = ifgf_plan_create(x1, x2, x3, n, kind, k, p, &P);
+  if (rc) return rc;
+  rc = ifgf_plan_apply(P, a_re, a_im, i_re, i_im, rep);
+  const double setup = P->setup_seconds;
+  const size_t setup_launches = P->launches;
+  ifgf_plan_destroy(P);
+  if (rc == 0 && rep) {
+    rep->setup = setup;
+    rep->total = since(t0);
+    rep->gpu_launches = setup_launches;  // setup + apply kernels of this call
+  }
+  return rc;
+}
+
+int ifgf_plan_get_info(const ifgf_plan* P, ifgf_plan_info* info) {
+  return guarded([&] {
+    if (!P || !info) throw Error(IFGF_EINVAL, "null argument");
+    std::memset(info, 0, sizeof *info);
+    info->n = P->n;
+    info->depth = P->depth;
+    for (int c = 0; c < 3; ++c) info->cube_origin[c] = P->cube[c];
+    info->cube_side = P->cube[3];
+    info->kappa = P->kappa;
+    info->p_s = P->K.ps;
+    info->p_theta = P->K.pt;
+    info->p_phi = P->K.pp;
+    info->P = P->K.P;
+    for (int d = 1; d <= P->depth; ++d) {
+      const Level& L = P->lv[d];
+      info->boxes[d] = L.nb;
+      info->cones[d] = d >= 3 ? L.nc : 0;
+      info->cousin_entries[d] = d >= 3 ? L.n_cous : 0;
+      info->h[d] = L.h;
+    }
+    // neighbour totals need the counts
+    for (int d = 1; d <= P->depth; ++d) {
+      const auto cnt = d2h(P->lv[d].nbr_cnt, P->lv[d].nb, P->s_main);
+      size_t t = 0;
+      for (auto c : cnt) t += c;
+      info->nbr_entries[d] = t;
+    }
+    info->setup_seconds = P->setup_seconds;
+    info->device_bytes = P->bytes;
+  });
+}
+
+int ifgf_plan_export_perm(const ifgf_plan* P, uint32_t* perm) {
+  return guarded([&] {
+    if (!P || !perm) throw Error(IFGF_EINVAL, "null argument");
+    IFGF_CUDA(cudaMemcpy(perm, P->perm, P->n * sizeof(uint32_t), cudaMemcpyDeviceToHost));
+  });
+}
+
+int ifgf_plan_export_level(const ifgf_plan* Pc, int d, uint64_t* codes, uint32_t* first,
+                           uint32_t* count, double* centers3, uint32_t* parent,
+                           uint32_t* child_begin, uint32_t* nbr_off, uint32_t* nbr,
+                           uint32_t* cousin_off, uint32_t* cousin, uint32_t* cone_box,
+                           uint64_t* cone_gamma, uint32_t* box_cone_begin) {
+  return guarded([&] {
+    ifgf_plan* P = const_cast<ifgf_plan*>(Pc);
+    if (!P) throw Error(IFGF_EINVAL, "null plan");
+    if (d < 1 || d > P->depth) throw Error(IFGF_EINVAL, "level out of range");
+    const Level& L = P->lv[d];
+    cudaStream_t s = P->s_main;
+    const size_t nb = L.nb;
+    auto cp = [&](void* dst, const void* src, size_t bytes) {
+      if (dst && src && bytes)
+        IFGF_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, s));
+    };
+    cp(codes, L.code, nb * 8);
+    cp(first, L.first, nb * 4);
+    cp(count, L.count, nb * 4);
+    cp(parent, L.parent, nb * 4);
+    if (d < P->depth) cp(child_begin, L.child_begin, (nb + 1) * 4);
+    if (centers3) {
+      const auto x = d2h(L.cx, nb, s), y = d2h(L.cy, nb, s), z = d2h(L.cz, nb, s);
+      for (size_t b = 0; b < nb; ++b) {
+        centers3[3 * b] = x[b];
+        centers3[3 * b + 1] = y[b];
+        centers3[3 * b + 2] = z[b];
+      }
+    }
+    if (nbr_off || nbr) {
+      const auto cnt = d2h(L.nbr_cnt, nb, s);
+      const auto all = d2h(L.nbr, nb * 27, s);
+      size_t o = 0;
+      for (size_t b = 0; b < nb; ++b) {
+        if (nbr_off) nbr_off[b] = (uint32_t)o;
+        for (uint32_t a = 0; a < cnt[b]; ++a, ++o)
+          if (nbr) nbr[o] = all[b * 27 + a];
+      }
+      if (nbr_off) nbr_off[nb] = (uint32_t)o;
+    }
+    if (d >= 3) {
+      cp(cousin_off, L.cous_off, (nb + 1) * 4);
+      cp(cousin, L.cous, L.n_cous * 4);
+      cp(cone_box, L.cone_box, (size_t)L.nc * 4);
+      cp(box_cone_begin, L.box_cone, (nb + 1) * 4);
+      if (cone_gamma) {
+        const auto g = d2h(L.cone_gamma, L.nc, s);
+        for (size_t q = 0; q < L.nc; ++q) cone_gamma[q] = g[q];
+      }
+    }
+    IFGF_CUDA(cudaStreamSynchronize(s));
+  });
+}
+
+int ifgf_plan_set_density(ifgf_plan* P, const double* a_re, const double* a_im) {
+  return guarded([&] {
+    if (!P || !a_re) throw Error(IFGF_EINVAL, "null argument");
+    IFGF_CUDA(cudaSetDevice(P->device));
+    const size_t n = P->n;
+    double* buf = P->alloc<double>(2 * n);
+    IFGF_CUDA(cudaMemcpyAsync(buf, a_re, n * 8, cudaMemcpyHostToDevice, P->s_main));
+    if (a_im) IFGF_CUDA(cudaMemcpyAsync(buf + n, a_im, n * 8, cudaMemcpyHostToDevice, P->s_main));
+    // gather without touching the result buffer
+    double* ir = P->ir;
+    double* ii = P->ii;
+    P->ir = P->ii = nullptr;
+    launch_gather_density(P, buf, a_im ? buf + n : nullptr, P->s_main);
+    P->ir = ir;
+    P->ii = ii;
+    IFGF_CUDA(cudaStreamSynchronize(P->s_main));
+  });
+}
+
+int ifgf_plan_zero_result(ifgf_plan* P) {
+  return guarded([&] {
+    if (!P) throw Error(IFGF_EINVAL, "null plan");
+    IFGF_CUDA(cudaMemsetAsync(P->ir, 0, P->n * 8, P->s_main));
+    IFGF_CUDA(cudaMemsetAsync(P->ii, 0, P->n * 8, P->s_main));
+    IFGF_CUDA(cudaStreamSynchronize(P->s_main));
+  });
+}
+
+int ifgf_plan_singular_pass(ifgf_plan* P, size_t b, size_t e) {
+  return guarded([&] {
+    if (!P) throw Error(IFGF_EINVAL, "null plan");
+    if (b > e || e > P->n) throw Error(IFGF_EINVAL, "point range out of bounds");
+    launch_singular(P, b, e, P->s_main);
+    IFGF_CUDA(cudaGetLastError());
+    check_device_error(P);
+  });
+}
+
+int ifgf_plan_level_d_pass(ifgf_plan* P, uint32_t qb, uint32_t qe) {
+  return guarded([&] {
+    if (!P) throw Error(IFGF_EINVAL, "null plan");
+    if (qb > qe || qe > P->lv[P->depth].nc) throw Error(IFGF_EINVAL, "cone range out of bounds");
+    launch_level_d(P, qb, qe, stage_blocks(P, P->depth), P->s_main);
+    IFGF_CUDA(cudaGetLastError());
+    check_device_error(P);
+  });
+}
+
+int ifgf_plan_propagation_pass(ifgf_plan* P, int d, uint32_t qb, uint32_t qe) {
+  return guarded([&] {
+    if (!P) throw Error(IFGF_EINVAL, "null plan");
+    if (d < 4 || d > P->depth) throw Error(IFGF_EINVAL, "propagation level out of range");
+    if (qb > qe || qe > P->lv[d - 1].nc) throw Error(IFGF_EINVAL, "cone range out of bounds");
+    double2* child = stage_blocks(P, d);
+    double2* parent = stage_blocks(P, d - 1);
+    launch_propagation(P, d, qb, qe, child, parent, P->s_main);
+    IFGF_CUDA(cudaGetLastError());
+    check_device_error(P);
+  });
+}
+
+int ifgf_plan_interpolation_pass(ifgf_plan* P, int d, size_t b, size_t e) {
+  return guarded([&] {
+    if (!P) throw Error(IFGF_EINVAL, "null plan");
+    if (d < 3 || d > P->depth) throw Error(IFGF_EINVAL, "level out of range");
+    if (b > e || e > P->n) throw Error(IFGF_EINVAL, "point range out of bounds");
+    launch_interpolation(P, d, b, e, stage_blocks(P, d), P->s_main);
+    IFGF_CUDA(cudaGetLastError());
+    check_device_error(P);
+  });
+}
+
+int ifgf_plan_read_blocks(ifgf_plan* P, int d, double* re, double* im) {
+  return guarded([&] {
+    if (!P || !re || !im) throw Error(IFGF_EINVAL, "null argument");
+    const double2* blk = stage_blocks(P, d);
+    const size_t cnt = (size_t)P->lv[d].nc * P->K.P;
+    const auto h = d2h(blk, cnt, P->s_main);
+    for (size_t k = 0; k < cnt; ++k) {
+      re[k] = h[k].x;
+      im[k] = h[k].y;
+    }
+  });
+}
+
+int ifgf_plan_write_blocks(ifgf_plan* P, int d, const double* re, const double* im) {
+  return guarded([&] {
+    if (!P || !re || !im) throw Error(IFGF_EINVAL, "null argument");
+    double2* blk = stage_blocks(P, d);
+    const size_t cnt = (size_t)P->lv[d].nc * P->K.P;
+    std::vector<double2> h(cnt);
+    for (size_t k = 0; k < cnt; ++k) h[k] = make_double2(re[k], im[k]);
+    IFGF_CUDA(cudaMemcpyAsync(blk, h.data(), cnt * sizeof(double2), cudaMemcpyHostToDevice,
+                              P->s_main));
+    IFGF_CUDA(cudaStreamSynchronize(P->s_main));
+  });
+}
+
+int ifgf_plan_read_result(ifgf_plan* P, int sorted, double* i_re, double* i_im) {
+  return guarded([&] {
+    if (!P || !i_re || !i_im) throw Error(IFGF_EINVAL, "null argument");
+    const size_t n = P->n;
+    if (sorted) {
+      IFGF_CUDA(cudaMemcpyAsync(i_re, P->ir, n * 8, cudaMemcpyDeviceToHost, P->s_main));
+      IFGF_CUDA(cudaMemcpyAsync(i_im, P->ii, n * 8, cudaMemcpyDeviceToHost, P->s_main));
+      IFGF_CUDA(cudaStreamSynchronize(P->s_main));
+      return;
+    }
+    double* buf = P->alloc<double>(2 * n);
+    launch_scatter_result(P, buf, buf + n, P->s_main);
+    IFGF_CUDA(cudaMemcpyAsync(i_re, buf, n * 8, cudaMemcpyDeviceToHost, P->s_main));
+    IFGF_CUDA(cudaMemcpyAsync(i_im, buf + n, n * 8, cudaMemcpyDeviceToHost, P->s_main));
+    IFGF_CUDA(cudaStreamSynchronize(P->s_main));
+  });
+}
+
+int ifgf_plan_pack_blocks(ifgf_plan* P, int d, const uint32_t* d_cones, size_t m, double* d_buf,
+                          void* stream) {
+  return guarded([&] {
+    if (!P) throw Error(IFGF_EINVAL, "null plan");
+    double2* blk = P->n_slots ? P->slots[d] : stage_blocks(P, d);
+    launch_pack(P, blk, d_cones, m, d_buf, 0, nullptr, static_cast<cudaStream_t>(stream));
+    IFGF_CUDA(cudaGetLastError());
+  });
+}
+
+int ifgf_plan_unpack_blocks(ifgf_plan* P, int d, const uint32_t* d_cones, size_t m,
+                            const double* d_buf, void* stream) {
+  return guarded([&] {
+    if (!P) throw Error(IFGF_EINVAL, "null plan");
+    double2* blk = P->n_slots ? P->slots[d] : stage_blocks(P, d);
+    launch_pack(P, nullptr, d_cones, m, const_cast<double*>(d_buf), 1, blk,
+                static_cast<cudaStream_t>(stream));
+    IFGF_CUDA(cudaGetLastError());
+  });
+}
+
+int ifgf_plan_partition(const ifgf_plan* P, int R, uint32_t* box_begin, uint32_t* point_begin,
+                        uint32_t* cone_begin) {
+  return guarded([&] {
+    if (!P || !box_begin || !point_begin) throw Error(IFGF_EINVAL, "null argument");
+    partition_host(const_cast<ifgf_plan*>(P), R, box_begin, point_begin, cone_begin);
+  });
+}
+
+int ifgf_plan_exchange_set(ifgf_plan* P, int R, int rank, int d, int kind, uint32_t* cones,
+                           size_t* count) {
+  return guarded([&] {
+    if (!P || !count) throw Error(IFGF_EINVAL, "null argument");
+    if (rank < 0 || rank >= R) throw Error(IFGF_EINVAL, "rank out of range");
+    if (d < 3 || d > P->depth || (kind == 1 && d < 4) || kind < 0 || kind > 1)
+      throw Error(IFGF_EINVAL, "bad level or kind");
+    std::vector<uint32_t> bb(R + 1), pb(R + 1), cb((size_t)(P->depth - 2) * (R + 1));
+    partition_host(P, R, bb.data(), pb.data(), cb.data());
+    const Level& L = P->lv[d];
+    uint8_t* need = P->alloc<uint8_t>(L.nc + 1);
+    IFGF_CUDA(cudaMemsetAsync(need, 0, L.nc + 1, P->s_main));
+    if (kind == 0) {
+      const uint32_t p0 = pb[rank], p1 = pb[rank + 1];
+      if (p1 > p0)
+        k_need_interp<<<(p1 - p0 + 127) / 128, 128, 0, P->s_main>>>(
+            L.dev(), L.ptbox, P->xs, P->ys, P->zs, p0, p1, R, rank, need, P->err);
+    } else {
+      const uint32_t* own = cb.data() + (size_t)(d - 4) * (R + 1);
+      const uint32_t q0 = own[rank], q1 = own[rank + 1];
+      const size_t work = (size_t)(q1 - q0) * P->K.P;
+      if (work)
+        k_need_prop<<<(unsigned)((work + 127) / 128), 128, 0, P->s_main>>>(
+            L.dev(), P->lv[d - 1].dev(), P->K, q0, q1, R, rank, need, P->err);
+    }
+    IFGF_CUDA(cudaGetLastError());
+    check_device_error(P);
+    const auto h = d2h(need, L.nc, P->s_main);
+    size_t k = 0;
+    for (size_t q = 0; q < L.nc; ++q)
+      if (h[q]) {
+        if (cones) cones[k] = (uint32_t)q;
+        ++k;
+      }
+    *count = k;
+  });
+}
+
+int ifgf_direct_eval(size_t n, const double* x1, const double* x2, const double* x3,
+                     const double* a_re, const double* a_im, int kind, double k,
+                     const uint32_t* targets, size_t m, int device, double* o_re, double* o_im) {
+  return guarded([&] {
+    if (n < 2) throw Error(IFGF_EINVAL, "direct_eval: need at least two points");
+    require_device(device);
+    const size_t cnt = targets ? m : n;
+    for (size_t j = 0; targets && j < m; ++j)
+      if (targets[j] >= n) throw Error(IFGF_EINVAL, "target index out of range");
+    const double kappa = kind == IFGF_LAPLACE ? 0.0 : k;
+    cudaStream_t s;
+    IFGF_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+    double* buf = nullptr;
+    uint32_t* tg = nullptr;
+    IFGF_CUDA(cudaMallocAsync(&buf, (5 * n + 2 * cnt) * sizeof(double), s));
+    IFGF_CUDA(cudaMemcpyAsync(buf, x1, n * 8, cudaMemcpyHostToDevice, s));
+    IFGF_CUDA(cudaMemcpyAsync(buf + n, x2, n * 8, cudaMemcpyHostToDevice, s));
+    IFGF_CUDA(cudaMemcpyAsync(buf + 2 * n, x3, n * 8, cudaMemcpyHostToDevice, s));
+    IFGF_CUDA(cudaMemcpyAsync(buf + 3 * n, a_re, n * 8, cudaMemcpyHostToDevice, s));
+    if (a_im) IFGF_CUDA(cudaMemcpyAsync(buf + 4 * n, a_im, n * 8, cudaMemcpyHostToDevice, s));
+    else IFGF_CUDA(cudaMemsetAsync(buf + 4 * n, 0, n * 8, s));
+    if (targets) {
+      IFGF_CUDA(cudaMallocAsync(&tg, m * 4, s));
+      IFGF_CUDA(cudaMemcpyAsync(tg, targets, m * 4, cudaMemcpyHostToDevice, s));
+    }
+    double* o = buf + 5 * n;
+    direct_sums(buf, buf + n, buf + 2 * n, buf + 3 * n, buf + 4 * n, n, kappa, tg, cnt, o,
+                o + cnt, s);
+    IFGF_CUDA(cudaMemcpyAsync(o_re, o, cnt * 8, cudaMemcpyDeviceToHost, s));
+    IFGF_CUDA(cudaMemcpyAsync(o_im, o + cnt, cnt * 8, cudaMemcpyDeviceToHost, s));
+    IFGF_CUDA(cudaFreeAsync(buf, s));
+    if (tg) IFGF_CUDA(cudaFreeAsync(tg, s));
+    IFGF_CUDA(cudaStreamSynchronize(s));
+    cudaStreamDestroy(s);
+  });
+}
+
+int ifgf_sample_indices(size_t n, size_t m, uint64_t seed, uint32_t* out) {
+  // engine.cpp:341-352: partial Fisher-Yates with mt19937_64(seed)
+  return guarded([&] {
+    if (m > n) throw Error(IFGF_EINVAL, "sample_indices: m > n");
+    std::vector<uint32_t> idx(n);
+    for (size_t i = 0; i < n; ++i) idx[i] = (uint32_t)i;
+    std::mt19937_64 rng(seed);
+    for (size_t j = 0; j < m; ++j) {
+      const size_t k = j + static_cast<size_t>(rng() % (n - j));
+      std::swap(idx[j], idx[k]);
+    }
+    std::memcpy(out, idx.data(), m * sizeof(uint32_t));
+  });
+}
+
+int ifgf_error_at_indices(size_t n, const double* x1, const double* x2, const double* x3,
+                          const double* a_re, const double* a_im, const double* i_re,
+                          const double* i_im, int kind, double k, const uint32_t* idx, size_t m,
+                          int device, double* eps) {
+  // engine.cpp:354-376 with the exact sums on the device
+  std::vector<double> dre(m ? m : 1), dim(m ? m : 1);
+  const int rc = ifgf_direct_eval(n, x1, x2, x3, a_re, a_im, kind, k, idx, m, device, dre.data(),
+                                  dim.data());
+  if (rc) return rc;
+  return guarded([&] {
+    double num = 0.0, den = 0.0;
+    for (size_t j = 0; j < m; ++j) {
+      const double er = dre[j] - i_re[idx[j]], ei = dim[j] - i_im[idx[j]];
+      num += er * er + ei * ei;
+      den += dre[j] * dre[j] + dim[j] * dim[j];
+    }
+    if (den == 0.0) throw Error(IFGF_EDOMAIN, "estimate_error: zero reference norm");
+    *eps = std::sqrt(num / den);
+  });
+}
+
+}  // extern "C"

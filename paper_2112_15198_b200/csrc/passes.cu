@@ -1,0 +1,374 @@
+// passes.cu -- the four IFGF passes of ifgf::apply (engine.cpp:233-325) as
+// sm_100a kernels, FP64 throughout.
+//
+//   K1 k_singular     singular_pass + green_sum       engine.cpp:233-258, kernels_scalar.cpp:12-30
+//   K2 k_level_d      eval_level_d + factored_sum     engine.cpp:107-136, kernels_scalar.cpp:32-52
+//                     + cheb_fit                      interp.cpp:68-91
+//   K3 k_propagate    propagation_pass                engine.cpp:138-189
+//   K4 k_interp       interpolation_pass              engine.cpp:191-231
+//   K6 gather/scatter density gather, apply tail     engine.cpp:312-315
+//
+// Every work item writes only its own output slot, in a fixed order, so the
+// result is bitwise reproducible run to run (parallel.hpp:17-19 contract).
+#include "plan.hpp"
+
+namespace ifgf_b200 {
+namespace {
+
+template <int A, int B, int C>
+struct Orders {
+  static constexpr int PS = A, PT = B, PP = C, P = A * B * C;
+};
+
+// Interpolation orders instantiated in this build (the hot default first).
+#define IFGF_FOR_ORDERS(X) \
+  X(3, 5, 5) X(4, 6, 6) X(5, 7, 7) X(1, 1, 1) X(2, 2, 2) X(3, 3, 3) X(4, 4, 4) X(2, 3, 3) X(3, 4, 4)
+
+template <class F>
+bool dispatch_orders(int ps, int pt, int pp, F&& f) {
+#define IFGF_CASE(a, b, c)                 \
+  if (ps == a && pt == b && pp == c) {     \
+    f(Orders<a, b, c>{});                  \
+    return true;                           \
+  }
+  IFGF_FOR_ORDERS(IFGF_CASE)
+#undef IFGF_CASE
+  return false;
+}
+
+inline unsigned blocks_for(size_t n, int t) { return (unsigned)((n + t - 1) / t); }
+
+// ---------------------------------------------------------------- K1 near field
+template <bool LAP>
+__global__ void __launch_bounds__(128) k_singular(const __grid_constant__ LevelDev L, const uint32_t* __restrict__ ptbox,
+                                                  const double* __restrict__ xs,
+                                                  const double* __restrict__ ys,
+                                                  const double* __restrict__ zs,
+                                                  const double* __restrict__ ar,
+                                                  const double* __restrict__ ai, double kappa,
+                                                  size_t b0, size_t e0, double* ir, double* ii) {
+  const size_t i = b0 + blockIdx.x * (size_t)blockDim.x + threadIdx.x;
+  if (i >= e0) return;
+  const uint32_t b = ptbox[i];
+  const double tx = xs[i], ty = ys[i], tz = zs[i];
+  double sr = 0.0, si = 0.0;
+  const uint32_t nn = L.nbr_cnt[b];
+  for (uint32_t a = 0; a < nn; ++a) {
+    const uint32_t o = L.nbr[(size_t)b * 27 + a];
+    const uint32_t f = L.first[o], e = f + L.count[o];
+    for (uint32_t m = f; m < e; ++m) {
+      if (m == i) continue;
+      const double dx = tx - __ldg(&xs[m]), dy = ty - __ldg(&ys[m]), dz = tz - __ldg(&zs[m]);
+      const double r2 = fma(dz, dz, fma(dy, dy, dx * dx));
+      const double rinv = rsqrt(r2);
+      const double inv = kQuarterInvPi * rinv;
+      const double a_r = __ldg(&ar[m]), a_i = __ldg(&ai[m]);
+      if (LAP) {
+        sr = fma(a_r, inv, sr);
+        si = fma(a_i, inv, si);
+      } else {
+        double sn, cs;
+        sincos_fast(kappa * (r2 * rinv), sn, cs);
+        const double gr = cs * inv, gi = sn * inv;
+        sr = fma(a_r, gr, fma(-a_i, gi, sr));
+        si = fma(a_r, gi, fma(a_i, gr, si));
+      }
+    }
+  }
+  ir[i] += sr;
+  ii[i] += si;
+}
+
+// ------------------------------------------------------- K2 level-D seeding
+template <int PS, int PT, int PP, bool LAP>
+__global__ void __launch_bounds__(320)
+    k_level_d(const __grid_constant__ LevelDev L, const __grid_constant__ InterpConsts K, const double* __restrict__ xs,
+              const double* __restrict__ ys, const double* __restrict__ zs,
+              const double* __restrict__ ar, const double* __restrict__ ai, double kappa,
+              uint32_t qb, uint32_t qe, int cpb, double2* out, int* err) {
+  constexpr int P = PS * PT * PP;
+  extern __shared__ double2 smem[];
+  double2* sv = smem;
+  double2* st = smem + cpb * P;
+  const uint32_t q0 = qb + blockIdx.x * cpb;
+  const int ncon = (int)min((uint32_t)cpb, qe - q0);
+  const int c = threadIdx.x / P, m = threadIdx.x % P;
+  if (c < ncon) {
+    const uint32_t q = q0 + c;
+    const uint32_t b = L.cone_box[q];
+    const int jp = m % PP, jt = (m / PP) % PT, js = m / (PP * PT);
+    const SegMid sg = segment_mid(L, L.cone_gamma[q]);
+    const double cx = L.cx[b], cy = L.cy[b], cz = L.cz[b];
+    double tx, ty, tz;
+    node_position(sg, L.rad, cx, cy, cz, K.ns[js], K.nt[jt], K.np[jp], tx, ty, tz);
+    const double ux = tx - cx, uy = ty - cy, uz = tz - cz;
+    const double rc = sqrt(fma(uz, uz, fma(uy, uy, ux * ux)));
+    double sr = 0.0, si = 0.0;
+    const uint32_t f = L.first[b], e = f + L.count[b];
+    for (uint32_t j = f; j < e; ++j) {
+      const double dx = tx - __ldg(&xs[j]), dy = ty - __ldg(&ys[j]), dz = tz - __ldg(&zs[j]);
+      const double r2 = fma(dz, dz, fma(dy, dy, dx * dx));
+      const double rinv = rsqrt(r2);
+      const double ratio = rc * rinv;
+      const double a_r = __ldg(&ar[j]), a_i = __ldg(&ai[j]);
+      if (LAP) {
+        sr = fma(a_r, ratio, sr);
+        si = fma(a_i, ratio, si);
+      } else {
+        double sn, cs;
+        sincos_fast(kappa * (r2 * rinv - rc), sn, cs);
+        const double gr = cs * ratio, gi = sn * ratio;
+        sr = fma(a_r, gr, fma(-a_i, gi, sr));
+        si = fma(a_r, gi, fma(a_i, gr, si));
+      }
+    }
+    sv[c * P + m] = make_double2(sr, si);
+  }
+  __syncthreads();
+  fit_cones<PS, PT, PP>(K, sv, st, ncon, out + (size_t)q0 * P, err);
+}
+
+// ------------------------------------------------------------ K3 propagation
+template <int PS, int PT, int PP, bool LAP>
+__global__ void __launch_bounds__(320)
+    k_propagate(const __grid_constant__ LevelDev U, const __grid_constant__ LevelDev L,
+                const __grid_constant__ InterpConsts K, double kappa, uint32_t qb, uint32_t qe,
+                int cpb, const double2* __restrict__ child, double2* parent, int* err) {
+  constexpr int P = PS * PT * PP;
+  extern __shared__ double2 smem[];
+  double2* sv = smem;
+  double2* st = smem + cpb * P;
+  const uint32_t q0 = qb + blockIdx.x * cpb;
+  const int ncon = (int)min((uint32_t)cpb, qe - q0);
+  const int c = threadIdx.x / P, m = threadIdx.x % P;
+  if (c < ncon) {
+    const uint32_t q = q0 + c;
+    const uint32_t pb = U.cone_box[q];
+    const int jp = m % PP, jt = (m / PP) % PT, js = m / (PP * PT);
+    const SegMid sg = segment_mid(U, U.cone_gamma[q]);
+    const double pcx = U.cx[pb], pcy = U.cy[pb], pcz = U.cz[pb];
+    double x, y, z;
+    node_position(sg, U.rad, pcx, pcy, pcz, K.ns[js], K.nt[jt], K.np[jp], x, y, z);
+    const double rp = norm_rn(x - pcx, y - pcy, z - pcz);
+    double acr = 0.0, aci = 0.0;
+    const uint32_t c0 = U.child_begin[pb], c1 = U.child_begin[pb + 1];
+    for (uint32_t cb = c0; cb < c1; ++cb) {
+      Loc o;
+      const int e = locate(L, L.cx[cb], L.cy[cb], L.cz[cb], x, y, z, o);
+      if (e) {
+        raise_err(err, e);
+        break;
+      }
+      const uint32_t cq = find_cone(L, cb, o.gamma);
+      if (cq == 0xffffffffu) {
+        raise_err(err, kErrPropCover);
+        break;
+      }
+      double vr, vi;
+      eval_block<PS, PT, PP>(child + (size_t)cq * P, o.ts, o.tt, o.tp, vr, vi);
+      const double ratio = rp / o.r;
+      if (LAP) {
+        acr = fma(vr, ratio, acr);
+        aci = fma(vi, ratio, aci);
+      } else {
+        double sn, cn;
+        sincos_fast(kappa * (o.r - rp), sn, cn);
+        const double tr = ratio * cn, ti = ratio * sn;
+        acr = fma(vr, tr, fma(-vi, ti, acr));
+        aci = fma(vr, ti, fma(vi, tr, aci));
+      }
+    }
+    sv[c * P + m] = make_double2(acr, aci);
+  }
+  __syncthreads();
+  fit_cones<PS, PT, PP>(K, sv, st, ncon, parent + (size_t)q0 * P, err);
+}
+
+// ---------------------------------------------------------- K4 interpolation
+template <int PS, int PT, int PP, bool LAP>
+__global__ void __launch_bounds__(128)
+    k_interp(const __grid_constant__ LevelDev L, const uint32_t* __restrict__ ptbox, const double* __restrict__ xs,
+             const double* __restrict__ ys, const double* __restrict__ zs, double kappa,
+             size_t b0, size_t e0, const double2* __restrict__ blocks, double* ir, double* ii,
+             int* err) {
+  constexpr int P = PS * PT * PP;
+  const size_t i = b0 + blockIdx.x * (size_t)blockDim.x + threadIdx.x;
+  if (i >= e0) return;
+  const uint32_t b = ptbox[i];
+  const double x = xs[i], y = ys[i], z = zs[i];
+  double acr = 0.0, aci = 0.0;
+  const uint32_t k0 = L.cous_off[b], k1 = L.cous_off[b + 1];
+  for (uint32_t k = k0; k < k1; ++k) {
+    const uint32_t cb = L.cous[k];
+    Loc o;
+    const int e = locate(L, L.cx[cb], L.cy[cb], L.cz[cb], x, y, z, o);
+    if (e) {
+      raise_err(err, e);
+      return;
+    }
+    const uint32_t q = find_cone(L, cb, o.gamma);
+    if (q == 0xffffffffu) {
+      raise_err(err, kErrInterpCover);
+      return;
+    }
+    double vr, vi;
+    eval_block<PS, PT, PP>(blocks + (size_t)q * P, o.ts, o.tt, o.tp, vr, vi);
+    const double inv = kQuarterInvPi / o.r;
+    if (LAP) {
+      acr = fma(vr, inv, acr);
+      aci = fma(vi, inv, aci);
+    } else {
+      double sn, cn;
+      sincos_fast(kappa * o.r, sn, cn);
+      const double gr = cn * inv, gi = sn * inv;
+      acr = fma(vr, gr, fma(-vi, gi, acr));
+      aci = fma(vr, gi, fma(vi, gr, aci));
+    }
+  }
+  ir[i] += acr;
+  ii[i] += aci;
+}
+
+// --------------------------------------------------------------- K6 permutes
+__global__ void k_gather_density(const uint32_t* __restrict__ perm, const double* __restrict__ a_re,
+                                 const double* __restrict__ a_im, size_t n, double* ar, double* ai,
+                                 double* ir, double* ii) {
+  const size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const uint32_t j = perm[i];
+  ar[i] = a_re[j];
+  ai[i] = a_im ? a_im[j] : 0.0;
+  if (ir) {
+    ir[i] = 0.0;
+    ii[i] = 0.0;
+  }
+}
+
+__global__ void k_scatter_result(const uint32_t* __restrict__ perm, const double* __restrict__ ir,
+                                 const double* __restrict__ ii, size_t n, double* o_re,
+                                 double* o_im) {
+  const size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const uint32_t j = perm[i];
+  o_re[j] = ir[i];
+  o_im[j] = ii[i];
+}
+
+__global__ void k_pack(const double2* __restrict__ blocks, const uint32_t* __restrict__ cones,
+                       size_t m, int P, double2* buf, int unpack, double2* blocks_out) {
+  const size_t t = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
+  if (t >= m * P) return;
+  const size_t j = t / P, k = t % P;
+  const size_t g = (size_t)cones[j] * P + k;
+  if (unpack) blocks_out[g] = buf[t];
+  else buf[t] = blocks[g];
+}
+
+inline int cones_per_cta(int P) {
+  int c = 320 / P;
+  if (c < 1) c = 1;
+  while (c > 1 && ((c * P + 31) / 32) * 32 > 320) --c;
+  return c;
+}
+
+inline unsigned threads_for(int cpb, int P) { return (unsigned)(((cpb * P + 31) / 32) * 32); }
+
+}  // namespace
+
+bool orders_supported(int ps, int pt, int pp) {
+  return dispatch_orders(ps, pt, pp, [](auto) {});
+}
+
+void launch_gather_density(ifgf_plan* P, const double* a_re, const double* a_im, cudaStream_t s) {
+  k_gather_density<<<blocks_for(P->n, 256), 256, 0, s>>>(P->perm, a_re, a_im, P->n, P->ar, P->ai,
+                                                         P->ir, P->ii);
+  ++P->launches;
+}
+
+void launch_scatter_result(ifgf_plan* P, double* o_re, double* o_im, cudaStream_t s) {
+  k_scatter_result<<<blocks_for(P->n, 256), 256, 0, s>>>(P->perm, P->ir, P->ii, P->n, o_re, o_im);
+  ++P->launches;
+}
+
+void launch_singular(ifgf_plan* P, size_t b, size_t e, cudaStream_t s) {
+  if (e <= b) return;
+  const Level& L = P->lv[P->depth];
+  const unsigned g = blocks_for(e - b, 128);
+  if (P->kappa == 0.0)
+    k_singular<true><<<g, 128, 0, s>>>(L.dev(), L.ptbox, P->xs, P->ys, P->zs, P->ar, P->ai,
+                                       P->kappa, b, e, P->ir, P->ii);
+  else
+    k_singular<false><<<g, 128, 0, s>>>(L.dev(), L.ptbox, P->xs, P->ys, P->zs, P->ar, P->ai,
+                                        P->kappa, b, e, P->ir, P->ii);
+  ++P->launches;
+}
+
+void launch_level_d(ifgf_plan* P, uint32_t qb, uint32_t qe, double2* out, cudaStream_t s) {
+  if (qe <= qb) return;
+  const Level& L = P->lv[P->depth];
+  const InterpConsts& K = P->K;
+  dispatch_orders(K.ps, K.pt, K.pp, [&](auto o) {
+    using O = decltype(o);
+    const int cpb = cones_per_cta(O::P);
+    const unsigned grid = blocks_for(qe - qb, cpb);
+    const size_t smem = 2 * (size_t)cpb * O::P * sizeof(double2);
+    if (P->kappa == 0.0)
+      k_level_d<O::PS, O::PT, O::PP, true><<<grid, threads_for(cpb, O::P), smem, s>>>(
+          L.dev(), K, P->xs, P->ys, P->zs, P->ar, P->ai, P->kappa, qb, qe, cpb, out, P->err);
+    else
+      k_level_d<O::PS, O::PT, O::PP, false><<<grid, threads_for(cpb, O::P), smem, s>>>(
+          L.dev(), K, P->xs, P->ys, P->zs, P->ar, P->ai, P->kappa, qb, qe, cpb, out, P->err);
+  });
+  ++P->launches;
+}
+
+void launch_propagation(ifgf_plan* P, int d, uint32_t qb, uint32_t qe, const double2* child,
+                        double2* parent, cudaStream_t s) {
+  if (qe <= qb) return;
+  const Level& U = P->lv[d - 1];
+  const Level& L = P->lv[d];
+  const InterpConsts& K = P->K;
+  dispatch_orders(K.ps, K.pt, K.pp, [&](auto o) {
+    using O = decltype(o);
+    const int cpb = cones_per_cta(O::P);
+    const unsigned grid = blocks_for(qe - qb, cpb);
+    const size_t smem = 2 * (size_t)cpb * O::P * sizeof(double2);
+    if (P->kappa == 0.0)
+      k_propagate<O::PS, O::PT, O::PP, true><<<grid, threads_for(cpb, O::P), smem, s>>>(
+          U.dev(), L.dev(), K, P->kappa, qb, qe, cpb, child, parent, P->err);
+    else
+      k_propagate<O::PS, O::PT, O::PP, false><<<grid, threads_for(cpb, O::P), smem, s>>>(
+          U.dev(), L.dev(), K, P->kappa, qb, qe, cpb, child, parent, P->err);
+  });
+  ++P->launches;
+}
+
+void launch_interpolation(ifgf_plan* P, int d, size_t b, size_t e, const double2* blocks,
+                          cudaStream_t s) {
+  if (e <= b) return;
+  const Level& L = P->lv[d];
+  const InterpConsts& K = P->K;
+  const unsigned g = blocks_for(e - b, 128);
+  dispatch_orders(K.ps, K.pt, K.pp, [&](auto o) {
+    using O = decltype(o);
+    if (P->kappa == 0.0)
+      k_interp<O::PS, O::PT, O::PP, true><<<g, 128, 0, s>>>(
+          L.dev(), L.ptbox, P->xs, P->ys, P->zs, P->kappa, b, e, blocks, P->ir, P->ii, P->err);
+    else
+      k_interp<O::PS, O::PT, O::PP, false><<<g, 128, 0, s>>>(
+          L.dev(), L.ptbox, P->xs, P->ys, P->zs, P->kappa, b, e, blocks, P->ir, P->ii, P->err);
+  });
+  ++P->launches;
+}
+
+void launch_pack(ifgf_plan* P, const double2* blocks, const uint32_t* cones, size_t m,
+                 double* buf, int unpack, double2* blocks_out, cudaStream_t s) {
+  if (!m) return;
+  const int Pn = P->K.P;
+  k_pack<<<blocks_for(m * Pn, 256), 256, 0, s>>>(blocks, cones, m, Pn,
+                                                 reinterpret_cast<double2*>(buf), unpack,
+                                                 blocks_out);
+  ++P->launches;
+}
+
+}  // namespace ifgf_b200

@@ -1,0 +1,159 @@
+// plan.hpp -- host-side plan object (device-resident Problem) shared by the
+// translation units of libifgf_b200.so.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/ifgf_b200.h"
+#include "ifgf_common.cuh"
+
+namespace ifgf_b200 {
+
+// C++ exception carrying one of the IFGF_E* codes; caught at the C ABI.
+struct Error : std::runtime_error {
+  int code;
+  Error(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+#define IFGF_CUDA(call)                                                                     \
+  do {                                                                                      \
+    cudaError_t e_ = (call);                                                                \
+    if (e_ != cudaSuccess)                                                                  \
+      throw ::ifgf_b200::Error(IFGF_ERUNTIME, std::string("CUDA: ") + cudaGetErrorString(e_) + \
+                                                  " at " __FILE__ ":" + std::to_string(__LINE__)); \
+  } while (0)
+
+// One octree level: owned device arrays + the LevelDev view handed to kernels.
+struct Level {
+  int d = 0;
+  uint32_t nb = 0;
+  double h = 0.0;
+  uint64_t* code = nullptr;
+  uint32_t* first = nullptr;
+  uint32_t* count = nullptr;
+  double *cx = nullptr, *cy = nullptr, *cz = nullptr;
+  uint32_t* parent = nullptr;
+  uint32_t* child_begin = nullptr;
+  uint32_t* nbr = nullptr;
+  uint32_t* nbr_cnt = nullptr;
+  uint32_t* cous_off = nullptr;
+  uint32_t* cous = nullptr;
+  size_t n_cous = 0;
+  size_t n_nbr = 0;
+  uint32_t* ptbox = nullptr;  // box ordinal of every sorted point at this level
+  // cone set
+  int n0 = 0, n1 = 0, n2 = 0;
+  double w0 = 0, w1 = 0, w2 = 0, iw0 = 0, iw1 = 0, iw2 = 0, rad = 0;
+  uint64_t G = 0;
+  uint32_t nc = 0;
+  uint32_t* cone_box = nullptr;
+  uint32_t* cone_gamma = nullptr;
+  uint32_t* box_cone = nullptr;
+  uint64_t* bits = nullptr;
+  uint32_t* rank = nullptr;
+  size_t nwords = 0;
+
+  LevelDev dev() const {
+    LevelDev v;
+    v.d = d;
+    v.nb = nb;
+    v.h = h;
+    v.code = code;
+    v.first = first;
+    v.count = count;
+    v.cx = cx;
+    v.cy = cy;
+    v.cz = cz;
+    v.parent = parent;
+    v.child_begin = child_begin;
+    v.nbr = nbr;
+    v.nbr_cnt = nbr_cnt;
+    v.cous_off = cous_off;
+    v.cous = cous;
+    v.n0 = n0;
+    v.n1 = n1;
+    v.n2 = n2;
+    v.w0 = w0;
+    v.w1 = w1;
+    v.w2 = w2;
+    v.iw0 = iw0;
+    v.iw1 = iw1;
+    v.iw2 = iw2;
+    v.rad = rad;
+    v.G = G;
+    v.nc = nc;
+    v.cone_box = cone_box;
+    v.cone_gamma = cone_gamma;
+    v.box_cone = box_cone;
+    v.bits = bits;
+    v.rank = rank;
+    return v;
+  }
+};
+
+}  // namespace ifgf_b200
+
+struct ifgf_plan {
+  int device = 0;
+  cudaStream_t s_main = nullptr, s_aux = nullptr;
+  size_t n = 0;
+  int kind = IFGF_HELMHOLTZ;
+  double kappa = 0.0;
+  ifgf_params params{};
+  ifgf_b200::InterpConsts K{};
+  double cube[4] = {0, 0, 0, 0};
+  int depth = 0;
+  uint32_t* perm = nullptr;
+  double *xs = nullptr, *ys = nullptr, *zs = nullptr;  // Morton-sorted coordinates
+  double *ar = nullptr, *ai = nullptr;                 // sorted densities
+  double *ir = nullptr, *ii = nullptr;                 // sorted results
+  int* err = nullptr;
+  ifgf_b200::Level lv[IFGF_MAX_LEVELS];
+  double2* stage_blocks[IFGF_MAX_LEVELS] = {};  // pass-level API storage
+  double2* slots[IFGF_MAX_LEVELS] = {};         // apply rotation
+  int n_slots = 0;
+  size_t slot_cap = 0;
+  std::vector<void*> allocs;
+  size_t bytes = 0;
+  double setup_seconds = 0.0;
+  size_t launches = 0;  // kernels launched by this plan since the last reset
+  bool serial = false;  // IFGF_OPT_SERIAL
+
+  template <class T>
+  T* alloc(size_t count) {
+    void* p = nullptr;
+    const size_t b = count * sizeof(T) + 16;
+    IFGF_CUDA(cudaMallocAsync(&p, b, s_main));
+    allocs.push_back(p);
+    bytes += b;
+    return static_cast<T*>(p);
+  }
+  const ifgf_b200::Level& L(int d) const { return lv[d]; }
+};
+
+namespace ifgf_b200 {
+// setup.cu
+void build_plan(ifgf_plan* P, const double* d_x, const double* d_y, const double* d_z);
+void check_device_error(ifgf_plan* P);
+// passes.cu
+void launch_gather_density(ifgf_plan* P, const double* a_re, const double* a_im, cudaStream_t s);
+void launch_scatter_result(ifgf_plan* P, double* o_re, double* o_im, cudaStream_t s);
+void launch_singular(ifgf_plan* P, size_t b, size_t e, cudaStream_t s);
+void launch_level_d(ifgf_plan* P, uint32_t qb, uint32_t qe, double2* out, cudaStream_t s);
+void launch_propagation(ifgf_plan* P, int d, uint32_t qb, uint32_t qe, const double2* child,
+                        double2* parent, cudaStream_t s);
+void launch_interpolation(ifgf_plan* P, int d, size_t b, size_t e, const double2* blocks,
+                          cudaStream_t s);
+void launch_pack(ifgf_plan* P, const double2* blocks, const uint32_t* cones, size_t m,
+                 double* buf, int unpack, double2* blocks_out, cudaStream_t s);
+bool orders_supported(int ps, int pt, int pp);
+// direct.cu
+void direct_sums(const double* x, const double* y, const double* z, const double* ar,
+                 const double* ai, size_t n, double kappa, const uint32_t* targets, size_t m,
+                 double* o_re, double* o_im, cudaStream_t s);
+}  // namespace ifgf_b200

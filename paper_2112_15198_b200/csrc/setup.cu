@@ -1,0 +1,581 @@
+// setup.cu -- Problem::build on the device (engine.cpp:74-94).
+//
+//   bounding cube      geometry.cpp:95-114   two-stage min/max reduction
+//   choose_depth       engine.cpp:55-72      host (scalar)
+//   Morton sort        morton.cpp:53-95      grid index + code kernel, CUB stable radix sort
+//   linear octree      octree.cpp:18-150     one "first level where point i starts a box"
+//                                            pass, then per level an inclusive scan gives
+//                                            every point's box ordinal; boxes, parents and
+//                                            child ranges follow from those ordinals;
+//                                            27-stencil neighbours by binary search;
+//                                            cousin CSR by count / scan / fill
+//   relevant cones     cones.cpp:90-150      per level d = 3..D: mark (box, gamma) bits from
+//                                            clause 1 (cousin points) and clause 2 (parent
+//                                            cone nodes), popcount prefix = cone ordinals in
+//                                            (box, gamma) order, compaction to the flat lists
+//
+// All structural arithmetic follows the reference operation order with
+// explicit _rn intrinsics (ifgf_common.cuh), so the result is identical to
+// the reference's Problem, which the parity tests check list by list.
+#include <cub/cub.cuh>
+
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+
+#include "plan.hpp"
+
+namespace ifgf_b200 {
+namespace {
+
+constexpr int kT = 256;
+
+inline unsigned grid_for(size_t n, int t = kT) {
+  size_t g = (n + t - 1) / t;
+  return (unsigned)(g ? g : 1);
+}
+
+__device__ __forceinline__ uint64_t spread3(uint64_t x) {
+  x &= 0x1fffffull;
+  x = (x | x << 32) & 0x1f00000000ffffull;
+  x = (x | x << 16) & 0x1f0000ff0000ffull;
+  x = (x | x << 8) & 0x100f00f00f00f00full;
+  x = (x | x << 4) & 0x10c30c30c30c30c3ull;
+  x = (x | x << 2) & 0x1249249249249249ull;
+  return x;
+}
+
+__device__ __forceinline__ uint32_t compact3(uint64_t x) {
+  x &= 0x1249249249249249ull;
+  x = (x ^ (x >> 2)) & 0x10c30c30c30c30c3ull;
+  x = (x ^ (x >> 4)) & 0x100f00f00f00f00full;
+  x = (x ^ (x >> 8)) & 0x1f0000ff0000ffull;
+  x = (x ^ (x >> 16)) & 0x1f00000000ffffull;
+  x = (x ^ (x >> 32)) & 0x1fffffull;
+  return (uint32_t)x;
+}
+
+// ---- bounding cube ---------------------------------------------------------
+__global__ void k_bbox_partial(const double* __restrict__ x, const double* __restrict__ y,
+                               const double* __restrict__ z, size_t n, double* part) {
+  double lo[3] = {INFINITY, INFINITY, INFINITY}, hi[3] = {-INFINITY, -INFINITY, -INFINITY};
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n;
+       i += (size_t)gridDim.x * blockDim.x) {
+    const double v[3] = {x[i], y[i], z[i]};
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      lo[c] = fmin(lo[c], v[c]);
+      hi[c] = fmax(hi[c], v[c]);
+    }
+  }
+  __shared__ double s[6][kT];
+#pragma unroll
+  for (int c = 0; c < 3; ++c) {
+    s[c][threadIdx.x] = lo[c];
+    s[3 + c][threadIdx.x] = hi[c];
+  }
+  __syncthreads();
+  for (int w = kT / 2; w > 0; w >>= 1) {
+    if (threadIdx.x < w)
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        s[c][threadIdx.x] = fmin(s[c][threadIdx.x], s[c][threadIdx.x + w]);
+        s[3 + c][threadIdx.x] = fmax(s[3 + c][threadIdx.x], s[3 + c][threadIdx.x + w]);
+      }
+    __syncthreads();
+  }
+  if (threadIdx.x < 6) part[blockIdx.x * 6 + threadIdx.x] = s[threadIdx.x][0];
+}
+
+__global__ void k_bbox_final(const double* part, int nparts, double* out) {
+  if (threadIdx.x >= 6) return;
+  const int c = threadIdx.x;
+  double v = part[c];
+  for (int b = 1; b < nparts; ++b) v = c < 3 ? fmin(v, part[b * 6 + c]) : fmax(v, part[b * 6 + c]);
+  out[c] = v;
+}
+
+// ---- Morton codes (morton.cpp:53-68 grid_index, :40-45 encode) --------------
+__global__ void k_morton(const double* __restrict__ x, const double* __restrict__ y,
+                         const double* __restrict__ z, size_t n, double ox, double oy, double oz,
+                         double side, double h, uint32_t ngrid, uint64_t* codes, uint32_t* idx,
+                         int* err) {
+  const size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const double rel[3] = {__dsub_rn(x[i], ox), __dsub_rn(y[i], oy), __dsub_rn(z[i], oz)};
+  uint64_t k[3];
+#pragma unroll
+  for (int c = 0; c < 3; ++c) {
+    if (!(rel[c] >= 0.0) || rel[c] >= side) {
+      raise_err(err, kErrOutside);
+      k[c] = 0;
+      continue;
+    }
+    int64_t v = (int64_t)floor(__ddiv_rn(rel[c], h));
+    if (v >= (int64_t)ngrid) v = ngrid - 1;
+    k[c] = (uint64_t)v;
+  }
+  codes[i] = spread3(k[0]) | spread3(k[1]) << 1 | spread3(k[2]) << 2;
+  idx[i] = (uint32_t)i;
+}
+
+__global__ void k_gather3(const uint32_t* __restrict__ perm, const double* __restrict__ x,
+                          const double* __restrict__ y, const double* __restrict__ z, size_t n,
+                          double* xs, double* ys, double* zs) {
+  const size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const uint32_t j = perm[i];
+  xs[i] = x[j];
+  ys[i] = y[j];
+  zs[i] = z[j];
+}
+
+// First (coarsest) level at which sorted point i opens a new box; level-d
+// codes are code >> 3(D-d) (octree.cpp:57-76).  Also histograms it.
+__global__ void k_start_level(const uint64_t* __restrict__ codes, size_t n, int D,
+                              uint8_t* start, uint32_t* hist) {
+  const size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
+  __shared__ uint32_t sh[32];
+  if (threadIdx.x < 32) sh[threadIdx.x] = 0;
+  __syncthreads();
+  if (i < n) {
+    int lvl = 1;
+    if (i > 0) {
+      const uint64_t diff = codes[i] ^ codes[i - 1];
+      if (diff == 0) {
+        lvl = 31;  // never starts a box
+      } else {
+        const int hb = 63 - __clzll(diff);
+        lvl = D - hb / 3;
+      }
+    }
+    start[i] = (uint8_t)lvl;
+    atomicAdd(&sh[lvl], 1u);
+  }
+  __syncthreads();
+  if (threadIdx.x < 32 && sh[threadIdx.x]) atomicAdd(&hist[threadIdx.x], sh[threadIdx.x]);
+}
+
+struct StartsAt {
+  const uint8_t* start;
+  int d;
+  __host__ __device__ uint32_t operator()(const size_t& i) const { return start[i] <= d ? 1u : 0u; }
+};
+
+// ptbox (inclusive count) -> ordinal; box heads record first point, code, centre.
+__global__ void k_boxes(uint32_t* ptbox, const uint8_t* __restrict__ start,
+                        const uint64_t* __restrict__ codes, size_t n, int d, int D, double ox,
+                        double oy, double oz, double h, uint32_t* first, uint64_t* bcode,
+                        double* cx, double* cy, double* cz) {
+  const size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const uint32_t b = ptbox[i] - 1;
+  ptbox[i] = b;
+  if (start[i] <= d) {
+    const uint64_t c = codes[i] >> (3 * (D - d));
+    first[b] = (uint32_t)i;
+    bcode[b] = c;
+    // octree.cpp:10-14: origin + (k + 0.5) * h
+    cx[b] = __dadd_rn(ox, __dmul_rn((double)compact3(c) + 0.5, h));
+    cy[b] = __dadd_rn(oy, __dmul_rn((double)compact3(c >> 1) + 0.5, h));
+    cz[b] = __dadd_rn(oz, __dmul_rn((double)compact3(c >> 2) + 0.5, h));
+  }
+}
+
+__global__ void k_box_links(uint32_t nb, size_t n, const uint32_t* __restrict__ first,
+                            uint32_t* count, const uint32_t* __restrict__ ptbox_up,
+                            uint32_t* parent, const uint32_t* __restrict__ ptbox_down,
+                            uint32_t* child_begin, uint32_t nb_down) {
+  const uint32_t b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b > nb) return;
+  if (b == nb) {
+    if (child_begin) child_begin[nb] = nb_down;
+    return;
+  }
+  const uint32_t f = first[b];
+  count[b] = (b + 1 < nb ? first[b + 1] : (uint32_t)n) - f;
+  if (parent) parent[b] = ptbox_up ? ptbox_up[f] : 0u;
+  if (child_begin) child_begin[b] = ptbox_down[f];
+}
+
+// 27-stencil neighbours incl. self, ascending ordinals (octree.cpp:97-122).
+__global__ void k_neighbors(uint32_t nb, int d, const uint64_t* __restrict__ code,
+                            uint32_t* nbr, uint32_t* nbr_cnt) {
+  const uint32_t b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= nb) return;
+  const uint64_t c = code[b];
+  const int64_t k[3] = {compact3(c), compact3(c >> 1), compact3(c >> 2)};
+  const int64_t side = (int64_t)1 << (d - 1);
+  uint32_t found[27];
+  int cnt = 0;
+  for (int dz = -1; dz <= 1; ++dz)
+    for (int dy = -1; dy <= 1; ++dy)
+      for (int dx = -1; dx <= 1; ++dx) {
+        const int64_t j[3] = {k[0] + dx, k[1] + dy, k[2] + dz};
+        if (j[0] < 0 || j[1] < 0 || j[2] < 0 || j[0] >= side || j[1] >= side || j[2] >= side)
+          continue;
+        const uint64_t t = spread3(j[0]) | spread3(j[1]) << 1 | spread3(j[2]) << 2;
+        uint32_t lo = 0, hi = nb;
+        while (lo < hi) {
+          const uint32_t mid = (lo + hi) >> 1;
+          if (code[mid] < t) lo = mid + 1;
+          else hi = mid;
+        }
+        if (lo < nb && code[lo] == t) found[cnt++] = lo;
+      }
+  for (int a = 1; a < cnt; ++a)
+    for (int q = a; q > 0 && found[q - 1] > found[q]; --q) {
+      const uint32_t tmp = found[q];
+      found[q] = found[q - 1];
+      found[q - 1] = tmp;
+    }
+  for (int a = 0; a < cnt; ++a) nbr[(size_t)b * 27 + a] = found[a];
+  nbr_cnt[b] = cnt;
+}
+
+// Cousins: children of parent-neighbours at Chebyshev distance > 1, visited in
+// Morton order (octree.cpp:127-147).  fill == nullptr: count only.
+__global__ void k_cousins(const __grid_constant__ LevelDev L, const __grid_constant__ LevelDev U, uint32_t* cnt_or_off, uint32_t* fill) {
+  const uint32_t b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= L.nb) return;
+  const uint64_t c = L.code[b];
+  const uint32_t k[3] = {compact3(c), compact3(c >> 1), compact3(c >> 2)};
+  const uint32_t pb = L.parent[b];
+  uint32_t w = fill ? cnt_or_off[b] : 0u;
+  const uint32_t np = U.nbr_cnt[pb];
+  for (uint32_t a = 0; a < np; ++a) {
+    const uint32_t pn = U.nbr[(size_t)pb * 27 + a];
+    for (uint32_t ch = U.child_begin[pn]; ch < U.child_begin[pn + 1]; ++ch) {
+      const uint64_t cc = L.code[ch];
+      const uint32_t j[3] = {compact3(cc), compact3(cc >> 1), compact3(cc >> 2)};
+      uint32_t dist = 0;
+#pragma unroll
+      for (int q = 0; q < 3; ++q) {
+        const uint32_t dd = j[q] > k[q] ? j[q] - k[q] : k[q] - j[q];
+        dist = dd > dist ? dd : dist;
+      }
+      if (dist > 1) {
+        if (fill) fill[w] = ch;
+        ++w;
+      }
+    }
+  }
+  if (!fill) cnt_or_off[b] = w;
+}
+
+__device__ __forceinline__ void set_bit(uint64_t* bits, uint64_t idx) {
+  const uint64_t m = 1ull << (idx & 63);
+  uint64_t* w = bits + (idx >> 6);
+  if (!(*w & m)) atomicOr((unsigned long long*)w, (unsigned long long)m);
+}
+
+// Clause 1 (cones.cpp:100-106), transposed: every sorted point marks, in each
+// cousin box of its own box (the cousin relation is symmetric), the segment
+// containing it.
+__global__ void k_mark_points(const __grid_constant__ LevelDev L, const uint32_t* __restrict__ ptbox,
+                              const double* __restrict__ xs, const double* __restrict__ ys,
+                              const double* __restrict__ zs, size_t n, uint64_t* bits, int* err) {
+  const size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const uint32_t b = ptbox[i];
+  const double x = xs[i], y = ys[i], z = zs[i];
+  for (uint32_t ci = L.cous_off[b]; ci < L.cous_off[b + 1]; ++ci) {
+    const uint32_t cb = L.cous[ci];
+    uint32_t g;
+    const int e = cone_of_point(L, L.cx[cb], L.cy[cb], L.cz[cb], x, y, z, g);
+    if (e) {
+      raise_err(err, e);
+      return;
+    }
+    set_bit(bits, (uint64_t)cb * L.G + g);
+  }
+}
+
+// Clause 2 (cones.cpp:108-119): nodes of every relevant cone of the parent box
+// mark the containing segment of each child box.
+__global__ void k_mark_nodes(const __grid_constant__ LevelDev L, const __grid_constant__ LevelDev U,
+                             const __grid_constant__ InterpConsts K, uint64_t* bits, int* err) {
+  const size_t t = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
+  if (t >= (size_t)U.nc * K.P) return;
+  const uint32_t q = (uint32_t)(t / K.P);
+  const int m = (int)(t % K.P);
+  const int jp = m % K.pp, jt = (m / K.pp) % K.pt, js = m / (K.pp * K.pt);
+  const uint32_t pb = U.cone_box[q];
+  const SegMid sm = segment_mid(U, U.cone_gamma[q]);
+  double x, y, z;
+  node_position(sm, U.rad, U.cx[pb], U.cy[pb], U.cz[pb], K.ns[js], K.nt[jt], K.np[jp], x, y, z);
+  for (uint32_t cb = U.child_begin[pb]; cb < U.child_begin[pb + 1]; ++cb) {
+    uint32_t g;
+    const int e = cone_of_point(L, L.cx[cb], L.cy[cb], L.cz[cb], x, y, z, g);
+    if (e) {
+      raise_err(err, e);
+      return;
+    }
+    set_bit(bits, (uint64_t)cb * L.G + g);
+  }
+}
+
+__global__ void k_popc(const uint64_t* __restrict__ bits, size_t nw, uint32_t* cnt) {
+  const size_t w = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
+  if (w < nw) cnt[w] = __popcll(bits[w]);
+  else if (w == nw) cnt[w] = 0;
+}
+
+__global__ void k_compact(const __grid_constant__ LevelDev L, size_t nw, uint32_t* cone_box, uint32_t* cone_gamma) {
+  const size_t w = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
+  if (w >= nw) return;
+  uint64_t v = L.bits[w];
+  uint32_t o = L.rank[w];
+  while (v) {
+    const int bit = __ffsll((long long)v) - 1;
+    v &= v - 1;
+    const uint64_t idx = (uint64_t)w * 64 + bit;
+    cone_box[o] = (uint32_t)(idx / L.G);
+    cone_gamma[o] = (uint32_t)(idx % L.G);
+    ++o;
+  }
+}
+
+__global__ void k_box_cone(const __grid_constant__ LevelDev L, uint32_t* box_cone) {
+  const uint32_t b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b > L.nb) return;
+  const uint64_t idx = (uint64_t)b * L.G;
+  const uint64_t w = idx >> 6;
+  const uint64_t m = (1ull << (idx & 63)) - 1;
+  box_cone[b] = L.rank[w] + (uint32_t)__popcll(L.bits[w] & m);
+}
+
+// grows the plan's CUB scratch buffer
+struct Scratch {
+  ifgf_plan* P;
+  void* p = nullptr;
+  size_t bytes = 0;
+  void* get(size_t b) {
+    if (b > bytes) {
+      if (p) IFGF_CUDA(cudaFreeAsync(p, P->s_main));
+      bytes = b + (b >> 2) + 256;
+      IFGF_CUDA(cudaMallocAsync(&p, bytes, P->s_main));
+    }
+    return p;
+  }
+  ~Scratch() {
+    if (p) cudaFreeAsync(p, P->s_main);
+  }
+};
+
+}  // namespace
+
+void check_device_error(ifgf_plan* P) {
+  int e = 0;
+  IFGF_CUDA(cudaMemcpyAsync(&e, P->err, sizeof(int), cudaMemcpyDeviceToHost, P->s_main));
+  IFGF_CUDA(cudaStreamSynchronize(P->s_main));
+  if (!e) return;
+  IFGF_CUDA(cudaMemsetAsync(P->err, 0, sizeof(int), P->s_main));
+  switch (e) {
+    case kErrSMax:
+      throw Error(IFGF_EDOMAIN, "cone_of_point: point inside the neighbor zone (s > s_max)");
+    case kErrCenter:
+      throw Error(IFGF_EDOMAIN, "cone_coords: point at box center");
+    case kErrPropCover:
+      throw Error(IFGF_ELOGIC, "propagation: node not covered by a relevant child cone");
+    case kErrInterpCover:
+      throw Error(IFGF_ELOGIC, "interpolation: cousin point not covered by a relevant cone");
+    case kErrOutside:
+      throw Error(IFGF_EDOMAIN, "point outside bounding cube");
+    case kErrNonFinite:
+      throw Error(IFGF_EINVAL, "cheb_fit: non-finite node value");
+    default:
+      throw Error(IFGF_ERUNTIME, "unknown device error " + std::to_string(e));
+  }
+}
+
+void build_plan(ifgf_plan* P, const double* d_x, const double* d_y, const double* d_z) {
+  const auto t0 = std::chrono::steady_clock::now();
+  cudaStream_t s = P->s_main;
+  const size_t n = P->n;
+  Scratch scratch{P};
+
+  // -- bounding cube (geometry.cpp:95-114)
+  const int nparts = 296;
+  double* part = P->alloc<double>(nparts * 6 + 6);
+  k_bbox_partial<<<nparts, kT, 0, s>>>(d_x, d_y, d_z, n, part);
+  k_bbox_final<<<1, 32, 0, s>>>(part, nparts, part + nparts * 6);
+  P->launches += 2;
+  double bb[6];
+  IFGF_CUDA(cudaMemcpyAsync(bb, part + nparts * 6, sizeof bb, cudaMemcpyDeviceToHost, s));
+  IFGF_CUDA(cudaStreamSynchronize(s));
+  for (int c = 0; c < 6; ++c)
+    if (!std::isfinite(bb[c])) throw Error(IFGF_EDOMAIN, "point outside bounding cube");
+  const double extent = std::max({bb[3] - bb[0], bb[4] - bb[1], bb[5] - bb[2]});
+  const double side = std::max((1.0 + 1e-6) * extent, 1e-9);
+  P->cube[3] = side;
+  for (int c = 0; c < 3; ++c) P->cube[c] = 0.5 * (bb[c] + bb[3 + c]) - 0.5 * side;
+
+  // -- depth (engine.cpp:55-72)
+  int D = 0;
+  {
+    const int rc = ifgf_choose_depth(n, side, P->kappa, &P->params, &D);
+    if (rc) throw Error(rc, ifgf_last_error());
+  }
+  P->depth = D;
+  {
+    // bitmap indices of the coarsest cone level must fit the u32 gamma
+    const double G3 = (double)P->params.base_s * P->params.base_theta * P->params.base_phi *
+                      std::pow(8.0, D - 3);
+    if (G3 >= 4294967296.0)
+      throw Error(IFGF_EINVAL, "depth " + std::to_string(D) +
+                                   " needs cone indices beyond 32 bits (unsupported)");
+  }
+
+  // -- Morton codes + stable sort (morton.cpp:70-95)
+  const uint32_t ngrid = 1u << (D - 1);
+  const double hD = side / static_cast<double>(ngrid);
+  uint64_t* codes_in = P->alloc<uint64_t>(n);
+  uint64_t* codes = P->alloc<uint64_t>(n);
+  uint32_t* idx_in = P->alloc<uint32_t>(n);
+  P->perm = P->alloc<uint32_t>(n);
+  k_morton<<<grid_for(n), kT, 0, s>>>(d_x, d_y, d_z, n, P->cube[0], P->cube[1], P->cube[2], side,
+                                      hD, ngrid, codes_in, idx_in, P->err);
+  ++P->launches;
+  {
+    size_t tb = 0;
+    cub::DeviceRadixSort::SortPairs(nullptr, tb, codes_in, codes, idx_in, P->perm, (int)n, 0,
+                                    3 * (D - 1), s);
+    IFGF_CUDA(cub::DeviceRadixSort::SortPairs(scratch.get(tb), tb, codes_in, codes, idx_in,
+                                              P->perm, (int)n, 0, 3 * (D - 1), s));
+  }
+  P->xs = P->alloc<double>(n);
+  P->ys = P->alloc<double>(n);
+  P->zs = P->alloc<double>(n);
+  k_gather3<<<grid_for(n), kT, 0, s>>>(P->perm, d_x, d_y, d_z, n, P->xs, P->ys, P->zs);
+  ++P->launches;
+
+  // -- octree levels (octree.cpp:18-94)
+  uint8_t* start = P->alloc<uint8_t>(n);
+  uint32_t* hist = P->alloc<uint32_t>(32);
+  IFGF_CUDA(cudaMemsetAsync(hist, 0, 32 * sizeof(uint32_t), s));
+  k_start_level<<<grid_for(n), kT, 0, s>>>(codes, n, D, start, hist);
+  ++P->launches;
+  uint32_t h_hist[32];
+  IFGF_CUDA(cudaMemcpyAsync(h_hist, hist, sizeof h_hist, cudaMemcpyDeviceToHost, s));
+  IFGF_CUDA(cudaStreamSynchronize(s));
+  {
+    uint32_t acc = 0;
+    for (int d = 1; d <= D; ++d) {
+      acc += h_hist[d];
+      P->lv[d].nb = acc;
+      P->lv[d].d = d;
+      P->lv[d].h = side / static_cast<double>(1u << (d - 1));
+    }
+  }
+  for (int d = 1; d <= D; ++d) {
+    Level& L = P->lv[d];
+    L.ptbox = P->alloc<uint32_t>(n);
+    cub::TransformInputIterator<uint32_t, StartsAt, cub::CountingInputIterator<size_t>> it(
+        cub::CountingInputIterator<size_t>(0), StartsAt{start, d});
+    size_t tb = 0;
+    cub::DeviceScan::InclusiveSum(nullptr, tb, it, L.ptbox, (int)n, s);
+    IFGF_CUDA(cub::DeviceScan::InclusiveSum(scratch.get(tb), tb, it, L.ptbox, (int)n, s));
+    L.first = P->alloc<uint32_t>(L.nb);
+    L.count = P->alloc<uint32_t>(L.nb);
+    L.code = P->alloc<uint64_t>(L.nb);
+    L.cx = P->alloc<double>(L.nb);
+    L.cy = P->alloc<double>(L.nb);
+    L.cz = P->alloc<double>(L.nb);
+    k_boxes<<<grid_for(n), kT, 0, s>>>(L.ptbox, start, codes, n, d, D, P->cube[0], P->cube[1],
+                                       P->cube[2], L.h, L.first, L.code, L.cx, L.cy, L.cz);
+    ++P->launches;
+  }
+  for (int d = 1; d <= D; ++d) {
+    Level& L = P->lv[d];
+    L.parent = P->alloc<uint32_t>(L.nb);
+    L.child_begin = d < D ? P->alloc<uint32_t>(L.nb + 1) : nullptr;
+    k_box_links<<<grid_for(L.nb + 1), kT, 0, s>>>(
+        L.nb, n, L.first, L.count, d > 1 ? P->lv[d - 1].ptbox : nullptr, L.parent,
+        d < D ? P->lv[d + 1].ptbox : nullptr, L.child_begin, d < D ? P->lv[d + 1].nb : 0);
+    L.nbr = P->alloc<uint32_t>((size_t)L.nb * 27);
+    L.nbr_cnt = P->alloc<uint32_t>(L.nb);
+    k_neighbors<<<grid_for(L.nb), kT, 0, s>>>(L.nb, d, L.code, L.nbr, L.nbr_cnt);
+    P->launches += 2;
+  }
+  // cousin CSR for d = 3..D
+  std::vector<uint32_t> cous_total(D + 1, 0);
+  for (int d = 3; d <= D; ++d) {
+    Level& L = P->lv[d];
+    uint32_t* cnt = P->alloc<uint32_t>(L.nb + 1);
+    L.cous_off = P->alloc<uint32_t>(L.nb + 1);
+    IFGF_CUDA(cudaMemsetAsync(cnt + L.nb, 0, sizeof(uint32_t), s));
+    k_cousins<<<grid_for(L.nb), kT, 0, s>>>(L.dev(), P->lv[d - 1].dev(), cnt, nullptr);
+    ++P->launches;
+    size_t tb = 0;
+    cub::DeviceScan::ExclusiveSum(nullptr, tb, cnt, L.cous_off, (int)(L.nb + 1), s);
+    IFGF_CUDA(
+        cub::DeviceScan::ExclusiveSum(scratch.get(tb), tb, cnt, L.cous_off, (int)(L.nb + 1), s));
+    IFGF_CUDA(cudaMemcpyAsync(&cous_total[d], L.cous_off + L.nb, sizeof(uint32_t),
+                              cudaMemcpyDeviceToHost, s));
+  }
+  IFGF_CUDA(cudaStreamSynchronize(s));
+  for (int d = 3; d <= D; ++d) {
+    Level& L = P->lv[d];
+    L.n_cous = cous_total[d];
+    L.cous = P->alloc<uint32_t>(L.n_cous + 1);
+    k_cousins<<<grid_for(L.nb), kT, 0, s>>>(L.dev(), P->lv[d - 1].dev(), L.cous_off, L.cous);
+    ++P->launches;
+  }
+
+  // -- relevant cones, d = 3..D (cones.cpp:90-150)
+  const ifgf_params& p = P->params;
+  for (int d = 3; d <= D; ++d) {
+    Level& L = P->lv[d];
+    const int f = 1 << (D - d);
+    L.n0 = p.base_s * f;
+    L.n1 = p.base_theta * f;
+    L.n2 = p.base_phi * f;
+    L.w0 = kSMax / L.n0;
+    L.w1 = kPi / L.n1;
+    L.w2 = 2.0 * kPi / L.n2;
+    L.iw0 = 1.0 / L.w0;
+    L.iw1 = 1.0 / L.w1;
+    L.iw2 = 1.0 / L.w2;
+    L.rad = std::sqrt(3.0) * L.h / 2.0;
+    L.G = (uint64_t)L.n0 * L.n1 * L.n2;
+    L.nwords = ((uint64_t)L.nb * L.G + 63) / 64;
+    L.bits = P->alloc<uint64_t>(L.nwords);
+    L.rank = P->alloc<uint32_t>(L.nwords + 1);
+    IFGF_CUDA(cudaMemsetAsync(L.bits, 0, L.nwords * sizeof(uint64_t), s));
+    k_mark_points<<<grid_for(n), kT, 0, s>>>(L.dev(), L.ptbox, P->xs, P->ys, P->zs, n, L.bits,
+                                             P->err);
+    ++P->launches;
+    if (d > 3 && P->lv[d - 1].nc > 0) {
+      const size_t work = (size_t)P->lv[d - 1].nc * P->K.P;
+      k_mark_nodes<<<grid_for(work), kT, 0, s>>>(L.dev(), P->lv[d - 1].dev(), P->K, L.bits,
+                                                 P->err);
+      ++P->launches;
+    }
+    uint32_t* cnt = P->alloc<uint32_t>(L.nwords + 1);
+    k_popc<<<grid_for(L.nwords + 1), kT, 0, s>>>(L.bits, L.nwords, cnt);
+    ++P->launches;
+    size_t tb = 0;
+    cub::DeviceScan::ExclusiveSum(nullptr, tb, cnt, L.rank, (int)(L.nwords + 1), s);
+    IFGF_CUDA(
+        cub::DeviceScan::ExclusiveSum(scratch.get(tb), tb, cnt, L.rank, (int)(L.nwords + 1), s));
+    uint32_t nc = 0;
+    IFGF_CUDA(
+        cudaMemcpyAsync(&nc, L.rank + L.nwords, sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
+    IFGF_CUDA(cudaStreamSynchronize(s));
+    check_device_error(P);
+    L.nc = nc;
+    L.cone_box = P->alloc<uint32_t>(nc + 1);
+    L.cone_gamma = P->alloc<uint32_t>(nc + 1);
+    L.box_cone = P->alloc<uint32_t>(L.nb + 1);
+    k_compact<<<grid_for(L.nwords), kT, 0, s>>>(L.dev(), L.nwords, L.cone_box, L.cone_gamma);
+    k_box_cone<<<grid_for(L.nb + 1), kT, 0, s>>>(L.dev(), L.box_cone);
+    P->launches += 2;
+  }
+  IFGF_CUDA(cudaStreamSynchronize(s));
+  check_device_error(P);
+  P->setup_seconds =
+      std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+}
+
+}  // namespace ifgf_b200
