@@ -1,0 +1,350 @@
+"""IFGF matvec benchmark (BASELINE.json metric: matvec time & Mpoints/s).
+
+One step = one full operator application as the reference defines it
+(ifgf::apply, engine.cpp:260-325): Problem::build (octree + relevant cones) on
+the device from device-resident coordinates, then the matvec on
+device-resident densities.  `value` = N / step time in Mpoints/s, timed with
+CUDA events on the caller stream (the library orders itself after it), L2
+flushed between steps.  `e2e` = the same operator through the C ABI
+(ifgf_apply) from pinned host buffers, H2D/D2H included.  `apply_only` =
+plan reused, matvec only (the iterative-solver case).
+
+Default workload: BASELINE configs[1] (C2, N=1,572,864 sphere, kappa=32pi,
+(3,5,5)) on one GPU.  --impl reference times the reference's own CPU
+implementation (oracle/_ref, compiled from the reference sources) on a bounded
+sample of the same workload with all host threads.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "IFGF matvec throughput (Mpoints/s; N / full apply time incl. device setup)"
+UNIT = "Mpoints/s"
+# Bounded CPU sample of C2: the same surface and points-per-wavelength density
+# at 1/16 of the points (N = 98,304, kappa = 8 pi, i.e. BASELINE configs[0]).
+REF_SAMPLE_N = 98_304
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--config", default="C2")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    return ap.parse_args()
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index, self.rows, self._stop = index, [], threading.Event()
+        self._t = threading.Thread(target=self._run, daemon=True)
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.index),
+                                      f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits"],
+                                     capture_output=True, text=True, timeout=5).stdout.strip()
+                if out:
+                    self.rows.append([v.strip() for v in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.1)
+
+    def __enter__(self):
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[k] for r in self.rows for k in range(4)
+                          if len(r) > 4 + k and r[4 + k] == "Active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(self.rows)}
+
+
+def dist_env():
+    return (int(os.environ.get("RANK", 0)), int(os.environ.get("LOCAL_RANK", 0)),
+            int(os.environ.get("WORLD_SIZE", 1)))
+
+
+def ref_checker():
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    from bindings import REF_SO, COracle, Params, RefOracle  # test infra: CPU baseline only
+    if os.path.exists(REF_SO):
+        return RefOracle(), Params(threads=os.cpu_count() or 1), "reference", os.cpu_count() or 1
+    return COracle(), Params(), "port", 1
+
+
+def cpu_sample_run(steps, warmup):
+    """The reference CPU path on the bounded C2-density sample; seconds per step."""
+    import paper_2112_15198_b200 as ifgf
+    cfg = ifgf.configs.scaled(ifgf.configs.C2, REF_SAMPLE_N)
+    pc = ifgf.generate(cfg.n, cfg.shape, cfg.c, cfg.dens, cfg.seed)
+    chk, params, kind, cores = ref_checker()
+    times = []
+    for i in range(warmup + steps):
+        t0 = time.perf_counter()
+        chk.apply(pc.x1, pc.x2, pc.x3, pc.a_re, pc.a_im, cfg.kind, cfg.kappa, params)
+        if i >= warmup:
+            times.append(time.perf_counter() - t0)
+    sample = (f"full reference apply (setup+passes) on C2's surface and density at "
+              f"N={cfg.n:,} (kappa={cfg.kappa / math.pi:g}pi = BASELINE configs[0]), "
+              f"IFGF_SIMD={os.environ.get('IFGF_SIMD', 'avx2')}")
+    return cfg.n, times, kind, cores, sample
+
+
+def run_reference(args):
+    rank, _, world = dist_env()
+    if rank != 0:
+        return
+    n, times, kind, cores, sample = cpu_sample_run(args.steps, args.warmup)
+    t = statistics.mean(times)
+    v = n / t / 1e6
+    print(json.dumps({
+        "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded, DESIGN.md Inputs)",
+        "config": {"workload": f"C2 sample: {sample}", "n": n},
+        "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": kind,
+                         "sample": sample},
+        "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }), flush=True)
+
+
+def run_ours(args):
+    import numpy as np
+    import torch
+
+    import paper_2112_15198_b200 as ifgf
+    from paper_2112_15198_b200 import _lib
+    from paper_2112_15198_b200.work import count_work
+
+    rank, local, world = dist_env()
+    torch.cuda.set_device(local)
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl")
+    if not ifgf.device_ok():
+        raise SystemExit("bench: no usable sm_100 device: " + _lib.last_error())
+    cfgd = ifgf.configs.CONFIGS[args.config]
+    kcfg = ifgf.KernelConfig(ifgf.KernelKind(cfgd.kind), cfgd.kappa)
+    params = ifgf.EngineParams(depth=cfgd.depth, device=local)
+    n = cfgd.n
+    # each rank owns a full replica (the distributed path lands in dist.py)
+    pc = ifgf.generate(n, cfgd.shape, cfgd.c, cfgd.dens, cfgd.seed + 1000 * rank)
+    dev = torch.device("cuda", local)
+    X = [torch.from_numpy(a).to(dev) for a in (pc.x1, pc.x2, pc.x3, pc.a_re, pc.a_im)]
+    out = [torch.empty(n, dtype=torch.float64, device=dev) for _ in range(2)]
+    flush = torch.empty(256 * 2**20 // 4, dtype=torch.float32, device=dev)  # 256 MB > 126 MB L2
+    s = torch.cuda.Stream(device=dev)
+    sh = s.cuda_stream
+
+    def step():
+        plan = ifgf.Plan.from_device(X[0].data_ptr(), X[1].data_ptr(), X[2].data_ptr(), n, kcfg,
+                                     params, stream=sh)
+        rep = plan.apply_device(X[3].data_ptr(), X[4].data_ptr(), out[0].data_ptr(),
+                                out[1].data_ptr(), stream=sh)
+        # our kernels in this step: setup (plan) + apply; CUB sort/scan launches excluded
+        rep.gpu_launches += int(plan.info.setup_launches)
+        plan.close()
+        return rep, None
+
+    def barrier():
+        torch.cuda.synchronize()
+        if world > 1:
+            torch.distributed.barrier()
+        torch.cuda.synchronize()
+
+    # ---- full operator (setup + apply), device-resident inputs
+    for _ in range(args.warmup):
+        step()
+    barrier()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+          for _ in range(args.steps)]
+    reps = []
+    with ClockSampler(local) as clocks:
+        for i in range(args.steps):
+            with torch.cuda.stream(s):
+                flush.zero_()
+            ev[i][0].record(s)
+            reps.append(step()[0])
+            ev[i][1].record(s)
+        torch.cuda.synchronize()
+    barrier()
+    step_ms = [a.elapsed_time(b) for a, b in ev]
+    t_step = sum(step_ms) / len(step_ms) / 1e3
+    if world > 1:
+        tt = torch.tensor([t_step], device=dev, dtype=torch.float64)
+        torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
+        t_step = float(tt.item())
+
+    # ---- apply only (plan reuse), and an exclusive per-pass timing run
+    plan = ifgf.Plan.from_device(X[0].data_ptr(), X[1].data_ptr(), X[2].data_ptr(), n, kcfg,
+                                 params, stream=sh)
+    for _ in range(2):
+        plan.apply_device(X[3].data_ptr(), X[4].data_ptr(), out[0].data_ptr(),
+                          out[1].data_ptr(), stream=sh)
+    ev2 = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+           for _ in range(args.steps)]
+    for i in range(args.steps):
+        with torch.cuda.stream(s):
+            flush.zero_()
+        ev2[i][0].record(s)
+        arep = plan.apply_device(X[3].data_ptr(), X[4].data_ptr(), out[0].data_ptr(),
+                                 out[1].data_ptr(), stream=sh)
+        ev2[i][1].record(s)
+    torch.cuda.synchronize()
+    t_apply = statistics.mean(a.elapsed_time(b) for a, b in ev2) / 1e3
+    plan.set_serial(True)
+    serial = []
+    for _ in range(3):
+        with torch.cuda.stream(s):
+            flush.zero_()
+        serial.append(plan.apply_device(X[3].data_ptr(), X[4].data_ptr(), out[0].data_ptr(),
+                                        out[1].data_ptr(), stream=sh))
+    torch.cuda.synchronize()
+    work = count_work(plan)
+    info = plan.info
+    plan.close()
+
+    # ---- measured FP64 peak (not in MEASURED_PEAKS.json)
+    import ctypes as C
+    pk, pk_ms = C.c_double(), C.c_double()
+    ifgf.engine.check(_lib.lib.ifgf_measure_fp64_peak(local, C.byref(pk), C.byref(pk_ms)))
+    fp64_peak = pk.value
+
+    # ---- e2e through the C ABI from pinned host buffers
+    e2e = None
+    if not args.no_e2e:
+        host = [torch.from_numpy(a).pin_memory().numpy() for a in
+                (pc.x1, pc.x2, pc.x3, pc.a_re, pc.a_im)]
+        hout = [torch.empty(n, dtype=torch.float64).pin_memory().numpy() for _ in range(2)]
+        hpc = ifgf.PointCloud(*host)
+        et = []
+        for i in range(args.warmup + args.steps):
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            rc = _lib.lib.ifgf_apply(n, _lib.ptr(hpc.x1), _lib.ptr(hpc.x2), _lib.ptr(hpc.x3),
+                                     _lib.ptr(hpc.a_re), _lib.ptr(hpc.a_im), int(kcfg.kind),
+                                     float(kcfg.wavenumber), C.byref(params.c()),
+                                     _lib.ptr(hout[0]), _lib.ptr(hout[1]), None)
+            ifgf.engine.check(rc)
+            if i >= args.warmup:
+                et.append(time.perf_counter() - t0)
+        te = statistics.mean(et)
+        if world > 1:
+            tt = torch.tensor([te], device=dev, dtype=torch.float64)
+            torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
+            te = float(tt.item())
+        e2e = {"value": world * n / te / 1e6, "unit": UNIT, "h2d_bytes_per_step": 5 * n * 8,
+               "d2h_bytes_per_step": 2 * n * 8, "ms_per_step": te * 1e3,
+               "api": "ifgf_apply (C ABI, pinned host buffers)"}
+
+    # ---- roofline of the dominant kernel (exclusive serial timings)
+    fl = work.flops
+    st = {k: statistics.median(getattr(r.seconds, k) for r in serial)
+          for k in ("singular", "level_d", "interpolation", "propagation")}
+    stage_key = {"near": "singular", "level_d": "level_d", "interpolation": "interpolation",
+                 "propagation": "propagation"}
+    per_kernel = {}
+    for k, sk in stage_key.items():
+        t = st[sk]
+        per_kernel[k] = {"ms": t * 1e3, "gflop": fl[k] / 1e9,
+                         "tflops": fl[k] / t / 1e12 if t > 0 else None,
+                         "frac_fp64": (fl[k] / t / 1e12) / fp64_peak if t > 0 else None}
+    dom = max(per_kernel, key=lambda k: per_kernel[k]["ms"])
+    traffic = None
+    summ = os.path.join(ROOT, "profiles", "ncu_summary.json")
+    if os.path.exists(summ):
+        try:
+            traffic = json.load(open(summ)).get("traffic_bytes_per_launch", {}).get(dom)
+        except Exception:
+            traffic = None
+    dk = per_kernel[dom]
+    roofline = {"bound": "fp64", "kernel": dom, "achieved": dk["tflops"], "peak": fp64_peak,
+                "unit": "TFLOP/s", "frac": dk["frac_fp64"], "traffic": traffic,
+                "peak_source": "measured in this run: DFMA chains over all SMs "
+                               "(ifgf_measure_fp64_peak); MEASURED_PEAKS.json has no FP64 figure",
+                "per_kernel": per_kernel,
+                "whole_apply_frac": work.total_flops / t_apply / 1e12 / fp64_peak}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cn, ct, kind, cores, sample = cpu_sample_run(1, 0)
+        cpu = {"value": cn / statistics.mean(ct) / 1e6, "unit": UNIT, "cores": cores,
+               "kind": kind, "sample": sample, "seconds": statistics.mean(ct)}
+
+    if rank == 0:
+        r0 = reps[-1]
+        line = {
+            "metric": METRIC, "value": world * n / t_step / 1e6, "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": t_step * 1e3,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (seeded generator, DESIGN.md Inputs)",
+            "config": {"workload": f"{cfgd.label} (BASELINE configs[1]), orders (3,5,5), "
+                                   f"depth {info.depth}",
+                       "n": n, "kappa": cfgd.kappa, "orders": [3, 5, 5], "depth": info.depth,
+                       "parallelism": f"replicas x{world}" if world > 1 else "1 GPU",
+                       "l2": "flushed between steps (256 MB write)",
+                       "step": "Problem::build on device + apply (device-resident inputs)"},
+            "apply_only": {"value": world * n / t_apply / 1e6, "unit": UNIT,
+                           "ms_per_step": t_apply * 1e3,
+                           "stages_ms_overlapped": {k: getattr(arep.seconds, k) * 1e3 for k in
+                                                    ("singular", "level_d", "interpolation",
+                                                     "propagation")},
+                           "stages_ms_serial": {k: v * 1e3 for k, v in st.items()}},
+            "setup_ms": (t_step - t_apply) * 1e3,
+            "gpu_launches": int(r0.gpu_launches),
+            "e2e": e2e,
+            "roofline": roofline,
+            "cpu_baseline": cpu,
+            "clocks": clocks.summary(),
+            "work": work.as_dict(),
+            "step_ms_all": step_ms,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        torch.distributed.destroy_process_group()
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

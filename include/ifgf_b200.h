@@ -125,6 +125,7 @@ typedef struct ifgf_plan_info {
   double h[IFGF_MAX_LEVELS];
   double setup_seconds;
   size_t device_bytes;
+  size_t setup_launches; /* our kernels launched by the plan's setup */
 } ifgf_plan_info;
 
 int ifgf_plan_get_info(const ifgf_plan* plan, ifgf_plan_info* info);
@@ -181,6 +182,10 @@ int ifgf_error_at_indices(size_t n, const double* x1, const double* x2, const do
                           const double* a_re, const double* a_im, const double* i_re,
                           const double* i_im, int kernel_kind, double wavenumber,
                           const uint32_t* idx, size_t m, int device, double* eps);
+
+/* ---- measurement helper: FP64 FMA-pipe peak of the device (TFLOP/s,
+ * best of 10 launches of independent DFMA chains over all SMs). ---- */
+int ifgf_measure_fp64_peak(int device, double* tflops, double* ms);
 
 /* ---- seeded synthetic inputs; host only ----
  * shape 0: unit sphere (normalised Gaussians); 1: spheroid (1,1,c), area

@@ -39,7 +39,8 @@ class CPlanInfo(C.Structure):
                 ("boxes", C.c_size_t * MAX_LEVELS), ("cones", C.c_size_t * MAX_LEVELS),
                 ("nbr_entries", C.c_size_t * MAX_LEVELS),
                 ("cousin_entries", C.c_size_t * MAX_LEVELS), ("h", C.c_double * MAX_LEVELS),
-                ("setup_seconds", C.c_double), ("device_bytes", C.c_size_t)]
+                ("setup_seconds", C.c_double), ("device_bytes", C.c_size_t),
+                ("setup_launches", C.c_size_t)]
 
 
 _dp = np.ctypeslib.ndpointer(dtype=np.float64, flags="C_CONTIGUOUS")
@@ -89,6 +90,8 @@ SIGNATURES = {
     "ifgf_sample_indices": (C.c_int, [_sz, _sz, C.c_uint64, _vp]),
     "ifgf_error_at_indices": (C.c_int, [_sz, _vp, _vp, _vp, _vp, _vp, _vp, _vp, C.c_int,
                                         C.c_double, _vp, _sz, C.c_int, C.POINTER(C.c_double)]),
+    "ifgf_measure_fp64_peak": (C.c_int, [C.c_int, C.POINTER(C.c_double),
+                                         C.POINTER(C.c_double)]),
     "ifgf_generate": (C.c_int, [_sz, C.c_int, C.c_double, C.c_int, C.c_uint64, _vp, _vp, _vp,
                                 _vp, _vp]),
 }

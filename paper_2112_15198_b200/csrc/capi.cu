@@ -148,6 +148,7 @@ ifgf_plan* new_plan(size_t n, int kind, double wavenumber, const ifgf_params* p)
 
 void finish_create(ifgf_plan* P, const double* dx, const double* dy, const double* dz) {
   build_plan(P, dx, dy, dz);
+  P->setup_launches = P->launches;
   P->ar = P->alloc<double>(P->n);
   P->ai = P->alloc<double>(P->n);
   P->ir = P->alloc<double>(P->n);
@@ -593,6 +594,7 @@ int ifgf_plan_get_info(const ifgf_plan* P, ifgf_plan_info* info) {
     }
     info->setup_seconds = P->setup_seconds;
     info->device_bytes = P->bytes;
+    info->setup_launches = P->setup_launches;
   });
 }
 

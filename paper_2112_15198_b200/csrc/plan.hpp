@@ -123,6 +123,7 @@ struct ifgf_plan {
   double setup_seconds = 0.0;
   size_t launches = 0;  // kernels launched by this plan since the last reset
   bool serial = false;  // IFGF_OPT_SERIAL
+  size_t setup_launches = 0;
 
   template <class T>
   T* alloc(size_t count) {
