@@ -156,7 +156,9 @@ int ifgf_plan_write_blocks(ifgf_plan* plan, int d, const double* re, const doubl
 int ifgf_plan_read_result(ifgf_plan* plan, int sorted_order, double* i_re, double* i_im);
 /* Device-side block exchange for multi-GPU: pack/unpack the blocks of the
  * listed cone ordinals (device u32 array) to/from a contiguous device buffer
- * of m * 2P doubles. */
+ * of m * 2 * Pst doubles, Pst = p_s * PL, PL = p_theta * p_phi rounded up to
+ * even (the device block layout; see ifgf_plan_block_stride). */
+int ifgf_plan_block_stride(const ifgf_plan* plan);
 int ifgf_plan_pack_blocks(ifgf_plan* plan, int d, const uint32_t* d_cones, size_t m,
                           double* d_buf, void* stream);
 int ifgf_plan_unpack_blocks(ifgf_plan* plan, int d, const uint32_t* d_cones, size_t m,

@@ -10,7 +10,7 @@ import os
 import numpy as np
 
 PKG_DIR = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(PKG_DIR, "libifgf_b200.so")
+LIB_PATH = os.environ.get("IFGF_B200_LIB") or os.path.join(PKG_DIR, "libifgf_b200.so")
 HEADER_PATH = os.path.join(os.path.dirname(PKG_DIR), "include", "ifgf_b200.h")
 
 IFGF_OK, IFGF_EINVAL, IFGF_EDOMAIN, IFGF_ELOGIC, IFGF_ERUNTIME = range(5)
@@ -80,6 +80,7 @@ SIGNATURES = {
     "ifgf_plan_read_blocks": (C.c_int, [_vp, C.c_int, _vp, _vp]),
     "ifgf_plan_write_blocks": (C.c_int, [_vp, C.c_int, _vp, _vp]),
     "ifgf_plan_read_result": (C.c_int, [_vp, C.c_int, _vp, _vp]),
+    "ifgf_plan_block_stride": (C.c_int, [_vp]),
     "ifgf_plan_pack_blocks": (C.c_int, [_vp, C.c_int, _vp, _sz, _vp, _vp]),
     "ifgf_plan_unpack_blocks": (C.c_int, [_vp, C.c_int, _vp, _sz, _vp, _vp]),
     "ifgf_plan_partition": (C.c_int, [_vp, C.c_int, _vp, _vp, _vp]),

@@ -95,6 +95,8 @@ InterpConsts make_consts(const ifgf_params* p) {
   K.pt = p->p_theta;
   K.pp = p->p_phi;
   K.P = K.ps * K.pt * K.pp;
+  K.PL = (K.pt * K.pp + 1) & ~1;
+  K.Pst = K.ps * K.PL;
   const auto fill = [](int q, double* nodes, double* M) {
     for (int j = 0; j < q; ++j) nodes[j] = std::cos(kPi * (2.0 * j + 1.0) / (2.0 * q));
     for (int k = 0; k < q; ++k) {
@@ -161,7 +163,7 @@ void finish_create(ifgf_plan* P, const double* dx, const double* dy, const doubl
 void ensure_slots(ifgf_plan* P) {
   if (P->n_slots) return;
   const int D = P->depth;
-  const size_t bpc = (size_t)P->K.P * sizeof(double2);
+  const size_t bpc = (size_t)P->K.Pst * sizeof(double2);
   size_t total = 0, mx = 0;
   for (int d = 3; d <= D; ++d) {
     total += P->lv[d].nc;
@@ -170,16 +172,16 @@ void ensure_slots(ifgf_plan* P) {
   size_t fr = 0, tot = 0;
   IFGF_CUDA(cudaMemGetInfo(&fr, &tot));
   if (total * bpc < fr / 2) {
-    double2* base = P->alloc<double2>(total * P->K.P + 1);
+    double2* base = P->alloc<double2>(total * P->K.Pst + 2);
     size_t off = 0;
     for (int d = 3; d <= D; ++d) {
-      P->slots[d] = base + off * P->K.P;
+      P->slots[d] = base + off * P->K.Pst;
       off += P->lv[d].nc;
     }
     P->n_slots = D - 2;
   } else {
-    double2* a = P->alloc<double2>(mx * P->K.P + 1);
-    double2* b = P->alloc<double2>(mx * P->K.P + 1);
+    double2* a = P->alloc<double2>(mx * P->K.Pst + 2);
+    double2* b = P->alloc<double2>(mx * P->K.Pst + 2);
     for (int d = 3; d <= D; ++d) P->slots[d] = (d % 2) ? a : b;
     P->n_slots = 2;
   }
@@ -293,9 +295,9 @@ void apply_device(ifgf_plan* P, const double* a_re, const double* a_im, double* 
 double2* stage_blocks(ifgf_plan* P, int d) {
   if (d < 3 || d > P->depth) throw Error(IFGF_EINVAL, "level out of range");
   if (!P->stage_blocks[d]) {
-    P->stage_blocks[d] = P->alloc<double2>((size_t)P->lv[d].nc * P->K.P + 1);
+    P->stage_blocks[d] = P->alloc<double2>((size_t)P->lv[d].nc * P->K.Pst + 2);
     IFGF_CUDA(cudaMemsetAsync(P->stage_blocks[d], 0,
-                              ((size_t)P->lv[d].nc * P->K.P + 1) * sizeof(double2), P->s_main));
+                              ((size_t)P->lv[d].nc * P->K.Pst + 2) * sizeof(double2), P->s_main));
   }
   return P->stage_blocks[d];
 }
@@ -360,7 +362,7 @@ __global__ void k_need_interp(const __grid_constant__ LevelDev L, const uint32_t
   for (uint32_t k = L.cous_off[b]; k < L.cous_off[b + 1]; ++k) {
     const uint32_t cb = L.cous[k];
     uint32_t g;
-    const int e = cone_of_point(L, L.cx[cb], L.cy[cb], L.cz[cb], xs[i], ys[i], zs[i], g);
+    const int e = cone_of_point_fast(L, L.cx[cb], L.cy[cb], L.cz[cb], xs[i], ys[i], zs[i], g);
     if (e) {
       raise_err(err, e);
       return;
@@ -390,7 +392,7 @@ __global__ void k_need_prop(const __grid_constant__ LevelDev L, const __grid_con
   node_position(sg, U.rad, U.cx[pb], U.cy[pb], U.cz[pb], K.ns[js], K.nt[jt], K.np[jp], x, y, z);
   for (uint32_t cb = U.child_begin[pb]; cb < U.child_begin[pb + 1]; ++cb) {
     uint32_t g;
-    const int e = cone_of_point(L, L.cx[cb], L.cy[cb], L.cz[cb], x, y, z, g);
+    const int e = cone_of_point_fast(L, L.cx[cb], L.cy[cb], L.cz[cb], x, y, z, g);
     if (e) {
       raise_err(err, e);
       return;
@@ -735,12 +737,15 @@ int ifgf_plan_read_blocks(ifgf_plan* P, int d, double* re, double* im) {
   return guarded([&] {
     if (!P || !re || !im) throw Error(IFGF_EINVAL, "null argument");
     const double2* blk = stage_blocks(P, d);
-    const size_t cnt = (size_t)P->lv[d].nc * P->K.P;
-    const auto h = d2h(blk, cnt, P->s_main);
-    for (size_t k = 0; k < cnt; ++k) {
-      re[k] = h[k].x;
-      im[k] = h[k].y;
-    }
+    const size_t nc = P->lv[d].nc, Pn = P->K.P, Ps = P->K.Pst;
+    const auto h = d2h(blk, nc * Ps, P->s_main);
+    const size_t plane = (size_t)P->K.pt * P->K.pp, PL = P->K.PL;
+    for (size_t q = 0; q < nc; ++q)
+      for (size_t k = 0; k < Pn; ++k) {
+        const size_t dk = (k / plane) * PL + k % plane;
+        re[q * Pn + k] = h[q * Ps + dk].x;
+        im[q * Pn + k] = h[q * Ps + dk].y;
+      }
   });
 }
 
@@ -748,10 +753,13 @@ int ifgf_plan_write_blocks(ifgf_plan* P, int d, const double* re, const double* 
   return guarded([&] {
     if (!P || !re || !im) throw Error(IFGF_EINVAL, "null argument");
     double2* blk = stage_blocks(P, d);
-    const size_t cnt = (size_t)P->lv[d].nc * P->K.P;
-    std::vector<double2> h(cnt);
-    for (size_t k = 0; k < cnt; ++k) h[k] = make_double2(re[k], im[k]);
-    IFGF_CUDA(cudaMemcpyAsync(blk, h.data(), cnt * sizeof(double2), cudaMemcpyHostToDevice,
+    const size_t nc = P->lv[d].nc, Pn = P->K.P, Ps = P->K.Pst;
+    std::vector<double2> h(nc * Ps, make_double2(0.0, 0.0));
+    const size_t plane = (size_t)P->K.pt * P->K.pp, PL = P->K.PL;
+    for (size_t q = 0; q < nc; ++q)
+      for (size_t k = 0; k < Pn; ++k)
+        h[q * Ps + (k / plane) * PL + k % plane] = make_double2(re[q * Pn + k], im[q * Pn + k]);
+    IFGF_CUDA(cudaMemcpyAsync(blk, h.data(), nc * Ps * sizeof(double2), cudaMemcpyHostToDevice,
                               P->s_main));
     IFGF_CUDA(cudaStreamSynchronize(P->s_main));
   });
@@ -774,6 +782,8 @@ int ifgf_plan_read_result(ifgf_plan* P, int sorted, double* i_re, double* i_im) 
     IFGF_CUDA(cudaStreamSynchronize(P->s_main));
   });
 }
+
+int ifgf_plan_block_stride(const ifgf_plan* P) { return P ? P->K.Pst : 0; }
 
 int ifgf_plan_pack_blocks(ifgf_plan* P, int d, const uint32_t* d_cones, size_t m, double* d_buf,
                           void* stream) {

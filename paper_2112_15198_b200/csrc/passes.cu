@@ -10,6 +10,8 @@
 //
 // Every work item writes only its own output slot, in a fixed order, so the
 // result is bitwise reproducible run to run (parallel.hpp:17-19 contract).
+#include <algorithm>
+
 #include "plan.hpp"
 
 namespace ifgf_b200 {
@@ -37,6 +39,14 @@ bool dispatch_orders(int ps, int pt, int pp, F&& f) {
 }
 
 inline unsigned blocks_for(size_t n, int t) { return (unsigned)((n + t - 1) / t); }
+
+// Occupancy targets (CTAs per SM) handed to __launch_bounds__; tuned on B200.
+#ifndef IFGF_PROP_MINB
+#define IFGF_PROP_MINB 2
+#endif
+#ifndef IFGF_INTERP_MINB
+#define IFGF_INTERP_MINB 4
+#endif
 
 // ---------------------------------------------------------------- K1 near field
 template <bool LAP>
@@ -125,68 +135,77 @@ __global__ void __launch_bounds__(320)
     sv[c * P + m] = make_double2(sr, si);
   }
   __syncthreads();
-  fit_cones<PS, PT, PP>(K, sv, st, ncon, out + (size_t)q0 * P, err);
+  fit_cones<PS, PT, PP>(K, sv, st, ncon, out + (size_t)q0 * BlockLayout<PS, PT, PP>::Pst, err);
 }
 
 // ------------------------------------------------------------ K3 propagation
+// One CTA = `groups` consecutive groups of `cpb` parent cones (cone order is
+// box-major, so a CTA mostly stays inside one parent box and re-reads the
+// same child blocks from L1); thread = (cone, node).
 template <int PS, int PT, int PP, bool LAP>
-__global__ void __launch_bounds__(320)
+__global__ void __launch_bounds__(320, IFGF_PROP_MINB)
     k_propagate(const __grid_constant__ LevelDev U, const __grid_constant__ LevelDev L,
                 const __grid_constant__ InterpConsts K, double kappa, uint32_t qb, uint32_t qe,
-                int cpb, const double2* __restrict__ child, double2* parent, int* err) {
+                int cpb, int groups, const double2* __restrict__ child, double2* parent,
+                int* err) {
   constexpr int P = PS * PT * PP;
   extern __shared__ double2 smem[];
   double2* sv = smem;
   double2* st = smem + cpb * P;
-  const uint32_t q0 = qb + blockIdx.x * cpb;
-  const int ncon = (int)min((uint32_t)cpb, qe - q0);
   const int c = threadIdx.x / P, m = threadIdx.x % P;
-  if (c < ncon) {
-    const uint32_t q = q0 + c;
-    const uint32_t pb = U.cone_box[q];
-    const int jp = m % PP, jt = (m / PP) % PT, js = m / (PP * PT);
-    const SegMid sg = segment_mid(U, U.cone_gamma[q]);
-    const double pcx = U.cx[pb], pcy = U.cy[pb], pcz = U.cz[pb];
-    double x, y, z;
-    node_position(sg, U.rad, pcx, pcy, pcz, K.ns[js], K.nt[jt], K.np[jp], x, y, z);
-    const double rp = norm_rn(x - pcx, y - pcy, z - pcz);
-    double acr = 0.0, aci = 0.0;
-    const uint32_t c0 = U.child_begin[pb], c1 = U.child_begin[pb + 1];
-    for (uint32_t cb = c0; cb < c1; ++cb) {
-      Loc o;
-      const int e = locate(L, L.cx[cb], L.cy[cb], L.cz[cb], x, y, z, o);
-      if (e) {
-        raise_err(err, e);
-        break;
+  const int jp = m % PP, jt = (m / PP) % PT, js = m / (PP * PT);
+  for (int g = 0; g < groups; ++g) {
+    const uint32_t q0 = qb + ((uint32_t)blockIdx.x * groups + g) * cpb;
+    if (q0 >= qe) break;
+    const int ncon = (int)min((uint32_t)cpb, qe - q0);
+    if (c < ncon) {
+      const uint32_t q = q0 + c;
+      const uint32_t pb = U.cone_box[q];
+      const SegMid sg = segment_mid(U, U.cone_gamma[q]);
+      const double pcx = U.cx[pb], pcy = U.cy[pb], pcz = U.cz[pb];
+      double x, y, z;
+      node_position(sg, U.rad, pcx, pcy, pcz, K.ns[js], K.nt[jt], K.np[jp], x, y, z);
+      const double ux = x - pcx, uy = y - pcy, uz = z - pcz;
+      const double rp = sqrt(fma(uz, uz, fma(uy, uy, ux * ux)));
+      double acr = 0.0, aci = 0.0;
+      const uint32_t c0 = U.child_begin[pb], c1 = U.child_begin[pb + 1];
+      for (uint32_t cb = c0; cb < c1; ++cb) {
+        Loc o;
+        const int e = locate_fast(L, L.cx[cb], L.cy[cb], L.cz[cb], x, y, z, o);
+        if (e) {
+          raise_err(err, e);
+          break;
+        }
+        const uint32_t cq = find_cone(L, cb, o.gamma);
+        if (cq == 0xffffffffu) {
+          raise_err(err, kErrPropCover);
+          break;
+        }
+        double vr, vi;
+        eval_block<PS, PT, PP>(child + (size_t)cq * BlockLayout<PS, PT, PP>::Pst, o.ts, o.tt, o.tp, vr, vi);
+        const double ratio = rp * o.rinv;
+        if (LAP) {
+          acr = fma(vr, ratio, acr);
+          aci = fma(vi, ratio, aci);
+        } else {
+          double sn, cn;
+          sincos_fast(kappa * (o.r - rp), sn, cn);
+          const double tr = ratio * cn, ti = ratio * sn;
+          acr = fma(vr, tr, fma(-vi, ti, acr));
+          aci = fma(vr, ti, fma(vi, tr, aci));
+        }
       }
-      const uint32_t cq = find_cone(L, cb, o.gamma);
-      if (cq == 0xffffffffu) {
-        raise_err(err, kErrPropCover);
-        break;
-      }
-      double vr, vi;
-      eval_block<PS, PT, PP>(child + (size_t)cq * P, o.ts, o.tt, o.tp, vr, vi);
-      const double ratio = rp / o.r;
-      if (LAP) {
-        acr = fma(vr, ratio, acr);
-        aci = fma(vi, ratio, aci);
-      } else {
-        double sn, cn;
-        sincos_fast(kappa * (o.r - rp), sn, cn);
-        const double tr = ratio * cn, ti = ratio * sn;
-        acr = fma(vr, tr, fma(-vi, ti, acr));
-        aci = fma(vr, ti, fma(vi, tr, aci));
-      }
+      sv[c * P + m] = make_double2(acr, aci);
     }
-    sv[c * P + m] = make_double2(acr, aci);
+    __syncthreads();
+    fit_cones<PS, PT, PP>(K, sv, st, ncon, parent + (size_t)q0 * BlockLayout<PS, PT, PP>::Pst, err);
+    __syncthreads();
   }
-  __syncthreads();
-  fit_cones<PS, PT, PP>(K, sv, st, ncon, parent + (size_t)q0 * P, err);
 }
 
 // ---------------------------------------------------------- K4 interpolation
 template <int PS, int PT, int PP, bool LAP>
-__global__ void __launch_bounds__(128)
+__global__ void __launch_bounds__(128, IFGF_INTERP_MINB)
     k_interp(const __grid_constant__ LevelDev L, const uint32_t* __restrict__ ptbox, const double* __restrict__ xs,
              const double* __restrict__ ys, const double* __restrict__ zs, double kappa,
              size_t b0, size_t e0, const double2* __restrict__ blocks, double* ir, double* ii,
@@ -201,7 +220,7 @@ __global__ void __launch_bounds__(128)
   for (uint32_t k = k0; k < k1; ++k) {
     const uint32_t cb = L.cous[k];
     Loc o;
-    const int e = locate(L, L.cx[cb], L.cy[cb], L.cz[cb], x, y, z, o);
+    const int e = locate_fast(L, L.cx[cb], L.cy[cb], L.cz[cb], x, y, z, o);
     if (e) {
       raise_err(err, e);
       return;
@@ -212,8 +231,8 @@ __global__ void __launch_bounds__(128)
       return;
     }
     double vr, vi;
-    eval_block<PS, PT, PP>(blocks + (size_t)q * P, o.ts, o.tt, o.tp, vr, vi);
-    const double inv = kQuarterInvPi / o.r;
+    eval_block<PS, PT, PP>(blocks + (size_t)q * BlockLayout<PS, PT, PP>::Pst, o.ts, o.tt, o.tp, vr, vi);
+    const double inv = kQuarterInvPi * o.rinv;
     if (LAP) {
       acr = fma(vr, inv, acr);
       aci = fma(vi, inv, aci);
@@ -255,11 +274,11 @@ __global__ void k_scatter_result(const uint32_t* __restrict__ perm, const double
 }
 
 __global__ void k_pack(const double2* __restrict__ blocks, const uint32_t* __restrict__ cones,
-                       size_t m, int P, double2* buf, int unpack, double2* blocks_out) {
+                       size_t m, int Pst, double2* buf, int unpack, double2* blocks_out) {
   const size_t t = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
-  if (t >= m * P) return;
-  const size_t j = t / P, k = t % P;
-  const size_t g = (size_t)cones[j] * P + k;
+  if (t >= m * Pst) return;
+  const size_t j = t / Pst, k = t % Pst;
+  const size_t g = (size_t)cones[j] * Pst + k;
   if (unpack) blocks_out[g] = buf[t];
   else buf[t] = blocks[g];
 }
@@ -331,14 +350,16 @@ void launch_propagation(ifgf_plan* P, int d, uint32_t qb, uint32_t qe, const dou
   dispatch_orders(K.ps, K.pt, K.pp, [&](auto o) {
     using O = decltype(o);
     const int cpb = cones_per_cta(O::P);
-    const unsigned grid = blocks_for(qe - qb, cpb);
+    // enough CTAs for ~8 per SM, at most 8 groups each
+    int groups = (int)std::min<size_t>(8, std::max<size_t>(1, (qe - qb) / ((size_t)cpb * 148 * 8)));
+    const unsigned grid = blocks_for(qe - qb, cpb * groups);
     const size_t smem = 2 * (size_t)cpb * O::P * sizeof(double2);
     if (P->kappa == 0.0)
       k_propagate<O::PS, O::PT, O::PP, true><<<grid, threads_for(cpb, O::P), smem, s>>>(
-          U.dev(), L.dev(), K, P->kappa, qb, qe, cpb, child, parent, P->err);
+          U.dev(), L.dev(), K, P->kappa, qb, qe, cpb, groups, child, parent, P->err);
     else
       k_propagate<O::PS, O::PT, O::PP, false><<<grid, threads_for(cpb, O::P), smem, s>>>(
-          U.dev(), L.dev(), K, P->kappa, qb, qe, cpb, child, parent, P->err);
+          U.dev(), L.dev(), K, P->kappa, qb, qe, cpb, groups, child, parent, P->err);
   });
   ++P->launches;
 }
@@ -364,7 +385,7 @@ void launch_interpolation(ifgf_plan* P, int d, size_t b, size_t e, const double2
 void launch_pack(ifgf_plan* P, const double2* blocks, const uint32_t* cones, size_t m,
                  double* buf, int unpack, double2* blocks_out, cudaStream_t s) {
   if (!m) return;
-  const int Pn = P->K.P;
+  const int Pn = P->K.Pst;
   k_pack<<<blocks_for(m * Pn, 256), 256, 0, s>>>(blocks, cones, m, Pn,
                                                  reinterpret_cast<double2*>(buf), unpack,
                                                  blocks_out);

@@ -57,6 +57,7 @@ struct Level {
   uint64_t* bits = nullptr;
   uint32_t* rank = nullptr;
   size_t nwords = 0;
+  const double4* trig = nullptr;
 
   LevelDev dev() const {
     LevelDev v;
@@ -92,6 +93,7 @@ struct Level {
     v.box_cone = box_cone;
     v.bits = bits;
     v.rank = rank;
+    v.trig = trig;
     return v;
   }
 };

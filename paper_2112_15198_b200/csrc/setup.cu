@@ -22,6 +22,7 @@
 #include <algorithm>
 #include <chrono>
 #include <cmath>
+#include <vector>
 
 #include "plan.hpp"
 
@@ -282,7 +283,7 @@ __global__ void k_mark_points(const __grid_constant__ LevelDev L, const uint32_t
   for (uint32_t ci = L.cous_off[b]; ci < L.cous_off[b + 1]; ++ci) {
     const uint32_t cb = L.cous[ci];
     uint32_t g;
-    const int e = cone_of_point(L, L.cx[cb], L.cy[cb], L.cz[cb], x, y, z, g);
+    const int e = cone_of_point_fast(L, L.cx[cb], L.cy[cb], L.cz[cb], x, y, z, g);
     if (e) {
       raise_err(err, e);
       return;
@@ -306,7 +307,7 @@ __global__ void k_mark_nodes(const __grid_constant__ LevelDev L, const __grid_co
   node_position(sm, U.rad, U.cx[pb], U.cy[pb], U.cz[pb], K.ns[js], K.nt[jt], K.np[jp], x, y, z);
   for (uint32_t cb = U.child_begin[pb]; cb < U.child_begin[pb + 1]; ++cb) {
     uint32_t g;
-    const int e = cone_of_point(L, L.cx[cb], L.cy[cb], L.cz[cb], x, y, z, g);
+    const int e = cone_of_point_fast(L, L.cx[cb], L.cy[cb], L.cz[cb], x, y, z, g);
     if (e) {
       raise_err(err, e);
       return;
@@ -418,6 +419,23 @@ void build_plan(ifgf_plan* P, const double* d_x, const double* d_y, const double
     if (rc) throw Error(rc, ifgf_last_error());
   }
   P->depth = D;
+  {
+    // angle seed table for the fast locate (ifgf_common.cuh fast_angles)
+    std::vector<double4> trig(kTrigPhi + kTrigTheta + 1);
+    for (int k = 0; k < kTrigPhi; ++k) {
+      const double a = k * (2.0 * kPi / kTrigPhi);
+      trig[k] = make_double4(std::cos(a), std::sin(a), a, 0.0);
+    }
+    for (int k = 0; k <= kTrigTheta; ++k) {
+      const double a = k * (kPi / kTrigTheta);
+      trig[kTrigPhi + k] = make_double4(std::cos(a), std::sin(a), a, 0.0);
+    }
+    double4* d_trig = P->alloc<double4>(trig.size());
+    IFGF_CUDA(cudaMemcpyAsync(d_trig, trig.data(), trig.size() * sizeof(double4),
+                              cudaMemcpyHostToDevice, s));
+    for (int d = 0; d < IFGF_MAX_LEVELS; ++d) P->lv[d].trig = d_trig;
+    IFGF_CUDA(cudaStreamSynchronize(s));  // trig lives on the stack until copied
+  }
   {
     // bitmap indices of the coarsest cone level must fit the u32 gamma
     const double G3 = (double)P->params.base_s * P->params.base_theta * P->params.base_phi *
