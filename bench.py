@@ -294,8 +294,8 @@ def run_ours(args):
     dk = per_kernel[dom]
     roofline = {"bound": "fp64", "kernel": dom, "achieved": dk["tflops"], "peak": fp64_peak,
                 "unit": "TFLOP/s", "frac": dk["frac_fp64"], "traffic": traffic,
-                "peak_source": "measured in this run: DFMA chains over all SMs "
-                               "(ifgf_measure_fp64_peak); MEASURED_PEAKS.json has no FP64 figure",
+                "peak_source": "measured in this run: best of DFMA chains and mma.sync m8n8k4 f64 "
+                               "over all SMs (ifgf_measure_fp64_peak); MEASURED_PEAKS.json has no FP64 figure",
                 "per_kernel": per_kernel,
                 "whole_apply_frac": work.total_flops / t_apply / 1e12 / fp64_peak}
 

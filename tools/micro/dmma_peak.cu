@@ -1,0 +1,59 @@
+// FP64 tensor-core (mma.sync m8n8k4 f64) vs DFMA throughput on this device.
+#include <cstdio>
+#include <cuda_runtime.h>
+
+__global__ void k_dmma(double* out, int iters) {
+  double a = 1.0 + threadIdx.x * 1e-9, b = 0.5;
+  double c[8][2];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) c[i][0] = c[i][1] = 0.0;
+  for (int it = 0; it < iters; ++it) {
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+      asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+                   : "+d"(c[i][0]), "+d"(c[i][1]) : "d"(a), "d"(b));
+  }
+  double s = 0;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) s += c[i][0] + c[i][1];
+  if (s == 1.2345) out[0] = s;
+}
+
+__global__ void k_dfma(double* out, int iters) {
+  double v[8];
+#pragma unroll
+  for (int c = 0; c < 8; ++c) v[c] = threadIdx.x * 1e-3 + c;
+  for (int i = 0; i < iters; ++i)
+#pragma unroll
+    for (int c = 0; c < 8; ++c) v[c] = fma(v[c], 0.9999999, 1e-7);
+  double s = 0;
+#pragma unroll
+  for (int c = 0; c < 8; ++c) s += v[c];
+  if (s == 1.2345) out[0] = s;
+}
+
+int main() {
+  cudaDeviceProp p;
+  cudaGetDeviceProperties(&p, 0);
+  double* o;
+  cudaMalloc(&o, 8);
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  const int blocks = p.multiProcessorCount * 4, threads = 256, iters = 4096;
+  for (int w = 0; w < 3; ++w) { k_dmma<<<blocks, threads>>>(o, iters); k_dfma<<<blocks, threads>>>(o, iters); }
+  float best_m = 1e9, best_f = 1e9, t;
+  for (int r = 0; r < 5; ++r) {
+    cudaEventRecord(e0); k_dmma<<<blocks, threads>>>(o, iters); cudaEventRecord(e1); cudaEventSynchronize(e1);
+    cudaEventElapsedTime(&t, e0, e1); best_m = t < best_m ? t : best_m;
+    cudaEventRecord(e0); k_dfma<<<blocks, threads>>>(o, iters); cudaEventRecord(e1); cudaEventSynchronize(e1);
+    cudaEventElapsedTime(&t, e0, e1); best_f = t < best_f ? t : best_f;
+  }
+  const double warps = blocks * threads / 32.0;
+  const double mma_flops = warps * iters * 8 * 8 * 8 * 4 * 2.0;   // 256 MAC per mma
+  const double fma_flops = blocks * (double)threads * iters * 8 * 2.0;
+  printf("DMMA m8n8k4: %.2f TFLOP/s   DFMA: %.2f TFLOP/s  (%s, %d SMs) err=%s\n",
+         mma_flops / (best_m * 1e-3) / 1e12, fma_flops / (best_f * 1e-3) / 1e12, p.name,
+         p.multiProcessorCount, cudaGetErrorString(cudaGetLastError()));
+  return 0;
+}
