@@ -96,8 +96,11 @@ void ifgf_plan_destroy(ifgf_plan* plan);
 
 /* Plan options.  IFGF_OPT_SERIAL = 1 runs every apply kernel on one stream
  * (no near-field / interpolation overlap) so per-pass event times are
- * exclusive; used for per-kernel roofline measurement. */
-enum { IFGF_OPT_SERIAL = 1 };
+ * exclusive; used for per-kernel roofline measurement.  IFGF_OPT_NODE_PROP = 1
+ * disables the precomputed (gamma, octant) propagation geometry (per-node
+ * locate in K3).  IFGF_OPT_PROP_MMA = 1 selects the FP64 tensor-core (DMMA)
+ * batched-GEMM propagation instead of the per-node evaluation. */
+enum { IFGF_OPT_SERIAL = 1, IFGF_OPT_NODE_PROP = 2, IFGF_OPT_PROP_MMA = 3 };
 int ifgf_plan_set_option(ifgf_plan* plan, int option, int value);
 
 /* ---- operator application; i_* in the caller's original point order ---- */

@@ -501,6 +501,8 @@ int ifgf_plan_set_option(ifgf_plan* P, int option, int value) {
   return guarded([&] {
     if (!P) throw Error(IFGF_EINVAL, "null plan");
     if (option == IFGF_OPT_SERIAL) P->serial = value != 0;
+    else if (option == IFGF_OPT_NODE_PROP) P->force_node_prop = value != 0;
+    else if (option == IFGF_OPT_PROP_MMA) P->prop_mode = value != 0 ? 1 : 0;
     else throw Error(IFGF_EINVAL, "unknown option");
   });
 }

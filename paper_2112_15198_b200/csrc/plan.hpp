@@ -98,6 +98,33 @@ struct Level {
   }
 };
 
+// Box-independent propagation geometry for child level d (parent level d-1).
+// A parent cone's nodes seen from a child centre depend only on the parent
+// segment gamma and the child's octant, so the child cone, the local
+// Chebyshev coordinates and the re-centring factor of every (gamma, octant,
+// node) are computed once per plan.  Entries within kIdxMargin of a segment
+// boundary are flagged and recomputed per box exactly (the reference's
+// absolute-coordinate rounding could move them).
+struct PropTiles {
+  bool enabled = false;
+  uint32_t ngamma = 0;          // distinct parent gammas in use
+  uint32_t* cone_gidx = nullptr;   // parent cone -> gamma index
+  uint32_t* gamma_of = nullptr;    // gamma index -> parent gamma
+  // entries [(gidx * 8 + octant) * P + node]
+  double* e_t = nullptr;        // ts, tt, tp
+  double2* e_T = nullptr;       // transfer factor (rp/rc) e^{i kappa (rc - rp)}
+  uint32_t* e_gc = nullptr;     // child gamma; bit 31 = flagged (exact per-box path)
+  // row tiles: 8 nodes sharing one child gamma; CSR over (gidx * 8 + octant)
+  uint32_t* rt_off = nullptr;
+  uint4* rt = nullptr;          // {child gamma, nodes 0-3 (u8), nodes 4-7 (u8), unused}
+  uint32_t* fl_off = nullptr;   // flagged nodes CSR over tiles
+  uint16_t* fl_node = nullptr;
+  // CTA chunks of <= kChunk parent cones sharing one gamma
+  uint32_t nchunks = 0;
+  uint32_t* qsorted = nullptr;
+  uint32_t* chunk_start = nullptr;
+};
+
 }  // namespace ifgf_b200
 
 struct ifgf_plan {
@@ -118,6 +145,7 @@ struct ifgf_plan {
   ifgf_b200::Level lv[IFGF_MAX_LEVELS];
   double2* stage_blocks[IFGF_MAX_LEVELS] = {};  // pass-level API storage
   double2* slots[IFGF_MAX_LEVELS] = {};         // apply rotation
+  ifgf_b200::PropTiles tiles[IFGF_MAX_LEVELS];  // index = child level d
   int n_slots = 0;
   size_t slot_cap = 0;
   std::vector<void*> allocs;
@@ -125,6 +153,8 @@ struct ifgf_plan {
   double setup_seconds = 0.0;
   size_t launches = 0;  // kernels launched by this plan since the last reset
   bool serial = false;  // IFGF_OPT_SERIAL
+  bool force_node_prop = false;  // IFGF_OPT_NODE_PROP: per-node K3 only
+  int prop_mode = 0;  // IFGF_OPT_PROP_MMA: 0 tiles per node, 1 tensor-core GEMM
   size_t setup_launches = 0;
 
   template <class T>
@@ -155,6 +185,11 @@ void launch_interpolation(ifgf_plan* P, int d, size_t b, size_t e, const double2
 void launch_pack(ifgf_plan* P, const double2* blocks, const uint32_t* cones, size_t m,
                  double* buf, int unpack, double2* blocks_out, cudaStream_t s);
 bool orders_supported(int ps, int pt, int pp);
+// propagate_mma.cu
+void build_prop_tiles(ifgf_plan* P, int d, void* (*scratch)(void*, size_t), void* sctx);
+void launch_mark_nodes_tiles(ifgf_plan* P, int d, uint64_t* bits);
+bool launch_propagation_mma(ifgf_plan* P, int d, const double2* child, double2* parent,
+                            cudaStream_t s);
 // direct.cu
 void direct_sums(const double* x, const double* y, const double* z, const double* ar,
                  const double* ai, size_t n, double kappa, const uint32_t* targets, size_t m,

@@ -1,0 +1,716 @@
+// propagate_mma.cu -- K3 as batched FP64 tensor-core GEMMs.
+//
+// propagation_pass (engine.cpp:138-189) evaluates, for every parent cone q of
+// level d-1 and every child box of q's box, the child interpolants at q's P
+// interpolation nodes.  The nodes relative to a child centre depend only on
+// the parent segment gamma and the child's octant in the parent box (child
+// centres sit at parent centre +-h_child/2 per axis), not on the box.  So per
+// (gamma, octant) "tile" the plan precomputes, once:
+//   * the child cone gamma_c, local coordinates (ts, tt, tp) and re-centring
+//     factor (rp/rc) e^{i kappa (rc - rp)} of every node (fast locate with the
+//     exact-fallback margin; entries within the margin are flagged and
+//     recomputed per box with the reference's exact formulas),
+//   * the nodes grouped by gamma_c into row tiles of 8.
+// At apply time a CTA takes up to kChunk parent cones that share one gamma
+// (cones sorted by gamma) and, octant by octant in Morton order, computes
+//   V[node][cone] = sum_k B_k(t_node) * C_{child cone}[k]
+// with mma.sync.m8n8k4.f64: A = Chebyshev basis products of 8 nodes (built in
+// shared memory), B = gathered child coefficients of 4 cones (re/im columns),
+// so a coefficient is loaded once per warp instead of once per node.  The
+// accumulated node values are fitted exactly as before.  Same result as the
+// per-node evaluation up to rounding (the basis is evaluated at identical t).
+#include <cub/cub.cuh>
+
+#include <algorithm>
+#include <vector>
+
+#include "plan.hpp"
+
+namespace ifgf_b200 {
+namespace {
+
+#ifndef IFGF_MMA_CHUNK
+#define IFGF_MMA_CHUNK 16
+#endif
+#ifndef IFGF_MMA_WARPS
+#define IFGF_MMA_WARPS 4
+#endif
+constexpr int kChunk = IFGF_MMA_CHUNK;    // parent cones per CTA (column tiles of 4)
+constexpr int kMmaWarps = IFGF_MMA_WARPS;  // warps per CTA
+constexpr uint32_t kNone = 0xffffffffu;
+constexpr uint32_t kFlag = 0x80000000u;
+
+struct TilesDev {
+  uint32_t ngamma;
+  const uint32_t* cone_gidx;
+  const uint32_t* gamma_of;
+  const double* e_t;
+  const double2* e_T;
+  const uint32_t* e_gc;
+  const uint32_t* rt_off;
+  const uint4* rt;
+  const uint32_t* fl_off;
+  const uint16_t* fl_node;
+  const uint32_t* qsorted;
+  const uint32_t* chunk_start;
+};
+
+TilesDev tiles_dev(const PropTiles& t) {
+  return {t.ngamma, t.cone_gidx, t.gamma_of, t.e_t, t.e_T, t.e_gc, t.rt_off,
+          t.rt,     t.fl_off,    t.fl_node,  t.qsorted, t.chunk_start};
+}
+
+inline unsigned nblk(size_t n, int t = 256) { return (unsigned)((n + t - 1) / t); }
+
+__device__ __forceinline__ int rt_node(const uint4& R, int r) {
+  const uint32_t w = r < 4 ? R.y : R.z;
+  return (int)((w >> (8 * (r & 3))) & 0xffu);
+}
+
+// ---------------------------------------------------------------- building
+__global__ void k_gamma_mark(const __grid_constant__ LevelDev U, uint64_t* gbits) {
+  const uint32_t q = blockIdx.x * blockDim.x + threadIdx.x;
+  if (q >= U.nc) return;
+  const uint32_t g = U.cone_gamma[q];
+  atomicOr((unsigned long long*)&gbits[g >> 6], 1ull << (g & 63));
+}
+
+__global__ void k_gamma_popc(const uint64_t* gbits, size_t nw, uint32_t* cnt) {
+  const size_t w = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
+  if (w < nw) cnt[w] = __popcll(gbits[w]);
+  else if (w == nw) cnt[w] = 0;
+}
+
+__global__ void k_gamma_index(const __grid_constant__ LevelDev U, const uint64_t* gbits,
+                              const uint32_t* grank, uint32_t* cone_gidx, uint32_t* gamma_of) {
+  const uint32_t q = blockIdx.x * blockDim.x + threadIdx.x;
+  if (q >= U.nc) return;
+  const uint32_t g = U.cone_gamma[q];
+  const uint64_t w = gbits[g >> 6];
+  const uint32_t idx = grank[g >> 6] + __popcll(w & ((1ull << (g & 63)) - 1));
+  cone_gidx[q] = idx;
+  gamma_of[idx] = g;  // same value from every cone of this gamma
+}
+
+// One thread per (gamma index, octant, node).
+__global__ void k_tile_entries(const __grid_constant__ LevelDev U, const __grid_constant__ LevelDev L,
+                               const __grid_constant__ InterpConsts K, const uint32_t* gamma_of,
+                               uint32_t ngamma, double kappa, double* e_t, double2* e_T,
+                               uint32_t* e_gc) {
+  const size_t t = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
+  if (t >= (size_t)ngamma * 8 * K.P) return;
+  const int m = (int)(t % K.P);
+  const uint32_t tile = (uint32_t)(t / K.P);
+  const int oct = (int)(tile & 7);
+  const uint32_t gi = tile >> 3;
+  const int jp = m % K.pp, jt = (m / K.pp) % K.pt, js = m / (K.pp * K.pt);
+  const SegMid sg = segment_mid(U, gamma_of[gi]);
+  // node relative to the parent centre (reference order without the centre)
+  double x, y, z;
+  node_position(sg, U.rad, 0.0, 0.0, 0.0, K.ns[js], K.nt[jt], K.np[jp], x, y, z);
+  const double hc = L.h;
+  const double ox = ((oct & 1) ? 0.5 : -0.5) * hc, oy = ((oct & 2) ? 0.5 : -0.5) * hc,
+               oz = ((oct & 4) ? 0.5 : -0.5) * hc;
+  const double rp = sqrt(fma(z, z, fma(y, y, x * x)));
+  // fast locate relative to the child centre; flag anything near a boundary
+  const double dx = x - ox, dy = y - oy, dz = z - oz;
+  const double rho2 = fma(dy, dy, dx * dx), r2 = fma(dz, dz, rho2);
+  const double rinv = rsqrt(r2), s = L.rad * rinv, rho_inv = rsqrt(rho2);
+  double theta, phi;
+  fast_angles(L.trig, dx, dy, dz, rho2 * rho_inv, rinv, rho_inv, theta, phi);
+  const double fs = s * L.iw0, ft = theta * L.iw1, fp = phi * L.iw2;
+  const bool flag = !(rho2 > 0.0) || s > kSMaxTol * (1.0 - 1e-12) || near_boundary(fs) ||
+                    near_boundary(ft) || near_boundary(fp);
+  int is = (int)fs, it = (int)ft, ip = (int)fp;
+  is = is < L.n0 - 1 ? is : L.n0 - 1;
+  it = it < L.n1 - 1 ? it : L.n1 - 1;
+  ip = ip < L.n2 - 1 ? ip : L.n2 - 1;
+  const uint32_t gc = ((uint32_t)is * (uint32_t)L.n1 + (uint32_t)it) * (uint32_t)L.n2 + (uint32_t)ip;
+  e_gc[t] = flag ? (kFlag | gc) : gc;
+  e_t[3 * t] = 2.0 * (fs - is) - 1.0;
+  e_t[3 * t + 1] = 2.0 * (ft - it) - 1.0;
+  e_t[3 * t + 2] = 2.0 * (fp - ip) - 1.0;
+  const double rc = r2 * rinv, ratio = rp * rinv;
+  double sn = 0.0, cn = 1.0;
+  if (kappa != 0.0) sincos_fast(kappa * (rc - rp), sn, cn);
+  e_T[t] = make_double2(ratio * cn, ratio * sn);
+}
+
+// One thread per tile: group its non-flagged nodes by child gamma (stable in
+// node order) into row tiles of 8; list flagged nodes.  Pass 1 counts.
+__global__ void k_tile_rows(uint32_t ntiles, int P, const uint32_t* e_gc, uint32_t* rt_cnt,
+                            uint32_t* fl_cnt, const uint32_t* rt_off, uint4* rt,
+                            const uint32_t* fl_off, uint16_t* fl_node) {
+  const uint32_t tile = blockIdx.x * blockDim.x + threadIdx.x;
+  if (tile >= ntiles) return;
+  const uint32_t* g = e_gc + (size_t)tile * P;
+  uint32_t nrt = 0, nfl = 0;
+  uint32_t wr = rt ? rt_off[tile] : 0;
+  uint32_t wfl = fl_node ? fl_off[tile] : 0;
+  // nodes in ascending (gamma, node) order: repeated min-scan (P <= 255)
+  uint32_t last = 0;
+  bool first = true;
+  for (;;) {
+    uint32_t cur = kNone;
+    for (int m = 0; m < P; ++m) {
+      const uint32_t v = g[m];
+      if (v & kFlag) continue;
+      if ((first || v > last) && v < cur) cur = v;
+    }
+    if (cur == kNone) break;
+    first = false;
+    last = cur;
+    // group size in nodes -> row tiles; the group's first row tile carries the count
+    int gsz = 0;
+    for (int m = 0; m < P; ++m) gsz += g[m] == cur;
+    const uint32_t ngt = (uint32_t)(gsz + 7) / 8;
+    uint4 R = make_uint4(cur, 0xffffffffu, 0xffffffffu, ngt);
+    int k = 0;
+    for (int m = 0; m < P; ++m) {
+      if (g[m] != cur) continue;
+      const uint32_t sh = 8 * (k & 3);
+      if (k < 4) R.y = (R.y & ~(0xffu << sh)) | ((uint32_t)m << sh);
+      else R.z = (R.z & ~(0xffu << sh)) | ((uint32_t)m << sh);
+      if (++k == 8) {
+        if (rt) rt[wr++] = R;
+        ++nrt;
+        R = make_uint4(cur, 0xffffffffu, 0xffffffffu, 0);
+        k = 0;
+      }
+    }
+    if (k) {
+      if (rt) rt[wr++] = R;
+      ++nrt;
+    }
+  }
+  for (int m = 0; m < P; ++m)
+    if (g[m] & kFlag) {
+      if (fl_node) fl_node[wfl++] = (uint16_t)m;
+      ++nfl;
+    }
+  if (rt_cnt) {
+    rt_cnt[tile] = nrt;
+    fl_cnt[tile] = nfl;
+  }
+}
+
+__global__ void k_chunk_flags(const uint32_t* gsorted, uint32_t n, uint32_t* flag) {
+  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i > n) return;
+  if (i == n) {
+    flag[i] = 0;
+    return;
+  }
+  // chunk starts: every kChunk-th element of each run of equal gamma index
+  uint32_t lo = 0, hi = i;
+  const uint32_t g = gsorted[i];
+  while (lo < hi) {  // run start = lower_bound(g)
+    const uint32_t mid = (lo + hi) >> 1;
+    if (gsorted[mid] < g) lo = mid + 1;
+    else hi = mid;
+  }
+  flag[i] = ((i - lo) % kChunk == 0) ? 1u : 0u;
+}
+
+__global__ void k_chunk_starts(const uint32_t* flag, const uint32_t* pos, uint32_t n,
+                               uint32_t* chunk_start, uint32_t nchunks) {
+  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n && flag[i]) chunk_start[pos[i]] = i;
+  if (i == 0) chunk_start[nchunks] = n;
+}
+
+// Clause 2 of compute_relevant_cones (cones.cpp:108-119) from the tiles: a
+// (parent cone, child box) pair marks the distinct child gammas of its tile
+// (one per node group, ~2-3 instead of P), flagged nodes are recomputed per
+// box with cone_of_point.
+__global__ void k_mark_nodes_tiles(const __grid_constant__ LevelDev L,
+                                   const __grid_constant__ LevelDev U,
+                                   const __grid_constant__ InterpConsts K, TilesDev T,
+                                   uint64_t* bits, int* err) {
+  const uint32_t q = blockIdx.x * blockDim.x + threadIdx.x;
+  if (q >= U.nc) return;
+  const uint32_t pb = U.cone_box[q];
+  const uint32_t gi = T.cone_gidx[q];
+  for (uint32_t cb = U.child_begin[pb]; cb < U.child_begin[pb + 1]; ++cb) {
+    const uint32_t tile = gi * 8 + (uint32_t)(L.code[cb] & 7);
+    for (uint32_t r = T.rt_off[tile]; r < T.rt_off[tile + 1]; ++r) {
+      const uint4 R = T.rt[r];
+      if (R.w == 0) continue;  // not the first row tile of its group
+      const uint64_t idx = (uint64_t)cb * L.G + R.x;
+      const uint64_t msk = 1ull << (idx & 63);
+      uint64_t* w = bits + (idx >> 6);
+      if (!(*w & msk)) atomicOr((unsigned long long*)w, (unsigned long long)msk);
+    }
+    for (uint32_t f = T.fl_off[tile]; f < T.fl_off[tile + 1]; ++f) {
+      const int m = T.fl_node[f];
+      const int jp = m % K.pp, jt = (m / K.pp) % K.pt, js = m / (K.pp * K.pt);
+      const SegMid sg = segment_mid(U, U.cone_gamma[q]);
+      double x, y, z;
+      node_position(sg, U.rad, U.cx[pb], U.cy[pb], U.cz[pb], K.ns[js], K.nt[jt], K.np[jp], x,
+                    y, z);
+      uint32_t gc;
+      const int e = cone_of_point(L, L.cx[cb], L.cy[cb], L.cz[cb], x, y, z, gc);
+      if (e) {
+        raise_err(err, e);
+        return;
+      }
+      const uint64_t idx = (uint64_t)cb * L.G + gc;
+      atomicOr((unsigned long long*)(bits + (idx >> 6)), 1ull << (idx & 63));
+    }
+  }
+}
+
+// ---------------------------------------------------------------- apply
+__device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+               : "+d"(d0), "+d"(d1)
+               : "d"(a), "d"(b));
+}
+
+// GEMM K index = device block layout index (planes padded to PL, total
+// KD = PS*PL rounded up to 4); the A operand is zero on the pad columns.
+template <int PS, int PT, int PP>
+struct MmaShape {
+  static constexpr int P = PS * PT * PP, NR = PT * PP;
+  static constexpr int PL = BlockLayout<PS, PT, PP>::PL, Pst = BlockLayout<PS, PT, PP>::Pst;
+  static constexpr int KD = (Pst + 3) & ~3, NS = KD / 4, NB = PS + PT + PP;
+  static constexpr int AST = KD + 1;   // A row stride (odd: spreads banks)
+  static constexpr int RT_BATCH = 8;   // row tiles whose A rows are staged at once
+  static constexpr size_t acc_bytes = (size_t)kChunk * P * sizeof(double2);
+  static constexpr size_t bas_bytes = (size_t)RT_BATCH * 8 * (NB + AST) * sizeof(double);
+  static constexpr size_t region = bas_bytes > acc_bytes ? bas_bytes : acc_bytes;
+  static constexpr size_t smem = acc_bytes + region;
+};
+
+template <int PS, int PT, int PP, bool LAP>
+__global__ void __launch_bounds__(kMmaWarps * 32)
+    k_propagate_mma(const __grid_constant__ LevelDev U, const __grid_constant__ LevelDev L,
+                    const __grid_constant__ InterpConsts K, const TilesDev T, double kappa,
+                    const double2* __restrict__ child, double2* parent, int* err) {
+  using S = MmaShape<PS, PT, PP>;
+  constexpr int P = S::P, NR = S::NR, PL = S::PL, NS = S::NS, NB = S::NB, AST = S::AST;
+  constexpr int RTB = S::RT_BATCH;
+  extern __shared__ double2 smem[];
+  double2* acc = smem;                                        // kChunk * P node values
+  double* bas = reinterpret_cast<double*>(acc + kChunk * P);  // RTB*8 rows x NB basis
+  double* Ash = bas + RTB * 8 * NB;                           // RTB*8 rows x AST (A operand)
+  double2* scr = acc + kChunk * P;                            // fit scratch (aliases bas/A)
+  __shared__ uint32_t qs[kChunk];
+  __shared__ uint32_t cbox[kChunk][8];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t c0 = T.chunk_start[blockIdx.x], c1 = T.chunk_start[blockIdx.x + 1];
+  const int nq = (int)(c1 - c0);
+  const int nct = (nq + 3) / 4;
+  for (int c = threadIdx.x; c < kChunk; c += blockDim.x) {
+    const uint32_t q = c < nq ? T.qsorted[c0 + c] : kNone;
+    qs[c] = q;
+    for (int o = 0; o < 8; ++o) cbox[c][o] = kNone;
+    if (q != kNone) {
+      const uint32_t pb = U.cone_box[q];
+      for (uint32_t cb = U.child_begin[pb]; cb < U.child_begin[pb + 1]; ++cb)
+        cbox[c][L.code[cb] & 7] = cb;
+    }
+  }
+  for (int i = threadIdx.x; i < kChunk * P; i += blockDim.x) acc[i] = make_double2(0.0, 0.0);
+  __syncthreads();
+  const uint32_t gi = T.cone_gidx[qs[0]];
+  const int arow = lane >> 2, acol = lane & 3;
+  for (int o = 0; o < 8; ++o) {
+    bool any = false;
+    for (int c = 0; c < nq; ++c) any |= cbox[c][o] != kNone;
+    if (!any) continue;
+    const uint32_t tile = gi * 8 + o;
+    const uint32_t r0 = T.rt_off[tile], r1 = T.rt_off[tile + 1];
+    for (uint32_t rb = r0; rb < r1; rb += RTB) {
+      const uint32_t re = min(r1, rb + RTB);
+      // 1. bases of all staged rows
+      for (uint32_t i = threadIdx.x; i < (re - rb) * 8; i += blockDim.x) {
+        const uint4 R = T.rt[rb + i / 8];
+        const int m = rt_node(R, (int)(i % 8));
+        double* b = bas + (size_t)i * NB;
+        if (m != 0xff) {
+          const double* tv = T.e_t + ((size_t)tile * P + m) * 3;
+          cheb_basis<PS>(tv[0], b);
+          cheb_basis<PT>(tv[1], b + PS);
+          cheb_basis<PP>(tv[2], b + PS + PT);
+        } else {
+          for (int j = 0; j < NB; ++j) b[j] = 0.0;
+        }
+      }
+      __syncthreads();
+      // 2. A rows: thread per (row, ks plane), compile-time (kt, kp) offsets
+      for (uint32_t i = threadIdx.x; i < (re - rb) * 8 * PS; i += blockDim.x) {
+        const uint32_t row = i / PS;
+        const int ks = (int)(i % PS);
+        const double* b = bas + (size_t)row * NB;
+        double* Ar = Ash + (size_t)row * AST + ks * PL;
+        const double ts = b[ks];
+#pragma unroll
+        for (int kt = 0; kt < PT; ++kt) {
+          const double w = ts * b[PS + kt];
+#pragma unroll
+          for (int kp = 0; kp < PP; ++kp) Ar[kt * PP + kp] = w * b[PS + PT + kp];
+        }
+#pragma unroll
+        for (int k = NR; k < PL; ++k) Ar[k] = 0.0;
+        if (ks == PS - 1)
+          for (int k = PS * PL; k < S::KD; ++k) Ash[(size_t)row * AST + k] = 0.0;
+      }
+      __syncthreads();
+      // 3. work items (column tile, group): B fragments loaded once, reused over the
+      //    group's row tiles; a group may straddle the batch end (continues next batch)
+      for (uint32_t item = warp; item < (re - rb) * (uint32_t)nct; item += kMmaWarps) {
+        const uint32_t rt = rb + item / nct;
+        const int ct = (int)(item % nct);
+        const uint4 R0 = T.rt[rt];
+        // process only from a group's first row tile, or the batch's first row tile
+        if (R0.w == 0 && rt != rb) continue;
+        uint32_t gend = rt + 1;
+        while (gend < re && T.rt[gend].w == 0) ++gend;
+        const uint32_t gc = R0.x;
+        const int col = lane >> 2;
+        const int cc = ct * 4 + (col >> 1);
+        const double* bp = nullptr;
+        if (cc < nq) {
+          const uint32_t cb = cbox[cc][o];
+          if (cb != kNone) {
+            const uint32_t cq = find_cone(L, cb, gc);
+            if (cq == kNone) raise_err(err, kErrPropCover);
+            else bp = reinterpret_cast<const double*>(child + (size_t)cq * S::Pst) + (col & 1) +
+                      2 * acol;
+          }
+        }
+        double bf[NS];
+#pragma unroll
+        for (int st = 0; st < NS; ++st)
+          bf[st] = (bp && 4 * st + acol < S::Pst) ? __ldg(bp + 8 * st) : 0.0;
+        const int cq = ct * 4 + acol;
+        const bool cq_ok = cq < nq && cbox[cq][o] != kNone;
+        for (uint32_t r = rt; r < gend; ++r) {
+          const double* ar = Ash + ((size_t)(r - rb) * 8 + arow) * AST + acol;
+          double d0 = 0.0, d1 = 0.0;
+#pragma unroll
+          for (int st = 0; st < NS; ++st) dmma(d0, d1, ar[4 * st], bf[st]);
+          // D[row = lane>>2][col = 2*(lane&3) + {0,1}] = (re, im) of cone ct*4 + (lane&3)
+          const int m = rt_node(T.rt[r], arow);
+          if (m != 0xff && cq_ok) {
+            const double2 Tf = T.e_T[(size_t)tile * P + m];
+            double2 v = acc[cq * P + m];
+            if (LAP) {
+              v.x = fma(d0, Tf.x, v.x);
+              v.y = fma(d1, Tf.x, v.y);
+            } else {
+              v.x = fma(d0, Tf.x, fma(-d1, Tf.y, v.x));
+              v.y = fma(d0, Tf.y, fma(d1, Tf.x, v.y));
+            }
+            acc[cq * P + m] = v;
+          }
+        }
+      }
+      __syncthreads();
+    }
+    // flagged nodes: per-box exact locate + evaluation (rare)
+    const uint32_t f0 = T.fl_off[tile], f1 = T.fl_off[tile + 1];
+    for (uint32_t i = threadIdx.x; i < (f1 - f0) * (uint32_t)nq; i += blockDim.x) {
+      const int c = (int)(i % nq);
+      const int m = T.fl_node[f0 + i / nq];
+      const uint32_t cb = cbox[c][o];
+      if (cb == kNone) continue;
+      const uint32_t q = qs[c], pb = U.cone_box[q];
+      const int jp = m % PP, jt = (m / PP) % PT, js = m / (PP * PT);
+      const SegMid sg = segment_mid(U, U.cone_gamma[q]);
+      const double pcx = U.cx[pb], pcy = U.cy[pb], pcz = U.cz[pb];
+      double x, y, z;
+      node_position(sg, U.rad, pcx, pcy, pcz, K.ns[js], K.nt[jt], K.np[jp], x, y, z);
+      const double ux = x - pcx, uy = y - pcy, uz = z - pcz;
+      const double rp = sqrt(fma(uz, uz, fma(uy, uy, ux * ux)));
+      Loc lo;
+      const int e = locate_fast(L, L.cx[cb], L.cy[cb], L.cz[cb], x, y, z, lo);
+      if (e) {
+        raise_err(err, e);
+        continue;
+      }
+      const uint32_t cq = find_cone(L, cb, lo.gamma);
+      if (cq == kNone) {
+        raise_err(err, kErrPropCover);
+        continue;
+      }
+      double vr, vi;
+      eval_block<PS, PT, PP>(child + (size_t)cq * S::Pst, lo.ts, lo.tt, lo.tp, vr, vi);
+      const double ratio = rp * lo.rinv;
+      double sn = 0.0, cn = 1.0;
+      if (!LAP) sincos_fast(kappa * (lo.r - rp), sn, cn);
+      const double tr = ratio * cn, ti = ratio * sn;
+      double2 v = acc[c * P + m];
+      v.x = fma(vr, tr, fma(-vi, ti, v.x));
+      v.y = fma(vr, ti, fma(vi, tr, v.y));
+      acc[c * P + m] = v;
+    }
+    __syncthreads();
+  }
+  fit_cones_scatter<PS, PT, PP>(K, acc, scr, nq, parent, qs, err);
+}
+
+// K3 per node with the tile geometry: thread = (parent cone, node); for each
+// child the (child gamma, t, transfer) entry of its (gamma, octant) tile
+// replaces locate + node trigonometry + sincos; flagged entries take the
+// per-box exact path.  CTAs walk consecutive cones (box-major) for L1 reuse.
+template <int PS, int PT, int PP, bool LAP>
+__global__ void __launch_bounds__(320, 2)
+    k_propagate_tab(const __grid_constant__ LevelDev U, const __grid_constant__ LevelDev L,
+                    const __grid_constant__ InterpConsts K, const TilesDev T, double kappa,
+                    uint32_t qb, uint32_t qe, int cpb, int groups,
+                    const double2* __restrict__ child, double2* parent, int* err) {
+  using BL = BlockLayout<PS, PT, PP>;
+  constexpr int P = PS * PT * PP;
+  extern __shared__ double2 smem[];
+  double2* sv = smem;
+  double2* st = smem + cpb * P;
+  const int c = threadIdx.x / P, m = threadIdx.x % P;
+  for (int g = 0; g < groups; ++g) {
+    const uint32_t q0 = qb + ((uint32_t)blockIdx.x * groups + g) * cpb;
+    if (q0 >= qe) break;
+    const int ncon = (int)min((uint32_t)cpb, qe - q0);
+    if (c < ncon) {
+      const uint32_t q = q0 + c;
+      const uint32_t pb = U.cone_box[q];
+      const size_t tbase = (size_t)T.cone_gidx[q] * 8;
+      double acr = 0.0, aci = 0.0;
+      const uint32_t c0 = U.child_begin[pb], c1 = U.child_begin[pb + 1];
+      for (uint32_t cb = c0; cb < c1; ++cb) {
+        const size_t e = (tbase + (L.code[cb] & 7)) * P + m;
+        const uint32_t gc = T.e_gc[e];
+        double ts, tt, tp, tr, ti;
+        uint32_t cq;
+        if (!(gc & kFlag)) {
+          cq = find_cone(L, cb, gc);
+          ts = T.e_t[3 * e];
+          tt = T.e_t[3 * e + 1];
+          tp = T.e_t[3 * e + 2];
+          const double2 Tf = T.e_T[e];
+          tr = Tf.x;
+          ti = Tf.y;
+        } else {
+          const int jp = m % PP, jt = (m / PP) % PT, js = m / (PP * PT);
+          const SegMid sg = segment_mid(U, U.cone_gamma[q]);
+          const double pcx = U.cx[pb], pcy = U.cy[pb], pcz = U.cz[pb];
+          double x, y, z;
+          node_position(sg, U.rad, pcx, pcy, pcz, K.ns[js], K.nt[jt], K.np[jp], x, y, z);
+          const double ux = x - pcx, uy = y - pcy, uz = z - pcz;
+          const double rp = sqrt(fma(uz, uz, fma(uy, uy, ux * ux)));
+          Loc lo;
+          const int er = locate_fast(L, L.cx[cb], L.cy[cb], L.cz[cb], x, y, z, lo);
+          if (er) {
+            raise_err(err, er);
+            break;
+          }
+          cq = find_cone(L, cb, lo.gamma);
+          ts = lo.ts;
+          tt = lo.tt;
+          tp = lo.tp;
+          const double ratio = rp * lo.rinv;
+          double sn = 0.0, cn = 1.0;
+          if (!LAP) sincos_fast(kappa * (lo.r - rp), sn, cn);
+          tr = ratio * cn;
+          ti = ratio * sn;
+        }
+        if (cq == kNone) {
+          raise_err(err, kErrPropCover);
+          break;
+        }
+        double vr, vi;
+        eval_block<PS, PT, PP>(child + (size_t)cq * BL::Pst, ts, tt, tp, vr, vi);
+        acr = fma(vr, tr, fma(-vi, ti, acr));
+        aci = fma(vr, ti, fma(vi, tr, aci));
+      }
+      sv[c * P + m] = make_double2(acr, aci);
+    }
+    __syncthreads();
+    fit_cones<PS, PT, PP>(K, sv, st, ncon, parent + (size_t)q0 * BL::Pst, err);
+    __syncthreads();
+  }
+}
+
+template <class F>
+bool dispatch_mma_orders(int ps, int pt, int pp, F&& f) {
+#define IFGF_MMA_CASE(a, b, c)          \
+  if (ps == a && pt == b && pp == c) {  \
+    f(std::integral_constant<int, a>{}, std::integral_constant<int, b>{}, \
+      std::integral_constant<int, c>{}); \
+    return true;                        \
+  }
+  IFGF_MMA_CASE(3, 5, 5)
+  IFGF_MMA_CASE(4, 6, 6)
+  IFGF_MMA_CASE(5, 7, 7)
+  IFGF_MMA_CASE(3, 3, 3)
+  IFGF_MMA_CASE(4, 4, 4)
+#undef IFGF_MMA_CASE
+  return false;
+}
+
+
+}  // namespace
+
+void build_prop_tiles(ifgf_plan* P, int d, void* (*scratch)(void*, size_t), void* sctx) {
+  PropTiles& T = P->tiles[d];
+  T = PropTiles{};
+  const Level& U = P->lv[d - 1];
+  const Level& L = P->lv[d];
+  const InterpConsts& K = P->K;
+  cudaStream_t s = P->s_main;
+  if (U.nc == 0 || K.P > 255) return;
+  if (!dispatch_mma_orders(K.ps, K.pt, K.pp, [](auto, auto, auto) {})) return;
+  if (U.G > (1ull << 28)) return;  // gamma bitmap too large: per-node kernel
+  // distinct parent gammas
+  const size_t nw = (U.G + 63) / 64;
+  uint64_t* gbits = P->alloc<uint64_t>(nw);
+  uint32_t* gcnt = P->alloc<uint32_t>(nw + 1);
+  uint32_t* grank = P->alloc<uint32_t>(nw + 1);
+  IFGF_CUDA(cudaMemsetAsync(gbits, 0, nw * 8, s));
+  k_gamma_mark<<<nblk(U.nc), 256, 0, s>>>(U.dev(), gbits);
+  k_gamma_popc<<<nblk(nw + 1), 256, 0, s>>>(gbits, nw, gcnt);
+  {
+    size_t tb = 0;
+    cub::DeviceScan::ExclusiveSum(nullptr, tb, gcnt, grank, (int)(nw + 1), s);
+    IFGF_CUDA(cub::DeviceScan::ExclusiveSum(scratch(sctx, tb), tb, gcnt, grank, (int)(nw + 1), s));
+  }
+  uint32_t ng = 0;
+  IFGF_CUDA(cudaMemcpyAsync(&ng, grank + nw, 4, cudaMemcpyDeviceToHost, s));
+  IFGF_CUDA(cudaStreamSynchronize(s));
+  // worth it only if a (gamma, octant) tile serves several parent cones
+  const double uses = (double)U.nc / ng;
+  P->launches += 2;
+  if (uses < 3.0) return;
+  T.ngamma = ng;
+  T.cone_gidx = P->alloc<uint32_t>(U.nc);
+  T.gamma_of = P->alloc<uint32_t>(ng);
+  k_gamma_index<<<nblk(U.nc), 256, 0, s>>>(U.dev(), gbits, grank, T.cone_gidx, T.gamma_of);
+  const uint32_t ntiles = ng * 8;
+  const size_t ne = (size_t)ntiles * K.P;
+  T.e_t = P->alloc<double>(3 * ne);
+  T.e_T = P->alloc<double2>(ne);
+  T.e_gc = P->alloc<uint32_t>(ne);
+  k_tile_entries<<<nblk(ne, 128), 128, 0, s>>>(U.dev(), L.dev(), K, T.gamma_of, ng, P->kappa, T.e_t,
+                                          T.e_T, T.e_gc);
+  uint32_t* rt_cnt = P->alloc<uint32_t>(ntiles + 1);
+  uint32_t* fl_cnt = P->alloc<uint32_t>(ntiles + 1);
+  IFGF_CUDA(cudaMemsetAsync(rt_cnt + ntiles, 0, 4, s));
+  IFGF_CUDA(cudaMemsetAsync(fl_cnt + ntiles, 0, 4, s));
+  k_tile_rows<<<nblk(ntiles, 64), 64, 0, s>>>(ntiles, K.P, T.e_gc, rt_cnt, fl_cnt, nullptr,
+                                              nullptr, nullptr, nullptr);
+  T.rt_off = P->alloc<uint32_t>(ntiles + 1);
+  T.fl_off = P->alloc<uint32_t>(ntiles + 1);
+  {
+    size_t tb = 0;
+    cub::DeviceScan::ExclusiveSum(nullptr, tb, rt_cnt, T.rt_off, (int)(ntiles + 1), s);
+    IFGF_CUDA(cub::DeviceScan::ExclusiveSum(scratch(sctx, tb), tb, rt_cnt, T.rt_off,
+                                            (int)(ntiles + 1), s));
+    IFGF_CUDA(cub::DeviceScan::ExclusiveSum(scratch(sctx, tb), tb, fl_cnt, T.fl_off,
+                                            (int)(ntiles + 1), s));
+  }
+  uint32_t tot[2];
+  IFGF_CUDA(cudaMemcpyAsync(&tot[0], T.rt_off + ntiles, 4, cudaMemcpyDeviceToHost, s));
+  IFGF_CUDA(cudaMemcpyAsync(&tot[1], T.fl_off + ntiles, 4, cudaMemcpyDeviceToHost, s));
+  IFGF_CUDA(cudaStreamSynchronize(s));
+  T.rt = P->alloc<uint4>(tot[0] + 1);
+  T.fl_node = P->alloc<uint16_t>(tot[1] + 1);
+  k_tile_rows<<<nblk(ntiles, 64), 64, 0, s>>>(ntiles, K.P, T.e_gc, nullptr, nullptr, T.rt_off,
+                                              T.rt, T.fl_off, T.fl_node);
+  // parent cones sorted by gamma index (stable) -> chunks of <= kChunk
+  uint32_t* qidx = P->alloc<uint32_t>(U.nc);
+  uint32_t* gsorted = P->alloc<uint32_t>(U.nc);
+  T.qsorted = P->alloc<uint32_t>(U.nc);
+  {
+    std::vector<uint32_t> iota(U.nc);
+    for (uint32_t i = 0; i < U.nc; ++i) iota[i] = i;
+    IFGF_CUDA(cudaMemcpyAsync(qidx, iota.data(), U.nc * 4, cudaMemcpyHostToDevice, s));
+    size_t tb = 0;
+    int bits = 1;
+    while ((1u << bits) < ng && bits < 32) ++bits;
+    cub::DeviceRadixSort::SortPairs(nullptr, tb, T.cone_gidx, gsorted, qidx, T.qsorted,
+                                    (int)U.nc, 0, bits, s);
+    IFGF_CUDA(cub::DeviceRadixSort::SortPairs(scratch(sctx, tb), tb, T.cone_gidx, gsorted, qidx,
+                                              T.qsorted, (int)U.nc, 0, bits, s));
+    IFGF_CUDA(cudaStreamSynchronize(s));
+  }
+  uint32_t* flag = P->alloc<uint32_t>(U.nc + 1);
+  uint32_t* pos = P->alloc<uint32_t>(U.nc + 1);
+  k_chunk_flags<<<nblk(U.nc + 1), 256, 0, s>>>(gsorted, U.nc, flag);
+  {
+    size_t tb = 0;
+    cub::DeviceScan::ExclusiveSum(nullptr, tb, flag, pos, (int)(U.nc + 1), s);
+    IFGF_CUDA(cub::DeviceScan::ExclusiveSum(scratch(sctx, tb), tb, flag, pos, (int)(U.nc + 1), s));
+  }
+  uint32_t nch = 0;
+  IFGF_CUDA(cudaMemcpyAsync(&nch, pos + U.nc, 4, cudaMemcpyDeviceToHost, s));
+  IFGF_CUDA(cudaStreamSynchronize(s));
+  T.nchunks = nch;
+  T.chunk_start = P->alloc<uint32_t>(nch + 1);
+  k_chunk_starts<<<nblk(U.nc + 1), 256, 0, s>>>(flag, pos, U.nc, T.chunk_start, nch);
+  IFGF_CUDA(cudaGetLastError());
+  P->launches += 7;
+  T.enabled = true;
+}
+
+void launch_mark_nodes_tiles(ifgf_plan* P, int d, uint64_t* bits) {
+  const PropTiles& T = P->tiles[d];
+  const Level& U = P->lv[d - 1];
+  k_mark_nodes_tiles<<<nblk(U.nc, 128), 128, 0, P->s_main>>>(P->lv[d].dev(), U.dev(), P->K,
+                                                             tiles_dev(T), bits, P->err);
+  ++P->launches;
+}
+
+bool launch_propagation_mma(ifgf_plan* P, int d, const double2* child, double2* parent,
+                            cudaStream_t s) {
+  const PropTiles& T = P->tiles[d];
+  if (!T.enabled || T.nchunks == 0) return false;
+  if (P->prop_mode == 0) {  // per node from the tiles (default)
+    const Level& U = P->lv[d - 1];
+    const Level& L = P->lv[d];
+    const InterpConsts& K = P->K;
+    return dispatch_mma_orders(K.ps, K.pt, K.pp, [&](auto A, auto B, auto C) {
+      constexpr int PS = decltype(A)::value, PT = decltype(B)::value, PP = decltype(C)::value;
+      constexpr int Pn = PS * PT * PP;
+      int cpb = std::max(1, 320 / Pn);
+      const uint32_t nq = U.nc;
+      const int groups =
+          (int)std::min<size_t>(8, std::max<size_t>(1, nq / ((size_t)cpb * 148 * 8)));
+      const unsigned grid = (unsigned)((nq + (size_t)cpb * groups - 1) / ((size_t)cpb * groups));
+      const unsigned thr = (unsigned)(((cpb * Pn + 31) / 32) * 32);
+      const size_t sm = 2 * (size_t)cpb * Pn * sizeof(double2);
+      if (P->kappa == 0.0)
+        k_propagate_tab<PS, PT, PP, true><<<grid, thr, sm, s>>>(
+            U.dev(), L.dev(), K, tiles_dev(T), P->kappa, 0, nq, cpb, groups, child, parent,
+            P->err);
+      else
+        k_propagate_tab<PS, PT, PP, false><<<grid, thr, sm, s>>>(
+            U.dev(), L.dev(), K, tiles_dev(T), P->kappa, 0, nq, cpb, groups, child, parent,
+            P->err);
+      ++P->launches;
+    });
+  }
+  const Level& U = P->lv[d - 1];
+  const Level& L = P->lv[d];
+  const InterpConsts& K = P->K;
+  return dispatch_mma_orders(K.ps, K.pt, K.pp, [&](auto A, auto B, auto C) {
+    constexpr int PS = decltype(A)::value, PT = decltype(B)::value, PP = decltype(C)::value;
+    const size_t sm = MmaShape<PS, PT, PP>::smem;
+    static bool attr_set = false;
+    if (!attr_set) {
+      cudaFuncSetAttribute(k_propagate_mma<PS, PT, PP, true>,
+                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+      cudaFuncSetAttribute(k_propagate_mma<PS, PT, PP, false>,
+                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+      attr_set = true;
+    }
+    if (P->kappa == 0.0)
+      k_propagate_mma<PS, PT, PP, true><<<T.nchunks, kMmaWarps * 32, sm, s>>>(
+          U.dev(), L.dev(), K, tiles_dev(T), P->kappa, child, parent, P->err);
+    else
+      k_propagate_mma<PS, PT, PP, false><<<T.nchunks, kMmaWarps * 32, sm, s>>>(
+          U.dev(), L.dev(), K, tiles_dev(T), P->kappa, child, parent, P->err);
+    ++P->launches;
+  });
+}
+
+}  // namespace ifgf_b200

@@ -565,10 +565,16 @@ void build_plan(ifgf_plan* P, const double* d_x, const double* d_y, const double
                                              P->err);
     ++P->launches;
     if (d > 3 && P->lv[d - 1].nc > 0) {
-      const size_t work = (size_t)P->lv[d - 1].nc * P->K.P;
-      k_mark_nodes<<<grid_for(work), kT, 0, s>>>(L.dev(), P->lv[d - 1].dev(), P->K, L.bits,
-                                                 P->err);
-      ++P->launches;
+      build_prop_tiles(
+          P, d, [](void* ctx, size_t b) { return static_cast<Scratch*>(ctx)->get(b); }, &scratch);
+      if (P->tiles[d].enabled) {
+        launch_mark_nodes_tiles(P, d, L.bits);
+      } else {
+        const size_t work = (size_t)P->lv[d - 1].nc * P->K.P;
+        k_mark_nodes<<<grid_for(work), kT, 0, s>>>(L.dev(), P->lv[d - 1].dev(), P->K, L.bits,
+                                                   P->err);
+        ++P->launches;
+      }
     }
     uint32_t* cnt = P->alloc<uint32_t>(L.nwords + 1);
     k_popc<<<grid_for(L.nwords + 1), kT, 0, s>>>(L.bits, L.nwords, cnt);

@@ -286,6 +286,11 @@ class Plan:
         """Run all apply kernels on one stream (exclusive per-pass timings)."""
         check(lib.ifgf_plan_set_option(self._h, 1, 1 if on else 0))
 
+    def set_option(self, option: int, value: int):
+        """IFGF_OPT_* (include/ifgf_b200.h): 1 serial, 2 per-node locate in K3,
+        3 tensor-core GEMM propagation."""
+        check(lib.ifgf_plan_set_option(self._h, option, value))
+
     def _info(self) -> _lib.CPlanInfo:
         info = _lib.CPlanInfo()
         check(lib.ifgf_plan_get_info(self._h, C.byref(info)))
