@@ -791,7 +791,7 @@ int ifgf_plan_pack_blocks(ifgf_plan* P, int d, const uint32_t* d_cones, size_t m
                           void* stream) {
   return guarded([&] {
     if (!P) throw Error(IFGF_EINVAL, "null plan");
-    double2* blk = P->n_slots ? P->slots[d] : stage_blocks(P, d);
+    double2* blk = stage_blocks(P, d);  // the pass-level API's level storage
     launch_pack(P, blk, d_cones, m, d_buf, 0, nullptr, static_cast<cudaStream_t>(stream));
     IFGF_CUDA(cudaGetLastError());
   });
@@ -801,7 +801,7 @@ int ifgf_plan_unpack_blocks(ifgf_plan* P, int d, const uint32_t* d_cones, size_t
                             const double* d_buf, void* stream) {
   return guarded([&] {
     if (!P) throw Error(IFGF_EINVAL, "null plan");
-    double2* blk = P->n_slots ? P->slots[d] : stage_blocks(P, d);
+    double2* blk = stage_blocks(P, d);
     launch_pack(P, nullptr, d_cones, m, const_cast<double*>(d_buf), 1, blk,
                 static_cast<cudaStream_t>(stream));
     IFGF_CUDA(cudaGetLastError());

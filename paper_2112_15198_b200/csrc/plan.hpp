@@ -188,8 +188,8 @@ bool orders_supported(int ps, int pt, int pp);
 // propagate_mma.cu
 void build_prop_tiles(ifgf_plan* P, int d, void* (*scratch)(void*, size_t), void* sctx);
 void launch_mark_nodes_tiles(ifgf_plan* P, int d, uint64_t* bits);
-bool launch_propagation_mma(ifgf_plan* P, int d, const double2* child, double2* parent,
-                            cudaStream_t s);
+bool launch_propagation_mma(ifgf_plan* P, int d, uint32_t qb, uint32_t qe, const double2* child,
+                            double2* parent, cudaStream_t s);
 // direct.cu
 void direct_sums(const double* x, const double* y, const double* z, const double* ar,
                  const double* ai, size_t n, double kappa, const uint32_t* targets, size_t m,

@@ -268,19 +268,29 @@ __device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b)
 }
 
 // GEMM K index = device block layout index (planes padded to PL, total
-// KD = PS*PL rounded up to 4); the A operand is zero on the pad columns.
+// KD = PS*PL rounded up to 4); A is zero on the pad columns, B on pad rows.
 template <int PS, int PT, int PP>
 struct MmaShape {
   static constexpr int P = PS * PT * PP, NR = PT * PP;
   static constexpr int PL = BlockLayout<PS, PT, PP>::PL, Pst = BlockLayout<PS, PT, PP>::Pst;
   static constexpr int KD = (Pst + 3) & ~3, NS = KD / 4, NB = PS + PT + PP;
-  static constexpr int AST = KD + 1;   // A row stride (odd: spreads banks)
-  static constexpr int RT_BATCH = 8;   // row tiles whose A rows are staged at once
+  static constexpr int AST = KD + 1;   // A row stride in doubles (odd: spreads banks)
+  static constexpr int BST = KD + 1;   // B column stride in double2
+  static constexpr int RTB = 4;        // row tiles staged per batch
   static constexpr size_t acc_bytes = (size_t)kChunk * P * sizeof(double2);
-  static constexpr size_t bas_bytes = (size_t)RT_BATCH * 8 * (NB + AST) * sizeof(double);
-  static constexpr size_t region = bas_bytes > acc_bytes ? bas_bytes : acc_bytes;
-  static constexpr size_t smem = acc_bytes + region;
+  static constexpr size_t b_bytes = (size_t)kChunk * BST * sizeof(double2);
+  static constexpr size_t a_bytes = (size_t)RTB * 8 * (AST + NB) * sizeof(double);
+  static constexpr size_t work = b_bytes + a_bytes;
+  static constexpr size_t smem = acc_bytes + (work > acc_bytes ? work : acc_bytes);
 };
+
+__device__ __forceinline__ void cp_async16(void* smem_dst, const void* gmem_src) {
+  const unsigned dst = (unsigned)__cvta_generic_to_shared(smem_dst);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(gmem_src));
+}
+__device__ __forceinline__ void cp_async_wait_all() {
+  asm volatile("cp.async.wait_all;" ::: "memory");
+}
 
 template <int PS, int PT, int PP, bool LAP>
 __global__ void __launch_bounds__(kMmaWarps * 32)
@@ -289,18 +299,20 @@ __global__ void __launch_bounds__(kMmaWarps * 32)
                     const double2* __restrict__ child, double2* parent, int* err) {
   using S = MmaShape<PS, PT, PP>;
   constexpr int P = S::P, NR = S::NR, PL = S::PL, NS = S::NS, NB = S::NB, AST = S::AST;
-  constexpr int RTB = S::RT_BATCH;
+  constexpr int BST = S::BST, RTB = S::RTB;
   extern __shared__ double2 smem[];
-  double2* acc = smem;                                        // kChunk * P node values
-  double* bas = reinterpret_cast<double*>(acc + kChunk * P);  // RTB*8 rows x NB basis
-  double* Ash = bas + RTB * 8 * NB;                           // RTB*8 rows x AST (A operand)
-  double2* scr = acc + kChunk * P;                            // fit scratch (aliases bas/A)
+  double2* acc = smem;                                        // kChunk x P node values
+  double2* Bs = acc + kChunk * P;                             // kChunk x BST child blocks
+  double* Ash = reinterpret_cast<double*>(Bs + kChunk * BST); // RTB*8 x AST
+  double* bas = Ash + RTB * 8 * AST;                          // RTB*8 x NB
+  double2* scr = acc + kChunk * P;                            // fit scratch (aliases Bs..)
   __shared__ uint32_t qs[kChunk];
   __shared__ uint32_t cbox[kChunk][8];
+  __shared__ int vl[kChunk];  // packed cones having a child in this octant
+  __shared__ int nv_s;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t c0 = T.chunk_start[blockIdx.x], c1 = T.chunk_start[blockIdx.x + 1];
   const int nq = (int)(c1 - c0);
-  const int nct = (nq + 3) / 4;
   for (int c = threadIdx.x; c < kChunk; c += blockDim.x) {
     const uint32_t q = c < nq ? T.qsorted[c0 + c] : kNone;
     qs[c] = q;
@@ -316,98 +328,122 @@ __global__ void __launch_bounds__(kMmaWarps * 32)
   const uint32_t gi = T.cone_gidx[qs[0]];
   const int arow = lane >> 2, acol = lane & 3;
   for (int o = 0; o < 8; ++o) {
-    bool any = false;
-    for (int c = 0; c < nq; ++c) any |= cbox[c][o] != kNone;
-    if (!any) continue;
+    if (threadIdx.x == 0) {
+      int n = 0;
+      for (int c = 0; c < nq; ++c)
+        if (cbox[c][o] != kNone) vl[n++] = c;
+      nv_s = n;
+    }
+    __syncthreads();
+    const int nv = nv_s;
+    if (nv == 0) continue;
+    const int nct = (nv + 3) / 4;
     const uint32_t tile = gi * 8 + o;
     const uint32_t r0 = T.rt_off[tile], r1 = T.rt_off[tile + 1];
-    for (uint32_t rb = r0; rb < r1; rb += RTB) {
-      const uint32_t re = min(r1, rb + RTB);
-      // 1. bases of all staged rows
-      for (uint32_t i = threadIdx.x; i < (re - rb) * 8; i += blockDim.x) {
-        const uint4 R = T.rt[rb + i / 8];
-        const int m = rt_node(R, (int)(i % 8));
-        double* b = bas + (size_t)i * NB;
-        if (m != 0xff) {
-          const double* tv = T.e_t + ((size_t)tile * P + m) * 3;
-          cheb_basis<PS>(tv[0], b);
-          cheb_basis<PT>(tv[1], b + PS);
-          cheb_basis<PP>(tv[2], b + PS + PT);
+    for (uint32_t ga = r0; ga < r1;) {
+      // group [ga, gb): row tiles sharing one child gamma
+      const uint4 RG = T.rt[ga];
+      const uint32_t gb = ga + max(RG.w, 1u);
+      const uint32_t gc = RG.x;
+      // stage B: the group's child block of every packed cone (zero for pads)
+      for (int i = threadIdx.x; i < nct * 4 * (S::KD / 2); i += blockDim.x) {
+        const int j = i / (S::KD / 2), h = i % (S::KD / 2);  // 2 complex (32 B) per step
+        double2* dst = Bs + j * BST + 2 * h;
+        const double2* src = nullptr;
+        if (j < nv && 2 * h < S::Pst) {
+          const uint32_t cq = find_cone(L, cbox[vl[j]][o], gc);
+          if (cq == kNone) raise_err(err, kErrPropCover);
+          else src = child + (size_t)cq * S::Pst + 2 * h;
+        }
+        if (src) {
+          cp_async16(dst, src);
+          cp_async16(dst + 1, src + 1);
         } else {
-          for (int j = 0; j < NB; ++j) b[j] = 0.0;
+          dst[0] = make_double2(0.0, 0.0);
+          dst[1] = make_double2(0.0, 0.0);
         }
       }
-      __syncthreads();
-      // 2. A rows: thread per (row, ks plane), compile-time (kt, kp) offsets
-      for (uint32_t i = threadIdx.x; i < (re - rb) * 8 * PS; i += blockDim.x) {
-        const uint32_t row = i / PS;
-        const int ks = (int)(i % PS);
-        const double* b = bas + (size_t)row * NB;
-        double* Ar = Ash + (size_t)row * AST + ks * PL;
-        const double ts = b[ks];
-#pragma unroll
-        for (int kt = 0; kt < PT; ++kt) {
-          const double w = ts * b[PS + kt];
-#pragma unroll
-          for (int kp = 0; kp < PP; ++kp) Ar[kt * PP + kp] = w * b[PS + PT + kp];
-        }
-#pragma unroll
-        for (int k = NR; k < PL; ++k) Ar[k] = 0.0;
-        if (ks == PS - 1)
-          for (int k = PS * PL; k < S::KD; ++k) Ash[(size_t)row * AST + k] = 0.0;
-      }
-      __syncthreads();
-      // 3. work items (column tile, group): B fragments loaded once, reused over the
-      //    group's row tiles; a group may straddle the batch end (continues next batch)
-      for (uint32_t item = warp; item < (re - rb) * (uint32_t)nct; item += kMmaWarps) {
-        const uint32_t rt = rb + item / nct;
-        const int ct = (int)(item % nct);
-        const uint4 R0 = T.rt[rt];
-        // process only from a group's first row tile, or the batch's first row tile
-        if (R0.w == 0 && rt != rb) continue;
-        uint32_t gend = rt + 1;
-        while (gend < re && T.rt[gend].w == 0) ++gend;
-        const uint32_t gc = R0.x;
-        const int col = lane >> 2;
-        const int cc = ct * 4 + (col >> 1);
-        const double* bp = nullptr;
-        if (cc < nq) {
-          const uint32_t cb = cbox[cc][o];
-          if (cb != kNone) {
-            const uint32_t cq = find_cone(L, cb, gc);
-            if (cq == kNone) raise_err(err, kErrPropCover);
-            else bp = reinterpret_cast<const double*>(child + (size_t)cq * S::Pst) + (col & 1) +
-                      2 * acol;
+      for (uint32_t rb = ga; rb < gb; rb += RTB) {
+        const uint32_t re = min(gb, rb + RTB);
+        const int nrow = (int)(re - rb) * 8;
+        // bases of the staged rows
+        for (int i = threadIdx.x; i < nrow; i += blockDim.x) {
+          const int m = rt_node(T.rt[rb + i / 8], i % 8);
+          double* b = bas + i * NB;
+          if (m != 0xff) {
+            const double* tv = T.e_t + ((size_t)tile * P + m) * 3;
+            cheb_basis<PS>(tv[0], b);
+            cheb_basis<PT>(tv[1], b + PS);
+            cheb_basis<PP>(tv[2], b + PS + PT);
+          } else {
+            for (int j = 0; j < NB; ++j) b[j] = 0.0;
           }
         }
-        double bf[NS];
+        __syncthreads();
+        // A rows: thread per (row, ks plane), compile-time (kt, kp) offsets
+        for (int i = threadIdx.x; i < nrow * PS; i += blockDim.x) {
+          const int row = i / PS, ks = i % PS;
+          const double* b = bas + row * NB;
+          double* Ar = Ash + row * AST + ks * PL;
+          const double ts = b[ks];
 #pragma unroll
-        for (int st = 0; st < NS; ++st)
-          bf[st] = (bp && 4 * st + acol < S::Pst) ? __ldg(bp + 8 * st) : 0.0;
-        const int cq = ct * 4 + acol;
-        const bool cq_ok = cq < nq && cbox[cq][o] != kNone;
-        for (uint32_t r = rt; r < gend; ++r) {
-          const double* ar = Ash + ((size_t)(r - rb) * 8 + arow) * AST + acol;
-          double d0 = 0.0, d1 = 0.0;
+          for (int kt = 0; kt < PT; ++kt) {
+            const double w = ts * b[PS + kt];
 #pragma unroll
-          for (int st = 0; st < NS; ++st) dmma(d0, d1, ar[4 * st], bf[st]);
-          // D[row = lane>>2][col = 2*(lane&3) + {0,1}] = (re, im) of cone ct*4 + (lane&3)
-          const int m = rt_node(T.rt[r], arow);
-          if (m != 0xff && cq_ok) {
-            const double2 Tf = T.e_T[(size_t)tile * P + m];
-            double2 v = acc[cq * P + m];
-            if (LAP) {
-              v.x = fma(d0, Tf.x, v.x);
-              v.y = fma(d1, Tf.x, v.y);
-            } else {
-              v.x = fma(d0, Tf.x, fma(-d1, Tf.y, v.x));
-              v.y = fma(d0, Tf.y, fma(d1, Tf.x, v.y));
+            for (int kp = 0; kp < PP; ++kp) Ar[kt * PP + kp] = w * b[PS + PT + kp];
+          }
+#pragma unroll
+          for (int k = NR; k < PL; ++k) Ar[k] = 0.0;
+          if (ks == PS - 1)
+            for (int k = PS * PL; k < S::KD; ++k) Ash[row * AST + k] = 0.0;
+        }
+        cp_async_wait_all();
+        __syncthreads();
+        // MMA: warp per row tile; A fragments in registers, 4 column tiles at a time
+        for (int rt = warp; rt < (int)(re - rb); rt += kMmaWarps) {
+          double af[NS];
+          const double* ar = Ash + (rt * 8 + arow) * AST + acol;
+#pragma unroll
+          for (int st = 0; st < NS; ++st) af[st] = ar[4 * st];
+          const int m = rt_node(T.rt[rb + rt], arow);
+          for (int cg = 0; cg < nct; cg += 4) {
+            double d[4][2];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) d[u][0] = d[u][1] = 0.0;
+            // B fragment: column lane>>2 -> cone (ct*4 + col/2), part col&1; row k = 4st+acol
+            const int col = lane >> 2;
+            const double* bcol = reinterpret_cast<const double*>(Bs) + (col & 1) + 2 * acol;
+#pragma unroll
+            for (int st = 0; st < NS; ++st) {
+#pragma unroll
+              for (int u = 0; u < 4; ++u) {
+                const int j = (cg + u) * 4 + (col >> 1);
+                const double bv = (cg + u < nct) ? bcol[2 * (j * BST + 4 * st)] : 0.0;
+                dmma(d[u][0], d[u][1], af[st], bv);
+              }
             }
-            acc[cq * P + m] = v;
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+              const int j = (cg + u) * 4 + acol;  // packed cone of this lane's D column pair
+              if (cg + u < nct && j < nv && m != 0xff) {
+                const int c = vl[j];
+                const double2 Tf = T.e_T[(size_t)tile * P + m];
+                double2 v = acc[c * P + m];
+                if (LAP) {
+                  v.x = fma(d[u][0], Tf.x, v.x);
+                  v.y = fma(d[u][1], Tf.x, v.y);
+                } else {
+                  v.x = fma(d[u][0], Tf.x, fma(-d[u][1], Tf.y, v.x));
+                  v.y = fma(d[u][0], Tf.y, fma(d[u][1], Tf.x, v.y));
+                }
+                acc[c * P + m] = v;
+              }
+            }
           }
         }
+        __syncthreads();
       }
-      __syncthreads();
+      ga = gb;
     }
     // flagged nodes: per-box exact locate + evaluation (rare)
     const uint32_t f0 = T.fl_off[tile], f1 = T.fl_off[tile + 1];
@@ -660,11 +696,12 @@ void launch_mark_nodes_tiles(ifgf_plan* P, int d, uint64_t* bits) {
   ++P->launches;
 }
 
-bool launch_propagation_mma(ifgf_plan* P, int d, const double2* child, double2* parent,
-                            cudaStream_t s) {
+bool launch_propagation_mma(ifgf_plan* P, int d, uint32_t qb, uint32_t qe, const double2* child,
+                            double2* parent, cudaStream_t s) {
   const PropTiles& T = P->tiles[d];
   if (!T.enabled || T.nchunks == 0) return false;
-  if (P->prop_mode == 0) {  // per node from the tiles (default)
+  const bool full = qb == 0 && qe == P->lv[d - 1].nc;
+  if (P->prop_mode == 0 || !full) {  // per node from the tiles (default; any cone range)
     const Level& U = P->lv[d - 1];
     const Level& L = P->lv[d];
     const InterpConsts& K = P->K;
@@ -672,7 +709,7 @@ bool launch_propagation_mma(ifgf_plan* P, int d, const double2* child, double2* 
       constexpr int PS = decltype(A)::value, PT = decltype(B)::value, PP = decltype(C)::value;
       constexpr int Pn = PS * PT * PP;
       int cpb = std::max(1, 320 / Pn);
-      const uint32_t nq = U.nc;
+      const uint32_t nq = qe - qb;
       const int groups =
           (int)std::min<size_t>(8, std::max<size_t>(1, nq / ((size_t)cpb * 148 * 8)));
       const unsigned grid = (unsigned)((nq + (size_t)cpb * groups - 1) / ((size_t)cpb * groups));
@@ -680,11 +717,11 @@ bool launch_propagation_mma(ifgf_plan* P, int d, const double2* child, double2* 
       const size_t sm = 2 * (size_t)cpb * Pn * sizeof(double2);
       if (P->kappa == 0.0)
         k_propagate_tab<PS, PT, PP, true><<<grid, thr, sm, s>>>(
-            U.dev(), L.dev(), K, tiles_dev(T), P->kappa, 0, nq, cpb, groups, child, parent,
+            U.dev(), L.dev(), K, tiles_dev(T), P->kappa, qb, qe, cpb, groups, child, parent,
             P->err);
       else
         k_propagate_tab<PS, PT, PP, false><<<grid, thr, sm, s>>>(
-            U.dev(), L.dev(), K, tiles_dev(T), P->kappa, 0, nq, cpb, groups, child, parent,
+            U.dev(), L.dev(), K, tiles_dev(T), P->kappa, qb, qe, cpb, groups, child, parent,
             P->err);
       ++P->launches;
     });
