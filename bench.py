@@ -286,13 +286,19 @@ def run_ours(args):
     dom = max(per_kernel, key=lambda k: per_kernel[k]["ms"])
     traffic = None
     summ = os.path.join(ROOT, "profiles", "ncu_summary.json")
+    kernel_prefix = {"near": "k_singular", "level_d": "k_level_d",
+                     "interpolation": "k_interp", "propagation": "k_propagate"}[dom]
     if os.path.exists(summ):
         try:
-            traffic = json.load(open(summ)).get("traffic_bytes_per_launch", {}).get(dom)
+            tb = json.load(open(summ)).get("traffic_bytes_per_launch", {})
+            hits = [v for k, v in tb.items() if k.startswith(kernel_prefix + "<")]
+            traffic = statistics.mean(hits) if hits else None
         except Exception:
             traffic = None
     dk = per_kernel[dom]
     roofline = {"bound": "fp64", "kernel": dom, "achieved": dk["tflops"], "peak": fp64_peak,
+                "traffic_note": "DRAM bytes per launch of the dominant kernel from the committed "
+                                "ncu --set full capture (profiles/ncu_summary.json, C2)",
                 "unit": "TFLOP/s", "frac": dk["frac_fp64"], "traffic": traffic,
                 "peak_source": "measured in this run: best of DFMA chains and mma.sync m8n8k4 f64 "
                                "over all SMs (ifgf_measure_fp64_peak); MEASURED_PEAKS.json has no FP64 figure",
@@ -338,10 +344,73 @@ def run_ours(args):
         torch.distributed.destroy_process_group()
 
 
+def run_ours_dist(args):
+    """N > 1: the C2 matvec split across ranks (strong scaling) with the
+    reference's rank algorithm (dist.cpp:241-361) -- per-level block exchange
+    over NCCL (paper_2112_15198_b200/dist.py).  One step = every rank builds
+    the plan + the distributed apply; inputs and the gathered result are host
+    arrays, so this is also the end-to-end number."""
+    import torch
+    import torch.distributed as dist
+
+    import paper_2112_15198_b200 as ifgf
+    from paper_2112_15198_b200.dist import DistributedPlan
+
+    rank, local, world = dist_env()
+    torch.cuda.set_device(local)
+    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    cfgd = ifgf.configs.CONFIGS[args.config]
+    kcfg = ifgf.KernelConfig(ifgf.KernelKind(cfgd.kind), cfgd.kappa)
+    n = cfgd.n
+    pc = ifgf.generate(n, cfgd.shape, cfgd.c, cfgd.dens, cfgd.seed)
+
+    def step():
+        dp = DistributedPlan(pc.x1, pc.x2, pc.x3, kcfg, ifgf.EngineParams(depth=cfgd.depth))
+        out = dp.apply(pc.a_re, pc.a_im)
+        vol = dp.ex.volume_blocks()
+        dp.plan.close()
+        return out, vol
+
+    for _ in range(args.warmup):
+        step()
+    times = []
+    with ClockSampler(local) as clocks:
+        for _ in range(args.steps):
+            torch.cuda.synchronize()
+            dist.barrier()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            _, vol = step()
+            e1.record()
+            torch.cuda.synchronize()
+            times.append(e0.elapsed_time(e1) / 1e3)
+    t = torch.tensor([statistics.mean(times)], device="cuda", dtype=torch.float64)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    t_step = float(t.item())
+    if rank == 0:
+        print(json.dumps({
+            "metric": METRIC, "value": n / t_step / 1e6, "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": t_step * 1e3,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (seeded generator, DESIGN.md Inputs)",
+            "config": {"workload": f"{cfgd.label} (BASELINE configs[1]) split over {world} GPUs",
+                       "n": n, "parallelism": f"rank layout dist.cpp:78-130 x{world}",
+                       "exchanged_blocks_per_step": vol,
+                       "step": "plan build (replicated) + distributed apply, host in/out"},
+            "e2e": {"value": n / t_step / 1e6, "unit": UNIT, "h2d_bytes_per_step": 5 * n * 8,
+                    "d2h_bytes_per_step": 2 * n * 8, "note": "the step is host-to-host"},
+            "gpu_launches": None, "roofline": None, "cpu_baseline": None,
+            "clocks": clocks.summary(),
+        }), flush=True)
+    dist.destroy_process_group()
+
+
 def main():
     args = parse()
     if args.impl == "reference":
         run_reference(args)
+    elif dist_env()[2] > 1:
+        run_ours_dist(args)
     else:
         run_ours(args)
 

@@ -94,13 +94,16 @@ int ifgf_plan_create_device(const double* d_x1, const double* d_x2, const double
                             const ifgf_params* p, void* stream, ifgf_plan** out);
 void ifgf_plan_destroy(ifgf_plan* plan);
 
-/* Plan options.  IFGF_OPT_SERIAL = 1 runs every apply kernel on one stream
- * (no near-field / interpolation overlap) so per-pass event times are
- * exclusive; used for per-kernel roofline measurement.  IFGF_OPT_NODE_PROP = 1
- * disables the precomputed (gamma, octant) propagation geometry (per-node
- * locate in K3).  IFGF_OPT_PROP_MMA = 1 selects the FP64 tensor-core (DMMA)
- * batched-GEMM propagation instead of the per-node evaluation. */
-enum { IFGF_OPT_SERIAL = 1, IFGF_OPT_NODE_PROP = 2, IFGF_OPT_PROP_MMA = 3 };
+/* Plan options.
+ * IFGF_OPT_SERIAL = 1: every apply kernel on one stream (no near-field /
+ *   interpolation overlap) so per-pass event times are exclusive.
+ * IFGF_OPT_PROP_KERNEL selects the propagation kernel:
+ *   IFGF_PROP_NODE  (0, default) thread per (parent cone, node), locate per child;
+ *   IFGF_PROP_TILES (1) per node from the precomputed (gamma, octant) geometry;
+ *   IFGF_PROP_DMMA  (2) FP64 tensor-core batched GEMM over cones sharing gamma.
+ *   All three agree to rounding; DESIGN.md records their measured times. */
+enum { IFGF_OPT_SERIAL = 1, IFGF_OPT_PROP_KERNEL = 2 };
+enum { IFGF_PROP_NODE = 0, IFGF_PROP_TILES = 1, IFGF_PROP_DMMA = 2 };
 int ifgf_plan_set_option(ifgf_plan* plan, int option, int value);
 
 /* ---- operator application; i_* in the caller's original point order ---- */

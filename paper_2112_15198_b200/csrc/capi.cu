@@ -113,9 +113,14 @@ InterpConsts make_consts(const ifgf_params* p) {
 void plan_free(ifgf_plan* P) {
   if (!P) return;
   cudaSetDevice(P->device);
-  if (P->s_main) cudaStreamSynchronize(P->s_main);
   if (P->s_aux) cudaStreamSynchronize(P->s_aux);
-  for (void* a : P->allocs) cudaFree(a);
+  // stream-ordered frees back into the pool (a cudaFree per allocation would
+  // synchronise the device ~150 times)
+  for (void* a : P->allocs) {
+    if (P->s_main) cudaFreeAsync(a, P->s_main);
+    else cudaFree(a);
+  }
+  if (P->s_main) cudaStreamSynchronize(P->s_main);
   if (P->s_main) cudaStreamDestroy(P->s_main);
   if (P->s_aux) cudaStreamDestroy(P->s_aux);
   delete P;
@@ -500,10 +505,15 @@ void ifgf_plan_destroy(ifgf_plan* plan) { plan_free(plan); }
 int ifgf_plan_set_option(ifgf_plan* P, int option, int value) {
   return guarded([&] {
     if (!P) throw Error(IFGF_EINVAL, "null plan");
-    if (option == IFGF_OPT_SERIAL) P->serial = value != 0;
-    else if (option == IFGF_OPT_NODE_PROP) P->force_node_prop = value != 0;
-    else if (option == IFGF_OPT_PROP_MMA) P->prop_mode = value != 0 ? 1 : 0;
-    else throw Error(IFGF_EINVAL, "unknown option");
+    if (option == IFGF_OPT_SERIAL) {
+      P->serial = value != 0;
+    } else if (option == IFGF_OPT_PROP_KERNEL) {
+      if (value < IFGF_PROP_NODE || value > IFGF_PROP_DMMA)
+        throw Error(IFGF_EINVAL, "unknown propagation kernel");
+      P->prop_kernel = value;
+    } else {
+      throw Error(IFGF_EINVAL, "unknown option");
+    }
   });
 }
 

@@ -344,8 +344,10 @@ void launch_level_d(ifgf_plan* P, uint32_t qb, uint32_t qe, double2* out, cudaSt
 void launch_propagation(ifgf_plan* P, int d, uint32_t qb, uint32_t qe, const double2* child,
                         double2* parent, cudaStream_t s) {
   if (qe <= qb) return;
-  // precomputed (gamma, octant) geometry when the plan built tiles for this level
-  if (!P->force_node_prop && launch_propagation_mma(P, d, qb, qe, child, parent, s)) return;
+  // precomputed (gamma, octant) geometry kernels when selected and the plan
+  // built tiles for this level (IFGF_OPT_PROP_KERNEL)
+  if (P->prop_kernel != IFGF_PROP_NODE && launch_propagation_mma(P, d, qb, qe, child, parent, s))
+    return;
   const Level& U = P->lv[d - 1];
   const Level& L = P->lv[d];
   const InterpConsts& K = P->K;

@@ -119,6 +119,7 @@ struct PropTiles {
   uint4* rt = nullptr;          // {child gamma, nodes 0-3 (u8), nodes 4-7 (u8), unused}
   uint32_t* fl_off = nullptr;   // flagged nodes CSR over tiles
   uint16_t* fl_node = nullptr;
+  uint8_t* e_perm = nullptr;    // per tile: nodes ordered by child gamma (flagged last)
   // CTA chunks of <= kChunk parent cones sharing one gamma
   uint32_t nchunks = 0;
   uint32_t* qsorted = nullptr;
@@ -153,8 +154,7 @@ struct ifgf_plan {
   double setup_seconds = 0.0;
   size_t launches = 0;  // kernels launched by this plan since the last reset
   bool serial = false;  // IFGF_OPT_SERIAL
-  bool force_node_prop = false;  // IFGF_OPT_NODE_PROP: per-node K3 only
-  int prop_mode = 0;  // IFGF_OPT_PROP_MMA: 0 tiles per node, 1 tensor-core GEMM
+  int prop_kernel = IFGF_PROP_NODE;  // IFGF_OPT_PROP_KERNEL
   size_t setup_launches = 0;
 
   template <class T>

@@ -53,11 +53,13 @@ struct TilesDev {
   const uint16_t* fl_node;
   const uint32_t* qsorted;
   const uint32_t* chunk_start;
+  const uint8_t* e_perm;
 };
 
 TilesDev tiles_dev(const PropTiles& t) {
-  return {t.ngamma, t.cone_gidx, t.gamma_of, t.e_t, t.e_T, t.e_gc, t.rt_off,
-          t.rt,     t.fl_off,    t.fl_node,  t.qsorted, t.chunk_start};
+  return {t.ngamma, t.cone_gidx, t.gamma_of, t.e_t,     t.e_T,
+          t.e_gc,   t.rt_off,    t.rt,       t.fl_off,  t.fl_node,
+          t.qsorted, t.chunk_start, t.e_perm};
 }
 
 inline unsigned nblk(size_t n, int t = 256) { return (unsigned)((n + t - 1) / t); }
@@ -140,7 +142,8 @@ __global__ void k_tile_entries(const __grid_constant__ LevelDev U, const __grid_
 // node order) into row tiles of 8; list flagged nodes.  Pass 1 counts.
 __global__ void k_tile_rows(uint32_t ntiles, int P, const uint32_t* e_gc, uint32_t* rt_cnt,
                             uint32_t* fl_cnt, const uint32_t* rt_off, uint4* rt,
-                            const uint32_t* fl_off, uint16_t* fl_node) {
+                            const uint32_t* fl_off, uint16_t* fl_node, uint8_t* e_perm) {
+  uint32_t wp = 0;
   const uint32_t tile = blockIdx.x * blockDim.x + threadIdx.x;
   if (tile >= ntiles) return;
   const uint32_t* g = e_gc + (size_t)tile * P;
@@ -168,6 +171,7 @@ __global__ void k_tile_rows(uint32_t ntiles, int P, const uint32_t* e_gc, uint32
     int k = 0;
     for (int m = 0; m < P; ++m) {
       if (g[m] != cur) continue;
+      if (e_perm) e_perm[(size_t)tile * P + wp++] = (uint8_t)m;
       const uint32_t sh = 8 * (k & 3);
       if (k < 4) R.y = (R.y & ~(0xffu << sh)) | ((uint32_t)m << sh);
       else R.z = (R.z & ~(0xffu << sh)) | ((uint32_t)m << sh);
@@ -186,6 +190,7 @@ __global__ void k_tile_rows(uint32_t ntiles, int P, const uint32_t* e_gc, uint32
   for (int m = 0; m < P; ++m)
     if (g[m] & kFlag) {
       if (fl_node) fl_node[wfl++] = (uint16_t)m;
+      if (e_perm) e_perm[(size_t)tile * P + wp++] = (uint8_t)m;
       ++nfl;
     }
   if (rt_cnt) {
@@ -487,10 +492,14 @@ __global__ void __launch_bounds__(kMmaWarps * 32)
   fit_cones_scatter<PS, PT, PP>(K, acc, scr, nq, parent, qs, err);
 }
 
-// K3 per node with the tile geometry: thread = (parent cone, node); for each
-// child the (child gamma, t, transfer) entry of its (gamma, octant) tile
-// replaces locate + node trigonometry + sincos; flagged entries take the
-// per-box exact path.  CTAs walk consecutive cones (box-major) for L1 reuse.
+// K3 per node with the tile geometry: thread = (parent cone, lane j); for
+// child octant o the lane takes the j-th node of tile (gamma, o) in child-cone
+// order, so neighbouring lanes read the same child block (broadcast loads --
+// the per-node evaluation is L1-throughput bound when lanes diverge).  The
+// (child gamma, t, transfer) entry replaces locate + node trigonometry +
+// sincos; flagged entries take the per-box exact path.  Node sums live in
+// shared memory; octants are processed in Morton order with a CTA barrier in
+// between, which keeps the reference's child summation order.
 template <int PS, int PT, int PP, bool LAP>
 __global__ void __launch_bounds__(320, 2)
     k_propagate_tab(const __grid_constant__ LevelDev U, const __grid_constant__ LevelDev L,
@@ -502,22 +511,45 @@ __global__ void __launch_bounds__(320, 2)
   extern __shared__ double2 smem[];
   double2* sv = smem;
   double2* st = smem + cpb * P;
-  const int c = threadIdx.x / P, m = threadIdx.x % P;
+  __shared__ uint32_t cfirst[16], cnum[16];
+  __shared__ int kmax_s;
+  const int c = threadIdx.x / P, j = threadIdx.x % P;
   for (int g = 0; g < groups; ++g) {
     const uint32_t q0 = qb + ((uint32_t)blockIdx.x * groups + g) * cpb;
     if (q0 >= qe) break;
     const int ncon = (int)min((uint32_t)cpb, qe - q0);
-    if (c < ncon) {
-      const uint32_t q = q0 + c;
-      const uint32_t pb = U.cone_box[q];
-      const size_t tbase = (size_t)T.cone_gidx[q] * 8;
-      double acr = 0.0, aci = 0.0;
-      const uint32_t c0 = U.child_begin[pb], c1 = U.child_begin[pb + 1];
-      for (uint32_t cb = c0; cb < c1; ++cb) {
-        const size_t e = (tbase + (L.code[cb] & 7)) * P + m;
+    if (threadIdx.x < cpb) {
+      const int cc = threadIdx.x;
+      cfirst[cc] = 0;
+      cnum[cc] = 0;
+      if (cc < ncon) {
+        const uint32_t pb = U.cone_box[q0 + cc];
+        cfirst[cc] = U.child_begin[pb];
+        cnum[cc] = U.child_begin[pb + 1] - U.child_begin[pb];
+      }
+    }
+    for (int i = threadIdx.x; i < cpb * P; i += blockDim.x) sv[i] = make_double2(0.0, 0.0);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      uint32_t k = 0;
+      for (int cc = 0; cc < ncon; ++cc) k = max(k, cnum[cc]);
+      kmax_s = (int)k;
+    }
+    __syncthreads();
+    const bool active = c < ncon;
+    const uint32_t q = q0 + c;
+    const size_t tbase = active ? (size_t)T.cone_gidx[q] * 8 : 0;
+    const int kmax = kmax_s;
+    for (int kc = 0; kc < kmax; ++kc) {  // k-th child, ascending Morton order
+      const uint32_t cb = (active && (uint32_t)kc < cnum[c]) ? cfirst[c] + kc : kNone;
+      if (cb != kNone) {
+        const size_t tile = tbase + (L.code[cb] & 7);
+        const int m = T.e_perm[tile * P + j];
+        const size_t e = tile * P + m;
         const uint32_t gc = T.e_gc[e];
         double ts, tt, tp, tr, ti;
         uint32_t cq;
+        bool ok = true;
         if (!(gc & kFlag)) {
           cq = find_cone(L, cb, gc);
           ts = T.e_t[3 * e];
@@ -527,6 +559,7 @@ __global__ void __launch_bounds__(320, 2)
           tr = Tf.x;
           ti = Tf.y;
         } else {
+          const uint32_t pb = U.cone_box[q];
           const int jp = m % PP, jt = (m / PP) % PT, js = m / (PP * PT);
           const SegMid sg = segment_mid(U, U.cone_gamma[q]);
           const double pcx = U.cx[pb], pcy = U.cy[pb], pcz = U.cz[pb];
@@ -538,30 +571,33 @@ __global__ void __launch_bounds__(320, 2)
           const int er = locate_fast(L, L.cx[cb], L.cy[cb], L.cz[cb], x, y, z, lo);
           if (er) {
             raise_err(err, er);
-            break;
+            ok = false;
           }
-          cq = find_cone(L, cb, lo.gamma);
+          cq = ok ? find_cone(L, cb, lo.gamma) : kNone;
           ts = lo.ts;
           tt = lo.tt;
           tp = lo.tp;
           const double ratio = rp * lo.rinv;
           double sn = 0.0, cn = 1.0;
-          if (!LAP) sincos_fast(kappa * (lo.r - rp), sn, cn);
+          if (!LAP && ok) sincos_fast(kappa * (lo.r - rp), sn, cn);
           tr = ratio * cn;
           ti = ratio * sn;
         }
-        if (cq == kNone) {
+        if (ok && cq == kNone) {
           raise_err(err, kErrPropCover);
-          break;
+          ok = false;
         }
-        double vr, vi;
-        eval_block<PS, PT, PP>(child + (size_t)cq * BL::Pst, ts, tt, tp, vr, vi);
-        acr = fma(vr, tr, fma(-vi, ti, acr));
-        aci = fma(vr, ti, fma(vi, tr, aci));
+        if (ok) {
+          double vr, vi;
+          eval_block<PS, PT, PP>(child + (size_t)cq * BL::Pst, ts, tt, tp, vr, vi);
+          double2 v = sv[c * P + m];
+          v.x = fma(vr, tr, fma(-vi, ti, v.x));
+          v.y = fma(vr, ti, fma(vi, tr, v.y));
+          sv[c * P + m] = v;
+        }
       }
-      sv[c * P + m] = make_double2(acr, aci);
+      __syncthreads();
     }
-    __syncthreads();
     fit_cones<PS, PT, PP>(K, sv, st, ncon, parent + (size_t)q0 * BL::Pst, err);
     __syncthreads();
   }
@@ -633,7 +669,7 @@ void build_prop_tiles(ifgf_plan* P, int d, void* (*scratch)(void*, size_t), void
   IFGF_CUDA(cudaMemsetAsync(rt_cnt + ntiles, 0, 4, s));
   IFGF_CUDA(cudaMemsetAsync(fl_cnt + ntiles, 0, 4, s));
   k_tile_rows<<<nblk(ntiles, 64), 64, 0, s>>>(ntiles, K.P, T.e_gc, rt_cnt, fl_cnt, nullptr,
-                                              nullptr, nullptr, nullptr);
+                                              nullptr, nullptr, nullptr, nullptr);
   T.rt_off = P->alloc<uint32_t>(ntiles + 1);
   T.fl_off = P->alloc<uint32_t>(ntiles + 1);
   {
@@ -650,8 +686,9 @@ void build_prop_tiles(ifgf_plan* P, int d, void* (*scratch)(void*, size_t), void
   IFGF_CUDA(cudaStreamSynchronize(s));
   T.rt = P->alloc<uint4>(tot[0] + 1);
   T.fl_node = P->alloc<uint16_t>(tot[1] + 1);
+  T.e_perm = P->alloc<uint8_t>(ne);
   k_tile_rows<<<nblk(ntiles, 64), 64, 0, s>>>(ntiles, K.P, T.e_gc, nullptr, nullptr, T.rt_off,
-                                              T.rt, T.fl_off, T.fl_node);
+                                              T.rt, T.fl_off, T.fl_node, T.e_perm);
   // parent cones sorted by gamma index (stable) -> chunks of <= kChunk
   uint32_t* qidx = P->alloc<uint32_t>(U.nc);
   uint32_t* gsorted = P->alloc<uint32_t>(U.nc);
@@ -701,14 +738,14 @@ bool launch_propagation_mma(ifgf_plan* P, int d, uint32_t qb, uint32_t qe, const
   const PropTiles& T = P->tiles[d];
   if (!T.enabled || T.nchunks == 0) return false;
   const bool full = qb == 0 && qe == P->lv[d - 1].nc;
-  if (P->prop_mode == 0 || !full) {  // per node from the tiles (default; any cone range)
+  if (P->prop_kernel == IFGF_PROP_TILES || !full) {  // per node from the tiles (any range)
     const Level& U = P->lv[d - 1];
     const Level& L = P->lv[d];
     const InterpConsts& K = P->K;
     return dispatch_mma_orders(K.ps, K.pt, K.pp, [&](auto A, auto B, auto C) {
       constexpr int PS = decltype(A)::value, PT = decltype(B)::value, PP = decltype(C)::value;
       constexpr int Pn = PS * PT * PP;
-      int cpb = std::max(1, 320 / Pn);
+      int cpb = std::max(1, std::min(16, 320 / Pn));
       const uint32_t nq = qe - qb;
       const int groups =
           (int)std::min<size_t>(8, std::max<size_t>(1, nq / ((size_t)cpb * 148 * 8)));

@@ -141,3 +141,16 @@ def test_direct_eval(built, gpu, oracle):
     gpu.direct_eval(q, cfg, targets=idx)
     o = oracle.direct(pc.x1, pc.x2, pc.x3, pc.a_re, pc.a_im, int(cfg.kind), cfg.wavenumber, idx)
     assert rel_l2(q.i_re[idx], q.i_im[idx], *o) <= 1e-13
+
+
+def test_propagation_kernels_agree(built):
+    """The three K3 implementations (per-node locate, precomputed tiles, FP64
+    DMMA batched GEMM) compute the same operator up to rounding."""
+    case, pc, cfg, ep, op, plan, prob = built
+    res = []
+    for kind in (plan.PROP_NODE, plan.PROP_TILES, plan.PROP_DMMA):
+        plan.set_prop_kernel(kind)
+        res.append(plan.apply(pc.a_re, pc.a_im)[:2])
+    plan.set_prop_kernel(plan.PROP_NODE)
+    for r in res[1:]:
+        assert rel_l2(r[0], r[1], res[0][0], res[0][1]) <= 1e-13

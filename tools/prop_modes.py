@@ -6,9 +6,8 @@ cfg = ifgf.KernelConfig(ifgf.KernelKind(c.kind), c.kappa)
 plan = ifgf.Plan.from_cloud(pc, cfg, ifgf.EngineParams())
 plan.set_serial(True)
 ref = None
-for name, opts in [("tab", {}), ("mma", {3: 1}), ("node", {2: 1})]:
-    plan.set_option(2, 0); plan.set_option(3, 0)
-    for k, v in opts.items(): plan.set_option(k, v)
+for name, kind in [("node", 0), ("tiles", 1), ("dmma", 2)]:
+    plan.set_prop_kernel(kind)
     for _ in range(3): ir, ii, rep = plan.apply(pc.a_re, pc.a_im)
     import numpy as np
     if ref is None: ref = (ir, ii)
