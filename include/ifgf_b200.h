@@ -98,12 +98,17 @@ void ifgf_plan_destroy(ifgf_plan* plan);
  * IFGF_OPT_SERIAL = 1: every apply kernel on one stream (no near-field /
  *   interpolation overlap) so per-pass event times are exclusive.
  * IFGF_OPT_PROP_KERNEL selects the propagation kernel:
- *   IFGF_PROP_NODE  (0, default) thread per (parent cone, node), locate per child;
+ *   IFGF_PROP_NODE  (0) thread per (parent cone, node), locate per child;
  *   IFGF_PROP_TILES (1) per node from the precomputed (gamma, octant) geometry;
- *   IFGF_PROP_DMMA  (2) FP64 tensor-core batched GEMM over cones sharing gamma.
- *   All three agree to rounding; DESIGN.md records their measured times. */
+ *   IFGF_PROP_DMMA  (2) FP64 tensor-core batched GEMM over cones sharing gamma;
+ *   IFGF_PROP_ROWS  (3, default) thread per (parent cone, child, row of <= 3
+ *                       nodes that share a child cone) from the precomputed
+ *                       geometry, one block load per row.
+ *   Where the precomputed geometry is not built (too few parent cones per
+ *   gamma, P > 255) every setting runs IFGF_PROP_NODE.
+ *   All agree to rounding; DESIGN.md records their measured times. */
 enum { IFGF_OPT_SERIAL = 1, IFGF_OPT_PROP_KERNEL = 2 };
-enum { IFGF_PROP_NODE = 0, IFGF_PROP_TILES = 1, IFGF_PROP_DMMA = 2 };
+enum { IFGF_PROP_NODE = 0, IFGF_PROP_TILES = 1, IFGF_PROP_DMMA = 2, IFGF_PROP_ROWS = 3 };
 int ifgf_plan_set_option(ifgf_plan* plan, int option, int value);
 
 /* ---- operator application; i_* in the caller's original point order ---- */

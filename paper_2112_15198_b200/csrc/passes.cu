@@ -152,6 +152,9 @@ __global__ void __launch_bounds__(320, IFGF_PROP_MINB)
   extern __shared__ double2 smem[];
   double2* sv = smem;
   double2* st = smem + cpb * P;
+  __shared__ double2 trig[kTrigEntries];
+  stage_trig(trig, L.trig);
+  __syncthreads();
   const int c = threadIdx.x / P, m = threadIdx.x % P;
   const int jp = m % PP, jt = (m / PP) % PT, js = m / (PP * PT);
   for (int g = 0; g < groups; ++g) {
@@ -171,7 +174,7 @@ __global__ void __launch_bounds__(320, IFGF_PROP_MINB)
       const uint32_t c0 = U.child_begin[pb], c1 = U.child_begin[pb + 1];
       for (uint32_t cb = c0; cb < c1; ++cb) {
         Loc o;
-        const int e = locate_fast(L, L.cx[cb], L.cy[cb], L.cz[cb], x, y, z, o);
+        const int e = locate_fast(L, trig, L.cx[cb], L.cy[cb], L.cz[cb], x, y, z, o);
         if (e) {
           raise_err(err, e);
           break;
@@ -211,6 +214,9 @@ __global__ void __launch_bounds__(128, IFGF_INTERP_MINB)
              size_t b0, size_t e0, const double2* __restrict__ blocks, double* ir, double* ii,
              int* err) {
   constexpr int P = PS * PT * PP;
+  __shared__ double2 trig[kTrigEntries];
+  stage_trig(trig, L.trig);
+  __syncthreads();
   const size_t i = b0 + blockIdx.x * (size_t)blockDim.x + threadIdx.x;
   if (i >= e0) return;
   const uint32_t b = ptbox[i];
@@ -220,7 +226,7 @@ __global__ void __launch_bounds__(128, IFGF_INTERP_MINB)
   for (uint32_t k = k0; k < k1; ++k) {
     const uint32_t cb = L.cous[k];
     Loc o;
-    const int e = locate_fast(L, L.cx[cb], L.cy[cb], L.cz[cb], x, y, z, o);
+    const int e = locate_fast(L, trig, L.cx[cb], L.cy[cb], L.cz[cb], x, y, z, o);
     if (e) {
       raise_err(err, e);
       return;

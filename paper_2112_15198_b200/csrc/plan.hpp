@@ -57,7 +57,7 @@ struct Level {
   uint64_t* bits = nullptr;
   uint32_t* rank = nullptr;
   size_t nwords = 0;
-  const double4* trig = nullptr;
+  const double2* trig = nullptr;
 
   LevelDev dev() const {
     LevelDev v;
@@ -120,6 +120,18 @@ struct PropTiles {
   uint32_t* fl_off = nullptr;   // flagged nodes CSR over tiles
   uint16_t* fl_node = nullptr;
   uint8_t* e_perm = nullptr;    // per tile: nodes ordered by child gamma (flagged last)
+  // rows of <= row_nodes nodes sharing one child gamma (IFGF_PROP_ROWS);
+  // CSR over tiles; entry data permuted into row order
+  int row_nodes = 3;
+  uint32_t* rw_off = nullptr;
+  uint2* rw = nullptr;          // {child gamma, first permuted position | count << 16}
+  struct Ent {
+    double ts, tt;  // local coordinates (16-byte aligned pairs)
+    double tr, ti;  // transfer factor
+    double tp;
+    uint32_t node, pad;
+  };
+  Ent* ent = nullptr;           // [(gidx * 8 + octant) * P + permuted position]
   // CTA chunks of <= kChunk parent cones sharing one gamma
   uint32_t nchunks = 0;
   uint32_t* qsorted = nullptr;
@@ -154,7 +166,7 @@ struct ifgf_plan {
   double setup_seconds = 0.0;
   size_t launches = 0;  // kernels launched by this plan since the last reset
   bool serial = false;  // IFGF_OPT_SERIAL
-  int prop_kernel = IFGF_PROP_NODE;  // IFGF_OPT_PROP_KERNEL
+  int prop_kernel = IFGF_PROP_ROWS;  // IFGF_OPT_PROP_KERNEL
   size_t setup_launches = 0;
 
   template <class T>

@@ -22,6 +22,7 @@
 #include <cub/cub.cuh>
 
 #include <algorithm>
+#include <cstdlib>
 #include <vector>
 
 #include "plan.hpp"
@@ -39,6 +40,16 @@ constexpr int kChunk = IFGF_MMA_CHUNK;    // parent cones per CTA (column tiles 
 constexpr int kMmaWarps = IFGF_MMA_WARPS;  // warps per CTA
 constexpr uint32_t kNone = 0xffffffffu;
 constexpr uint32_t kFlag = 0x80000000u;
+// 12 warps of <= 168 registers per SM (measured best at C2 among 256/320/384
+// threads and 1-2 CTAs per SM)
+#ifndef IFGF_ROWS_THREADS
+#define IFGF_ROWS_THREADS 384
+#endif
+#ifndef IFGF_ROWS_MINB
+#define IFGF_ROWS_MINB 1
+#endif
+constexpr int kRowThreads = IFGF_ROWS_THREADS;
+constexpr int kRowMaxCpw = 16;  // parent cones per warp
 
 struct TilesDev {
   uint32_t ngamma;
@@ -54,12 +65,15 @@ struct TilesDev {
   const uint32_t* qsorted;
   const uint32_t* chunk_start;
   const uint8_t* e_perm;
+  const uint32_t* rw_off;
+  const uint2* rw;
+  const PropTiles::Ent* ent;
 };
 
 TilesDev tiles_dev(const PropTiles& t) {
-  return {t.ngamma, t.cone_gidx, t.gamma_of, t.e_t,     t.e_T,
-          t.e_gc,   t.rt_off,    t.rt,       t.fl_off,  t.fl_node,
-          t.qsorted, t.chunk_start, t.e_perm};
+  return {t.ngamma,   t.cone_gidx,   t.gamma_of, t.e_t,    t.e_T,  t.e_gc, t.rt_off,
+          t.rt,       t.fl_off,      t.fl_node,  t.qsorted, t.chunk_start, t.e_perm,
+          t.rw_off,   t.rw,          t.ent};
 }
 
 inline unsigned nblk(size_t n, int t = 256) { return (unsigned)((n + t - 1) / t); }
@@ -197,6 +211,48 @@ __global__ void k_tile_rows(uint32_t ntiles, int P, const uint32_t* e_gc, uint32
     rt_cnt[tile] = nrt;
     fl_cnt[tile] = nfl;
   }
+}
+
+// One thread per tile: rows of <= rmax consecutive nodes of one child
+// gamma group, in e_perm order (flagged nodes, which e_perm lists last, are
+// not in any row).  Pass 1 (rw == nullptr) counts.
+__global__ void k_tile_rows_n(uint32_t ntiles, int P, int rmax, const uint32_t* e_gc,
+                              const uint8_t* e_perm, uint32_t* cnt, const uint32_t* off,
+                              uint2* rw) {
+  const uint32_t tile = blockIdx.x * blockDim.x + threadIdx.x;
+  if (tile >= ntiles) return;
+  const uint32_t* g = e_gc + (size_t)tile * P;
+  const uint8_t* pm = e_perm + (size_t)tile * P;
+  uint32_t n = 0, w = rw ? off[tile] : 0;
+  int p = 0;
+  while (p < P) {
+    const uint32_t gc = g[pm[p]];
+    if (gc & kFlag) break;
+    int k = 1;
+    while (k < rmax && p + k < P && g[pm[p + k]] == gc) ++k;
+    if (rw) rw[w++] = make_uint2(gc, (uint32_t)p | ((uint32_t)k << 16));
+    ++n;
+    p += k;
+  }
+  if (cnt) cnt[tile] = n;
+}
+
+// One thread per (tile, permuted position): entry data in row order.
+__global__ void k_tile_ent(size_t ne, int P, const uint8_t* e_perm, const double* e_t,
+                           const double2* e_T, PropTiles::Ent* ent) {
+  const size_t t = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
+  if (t >= ne) return;
+  const int m = e_perm[t];
+  const size_t e = (t / P) * P + m;
+  PropTiles::Ent x;
+  x.ts = e_t[3 * e];
+  x.tt = e_t[3 * e + 1];
+  x.tp = e_t[3 * e + 2];
+  x.tr = e_T[e].x;
+  x.ti = e_T[e].y;
+  x.node = (uint32_t)m;
+  x.pad = 0;
+  ent[t] = x;
 }
 
 __global__ void k_chunk_flags(const uint32_t* gsorted, uint32_t n, uint32_t* flag) {
@@ -603,6 +659,182 @@ __global__ void __launch_bounds__(320, 2)
   }
 }
 
+// K3 with register-blocked rows: task = (parent cone, child k, row of <= R
+// nodes whose child cone coincides -- box-independent, from the tiles).  The
+// thread loads the child block once and evaluates all nodes of the row
+// (eval_block_multi), so a coefficient load feeds R FMA chains instead of
+// one; the per-node kernel is bound by L1->register bandwidth (16 B per
+// 2 FMAs, also for broadcast loads).  Flagged nodes (within the margin of a
+// cone boundary) take the exact per-box path.  Each warp works alone on
+// `cpw` consecutive parent cones at a time: it walks their children in
+// Morton order with a warp barrier in between (every node receives one
+// contribution per child, in the reference's child order: deterministic
+// sums), then fits them (fit_cones_warp).  No CTA barriers, so load
+// imbalance stays within the warp.
+template <int PS, int PT, int PP, bool LAP, int R>
+__global__ void __launch_bounds__(kRowThreads, IFGF_ROWS_MINB)
+    k_propagate_rows(const __grid_constant__ LevelDev U, const __grid_constant__ LevelDev L,
+                     const __grid_constant__ InterpConsts K, const TilesDev T, double kappa,
+                     uint32_t qb, uint32_t qe, int cpw, int groups,
+                     const double2* __restrict__ child, double2* parent, int* err) {
+  using BL = BlockLayout<PS, PT, PP>;
+  constexpr int P = PS * PT * PP;
+  constexpr int NW = kRowThreads / 32;
+  extern __shared__ double2 smem[];
+  __shared__ uint32_t s_cb0[NW][kRowMaxCpw], s_tile[NW][kRowMaxCpw], s_nrow[NW][kRowMaxCpw],
+      s_pre[NW][kRowMaxCpw + 1];
+  __shared__ double sM[PP * PP + PT * PT + PS * PS];
+  stage_fit_matrices<PS, PT, PP>(K, sM);
+  __syncthreads();
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  double2* sv = smem + (size_t)w * 2 * cpw * P;
+  double2* st = sv + cpw * P;
+  for (int g = 0; g < groups; ++g) {
+    const uint32_t q0 = qb + (((uint32_t)blockIdx.x * groups + g) * NW + w) * cpw;
+    if (q0 >= qe) break;
+    const int nw = (int)min((uint32_t)cpw, qe - q0);
+    for (int i = lane; i < nw * P; i += 32) sv[i] = make_double2(0.0, 0.0);
+    uint32_t cb0 = 0, nch = 0, tbase = 0;
+    if (lane < nw) {
+      const uint32_t q = q0 + lane;
+      const uint32_t pb = U.cone_box[q];
+      cb0 = U.child_begin[pb];
+      nch = U.child_begin[pb + 1] - cb0;
+      tbase = T.cone_gidx[q] * 8;
+    }
+    if (lane < cpw) s_cb0[w][lane] = cb0;
+    uint32_t kmax = nch;
+#pragma unroll
+    for (int o = 16; o; o >>= 1) kmax = max(kmax, __shfl_xor_sync(0xffffffffu, kmax, o));
+    for (uint32_t kc = 0; kc < kmax; ++kc) {  // k-th child, ascending Morton order
+      uint32_t n = 0, tile = 0, nrow = 0;
+      if (lane < nw && kc < nch) {
+        const uint32_t cb = cb0 + kc;
+        tile = tbase + (uint32_t)(L.code[cb] & 7);
+        const uint32_t r0 = T.rw_off[tile];
+        nrow = T.rw_off[tile + 1] - r0;
+        n = nrow + T.fl_off[tile + 1] - T.fl_off[tile];
+      }
+      uint32_t incl = n;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t v = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += v;
+      }
+      const uint32_t total = __shfl_sync(0xffffffffu, incl, 31);
+      __syncwarp();  // previous child's readers of s_* are done
+      if (lane < cpw) {
+        s_tile[w][lane] = tile;
+        s_nrow[w][lane] = nrow;
+        s_pre[w][lane + 1] = incl;
+      }
+      if (lane == 0) s_pre[w][0] = 0;
+      __syncwarp();
+      // task t -> (cone c, row) and its child block; the next task's block is
+      // prefetched into L1 while the current one is evaluated
+      auto row_of = [&](uint32_t t, int& c, uint32_t& cq, uint32_t& rwy) {
+        c = 0;
+        while (s_pre[w][c + 1] <= t) ++c;
+        const uint32_t tl = s_tile[w][c], loc = t - s_pre[w][c];
+        cq = kNone;
+        rwy = 0;
+        if (loc < s_nrow[w][c]) {
+          const uint2 rw = T.rw[T.rw_off[tl] + loc];
+          rwy = rw.y;
+          cq = find_cone(L, s_cb0[w][c] + kc, rw.x);
+        }
+      };
+      int nc_ = 0;
+      uint32_t ncq = kNone, nrwy = 0;
+      if (lane < total) row_of(lane, nc_, ncq, nrwy);
+      for (uint32_t t = lane; t < total; t += 32) {
+        const int c = nc_;
+        const uint32_t cq = ncq, rwy = nrwy;
+        if (t + 32 < total) {
+          row_of(t + 32, nc_, ncq, nrwy);
+          if (ncq != kNone) {
+            const char* pf = (const char*)(child + (size_t)ncq * BL::Pst);
+#pragma unroll
+            for (int l = 0; l < (BL::Pst * 16 + 127) / 128; ++l)
+              asm volatile("prefetch.global.L1 [%0];" ::"l"(pf + 128 * l));
+          }
+        }
+        const uint32_t tl = s_tile[w][c], cb = s_cb0[w][c] + kc, loc = t - s_pre[w][c];
+        double2* acc = sv + c * P;
+        if (loc < s_nrow[w][c]) {
+          if (cq == kNone) {
+            raise_err(err, kErrPropCover);
+            continue;
+          }
+          const int pos = (int)(rwy & 0xffffu), cnt = (int)(rwy >> 16);
+          const PropTiles::Ent* en = T.ent + (size_t)tl * P + pos;
+          double ts[R], tt[R], tp[R];
+#pragma unroll
+          for (int j = 0; j < R; ++j) {
+            if (j < cnt) {
+              const double2 a = __ldg((const double2*)&en[j].ts);
+              ts[j] = a.x;
+              tt[j] = a.y;
+              tp[j] = __ldg(&en[j].tp);
+            } else {
+              ts[j] = tt[j] = tp[j] = 0.0;
+            }
+          }
+          double vr[R], vi[R];
+          eval_block_multi<PS, PT, PP, R>(child + (size_t)cq * BL::Pst, ts, tt, tp, vr, vi);
+#pragma unroll
+          for (int j = 0; j < R; ++j) {
+            if (j < cnt) {
+              const double2 b = __ldg((const double2*)&en[j].tr);  // tr, ti
+              const int m = (int)__ldg(&en[j].node);
+              double2 v = acc[m];
+              v.x = fma(vr[j], b.x, fma(-vi[j], b.y, v.x));
+              v.y = fma(vr[j], b.y, fma(vi[j], b.x, v.y));
+              acc[m] = v;
+            }
+          }
+        } else {
+          // flagged node: the exact per-box path
+          const uint32_t q = q0 + c;
+          const int m = T.fl_node[T.fl_off[tl] + (loc - s_nrow[w][c])];
+          const uint32_t pb = U.cone_box[q];
+          const int jp = m % PP, jt = (m / PP) % PT, js = m / (PP * PT);
+          const SegMid sg = segment_mid(U, U.cone_gamma[q]);
+          const double pcx = U.cx[pb], pcy = U.cy[pb], pcz = U.cz[pb];
+          double x, y, z;
+          node_position(sg, U.rad, pcx, pcy, pcz, K.ns[js], K.nt[jt], K.np[jp], x, y, z);
+          const double ux = x - pcx, uy = y - pcy, uz = z - pcz;
+          const double rp = sqrt(fma(uz, uz, fma(uy, uy, ux * ux)));
+          Loc lo;
+          const int er = locate_fast(L, L.cx[cb], L.cy[cb], L.cz[cb], x, y, z, lo);
+          if (er) {
+            raise_err(err, er);
+            continue;
+          }
+          const uint32_t cq = find_cone(L, cb, lo.gamma);
+          if (cq == kNone) {
+            raise_err(err, kErrPropCover);
+            continue;
+          }
+          double vr, vi;
+          eval_block<PS, PT, PP>(child + (size_t)cq * BL::Pst, lo.ts, lo.tt, lo.tp, vr, vi);
+          const double ratio = rp * lo.rinv;
+          double sn = 0.0, cn = 1.0;
+          if (!LAP) sincos_fast(kappa * (lo.r - rp), sn, cn);
+          const double tr = ratio * cn, ti = ratio * sn;
+          double2 v = acc[m];
+          v.x = fma(vr, tr, fma(-vi, ti, v.x));
+          v.y = fma(vr, ti, fma(vi, tr, v.y));
+          acc[m] = v;
+        }
+      }
+      __syncwarp();
+    }
+    fit_cones_warp<PS, PT, PP>(sM, sv, st, nw, parent + (size_t)q0 * BL::Pst, err);
+    __syncwarp();
+  }
+}
+
 template <class F>
 bool dispatch_mma_orders(int ps, int pt, int pp, F&& f) {
 #define IFGF_MMA_CASE(a, b, c)          \
@@ -620,6 +852,29 @@ bool dispatch_mma_orders(int ps, int pt, int pp, F&& f) {
   return false;
 }
 
+// Orders served by the tiles and the row kernel: every shipped order triple
+// (passes.cu dispatch_orders).
+template <class F>
+bool dispatch_rows_orders(int ps, int pt, int pp, F&& f) {
+#define IFGF_ROWS_CASE(a, b, c)         \
+  if (ps == a && pt == b && pp == c) {  \
+    f(std::integral_constant<int, a>{}, std::integral_constant<int, b>{}, \
+      std::integral_constant<int, c>{}); \
+    return true;                        \
+  }
+  IFGF_ROWS_CASE(3, 5, 5)
+  IFGF_ROWS_CASE(4, 6, 6)
+  IFGF_ROWS_CASE(5, 7, 7)
+  IFGF_ROWS_CASE(1, 1, 1)
+  IFGF_ROWS_CASE(2, 2, 2)
+  IFGF_ROWS_CASE(3, 3, 3)
+  IFGF_ROWS_CASE(4, 4, 4)
+  IFGF_ROWS_CASE(2, 3, 3)
+  IFGF_ROWS_CASE(3, 4, 4)
+#undef IFGF_ROWS_CASE
+  return false;
+}
+
 
 }  // namespace
 
@@ -631,7 +886,7 @@ void build_prop_tiles(ifgf_plan* P, int d, void* (*scratch)(void*, size_t), void
   const InterpConsts& K = P->K;
   cudaStream_t s = P->s_main;
   if (U.nc == 0 || K.P > 255) return;
-  if (!dispatch_mma_orders(K.ps, K.pt, K.pp, [](auto, auto, auto) {})) return;
+  if (!dispatch_rows_orders(K.ps, K.pt, K.pp, [](auto, auto, auto) {})) return;
   if (U.G > (1ull << 28)) return;  // gamma bitmap too large: per-node kernel
   // distinct parent gammas
   const size_t nw = (U.G + 63) / 64;
@@ -689,6 +944,31 @@ void build_prop_tiles(ifgf_plan* P, int d, void* (*scratch)(void*, size_t), void
   T.e_perm = P->alloc<uint8_t>(ne);
   k_tile_rows<<<nblk(ntiles, 64), 64, 0, s>>>(ntiles, K.P, T.e_gc, nullptr, nullptr, T.rt_off,
                                               T.rt, T.fl_off, T.fl_node, T.e_perm);
+  // rows of <= row_nodes (IFGF_PROP_ROWS) and the entries in row order
+  {
+    static const int rn_env = [] {
+      const char* v = std::getenv("IFGF_ROWS_R");
+      return v ? std::atoi(v) : 0;
+    }();
+    // nodes per row: register budget of eval_block_multi (~17 doubles per node)
+    T.row_nodes = rn_env >= 2 && rn_env <= 3 ? rn_env : (K.P <= 100 ? 3 : 2);
+    k_tile_rows_n<<<nblk(ntiles, 64), 64, 0, s>>>(ntiles, K.P, T.row_nodes, T.e_gc, T.e_perm,
+                                                  rt_cnt, nullptr, nullptr);
+    T.rw_off = P->alloc<uint32_t>(ntiles + 1);
+    size_t tb = 0;
+    cub::DeviceScan::ExclusiveSum(nullptr, tb, rt_cnt, T.rw_off, (int)(ntiles + 1), s);
+    IFGF_CUDA(cub::DeviceScan::ExclusiveSum(scratch(sctx, tb), tb, rt_cnt, T.rw_off,
+                                            (int)(ntiles + 1), s));
+    uint32_t nrw = 0;
+    IFGF_CUDA(cudaMemcpyAsync(&nrw, T.rw_off + ntiles, 4, cudaMemcpyDeviceToHost, s));
+    IFGF_CUDA(cudaStreamSynchronize(s));
+    T.rw = P->alloc<uint2>(nrw + 1);
+    k_tile_rows_n<<<nblk(ntiles, 64), 64, 0, s>>>(ntiles, K.P, T.row_nodes, T.e_gc, T.e_perm,
+                                                  nullptr, T.rw_off, T.rw);
+    T.ent = P->alloc<PropTiles::Ent>(ne);
+    k_tile_ent<<<nblk(ne, 256), 256, 0, s>>>(ne, K.P, T.e_perm, T.e_t, T.e_T, T.ent);
+    P->launches += 4;
+  }
   // parent cones sorted by gamma index (stable) -> chunks of <= kChunk
   uint32_t* qidx = P->alloc<uint32_t>(U.nc);
   uint32_t* gsorted = P->alloc<uint32_t>(U.nc);
@@ -738,6 +1018,42 @@ bool launch_propagation_mma(ifgf_plan* P, int d, uint32_t qb, uint32_t qe, const
   const PropTiles& T = P->tiles[d];
   if (!T.enabled || T.nchunks == 0) return false;
   const bool full = qb == 0 && qe == P->lv[d - 1].nc;
+  if (P->prop_kernel == IFGF_PROP_ROWS) {
+    const Level& U = P->lv[d - 1];
+    const Level& L = P->lv[d];
+    const InterpConsts& K = P->K;
+    return dispatch_rows_orders(K.ps, K.pt, K.pp, [&](auto A, auto B, auto C) {
+      constexpr int PS = decltype(A)::value, PT = decltype(B)::value, PP = decltype(C)::value;
+      constexpr int Pn = PS * PT * PP;
+      constexpr int NW = kRowThreads / 32;
+      static const int cpw_env = [] {
+        const char* v = std::getenv("IFGF_ROWS_CPW");
+        return v ? std::atoi(v) : 0;
+      }();
+      // shared memory for sv + st: ~64 KB per CTA (the rest of the SM's SRAM is L1)
+      const int cpw_fit = (int)(64 * 1024 / IFGF_ROWS_MINB / (2 * Pn * sizeof(double2)) / NW);
+      const int cpw = std::max(1, std::min(kRowMaxCpw, cpw_env > 0 ? cpw_env : std::max(1, cpw_fit)));
+      const int cpb = NW * cpw;
+      const uint32_t nq = qe - qb;
+      const int groups =
+          (int)std::min<size_t>(8, std::max<size_t>(1, nq / ((size_t)cpb * 148 * 4)));
+      const unsigned grid = (unsigned)((nq + (size_t)cpb * groups - 1) / ((size_t)cpb * groups));
+      const size_t sm = 2 * (size_t)cpb * Pn * sizeof(double2);
+      auto launch = [&](auto kern) {
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+        kern<<<grid, kRowThreads, sm, s>>>(U.dev(), L.dev(), K, tiles_dev(T), P->kappa, qb, qe,
+                                          cpw, groups, child, parent, P->err);
+      };
+      const bool lap = P->kappa == 0.0;
+      if (T.row_nodes == 2)
+        lap ? launch(k_propagate_rows<PS, PT, PP, true, 2>)
+            : launch(k_propagate_rows<PS, PT, PP, false, 2>);
+      else
+        lap ? launch(k_propagate_rows<PS, PT, PP, true, 3>)
+            : launch(k_propagate_rows<PS, PT, PP, false, 3>);
+      ++P->launches;
+    });
+  }
   if (P->prop_kernel == IFGF_PROP_TILES || !full) {  // per node from the tiles (any range)
     const Level& U = P->lv[d - 1];
     const Level& L = P->lv[d];

@@ -421,17 +421,17 @@ void build_plan(ifgf_plan* P, const double* d_x, const double* d_y, const double
   P->depth = D;
   {
     // angle seed table for the fast locate (ifgf_common.cuh fast_angles)
-    std::vector<double4> trig(kTrigPhi + kTrigTheta + 1);
+    std::vector<double2> trig(kTrigEntries);
     for (int k = 0; k < kTrigPhi; ++k) {
-      const double a = k * (2.0 * kPi / kTrigPhi);
-      trig[k] = make_double4(std::cos(a), std::sin(a), a, 0.0);
+      const double a = (double)k * kTrigHPhi;  // same rounded product as fast_angles
+      trig[k] = make_double2(std::cos(a), std::sin(a));
     }
     for (int k = 0; k <= kTrigTheta; ++k) {
-      const double a = k * (kPi / kTrigTheta);
-      trig[kTrigPhi + k] = make_double4(std::cos(a), std::sin(a), a, 0.0);
+      const double a = (double)k * kTrigHTheta;
+      trig[kTrigPhi + k] = make_double2(std::cos(a), std::sin(a));
     }
-    double4* d_trig = P->alloc<double4>(trig.size());
-    IFGF_CUDA(cudaMemcpyAsync(d_trig, trig.data(), trig.size() * sizeof(double4),
+    double2* d_trig = P->alloc<double2>(trig.size());
+    IFGF_CUDA(cudaMemcpyAsync(d_trig, trig.data(), trig.size() * sizeof(double2),
                               cudaMemcpyHostToDevice, s));
     for (int d = 0; d < IFGF_MAX_LEVELS; ++d) P->lv[d].trig = d_trig;
     IFGF_CUDA(cudaStreamSynchronize(s));  // trig lives on the stack until copied

@@ -144,13 +144,14 @@ def test_direct_eval(built, gpu, oracle):
 
 
 def test_propagation_kernels_agree(built):
-    """The three K3 implementations (per-node locate, precomputed tiles, FP64
-    DMMA batched GEMM) compute the same operator up to rounding."""
+    """The K3 implementations (per-node locate, precomputed tiles, FP64 DMMA
+    batched GEMM, register-blocked node rows) compute the same operator up to
+    rounding."""
     case, pc, cfg, ep, op, plan, prob = built
     res = []
-    for kind in (plan.PROP_NODE, plan.PROP_TILES, plan.PROP_DMMA):
+    for kind in (plan.PROP_NODE, plan.PROP_TILES, plan.PROP_DMMA, plan.PROP_ROWS):
         plan.set_prop_kernel(kind)
         res.append(plan.apply(pc.a_re, pc.a_im)[:2])
-    plan.set_prop_kernel(plan.PROP_NODE)
+    plan.set_prop_kernel(plan.PROP_ROWS)
     for r in res[1:]:
         assert rel_l2(r[0], r[1], res[0][0], res[0][1]) <= 1e-13

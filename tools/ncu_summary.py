@@ -52,9 +52,11 @@ def main(rep, out_prefix):
                 v = to_num(r[col[m]])
                 u = units[col[m]]
                 if k == "duration_us" and v is not None:
-                    v = v / 1e3 if u == "nsecond" else (v * 1e3 if u == "msecond" else v)
+                    v = v * {"ns": 1e-3, "nsecond": 1e-3, "ms": 1e3, "msecond": 1e3,
+                             "s": 1e6, "second": 1e6}.get(u, 1.0)
                 if k.startswith("dram_") and v is not None:
-                    scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}.get(u, 1)
+                    scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9,
+                             "KB": 1e3, "MB": 1e6, "GB": 1e9}.get(u, 1)
                     v = v * scale
                 rec[k] = v
         for s in STALLS:
