@@ -287,7 +287,7 @@ def run_ours(args):
     traffic = None
     summ = os.path.join(ROOT, "profiles", "ncu_summary.json")
     kernel_prefix = {"near": "k_singular", "level_d": "k_level_d",
-                     "interpolation": "k_interp", "propagation": "k_propagate"}[dom]
+                     "interpolation": "k_interp", "propagation": "k_propagate_rows"}[dom]
     if os.path.exists(summ):
         try:
             tb = json.load(open(summ)).get("traffic_bytes_per_launch", {})

@@ -45,8 +45,10 @@ inline unsigned blocks_for(size_t n, int t) { return (unsigned)((n + t - 1) / t)
 #define IFGF_PROP_MINB 2
 #endif
 #ifndef IFGF_INTERP_MINB
-#define IFGF_INTERP_MINB 4
+#define IFGF_INTERP_MINB 3
 #endif
+
+
 
 // ---------------------------------------------------------------- K1 near field
 template <bool LAP>
@@ -207,51 +209,103 @@ __global__ void __launch_bounds__(320, IFGF_PROP_MINB)
 }
 
 // ---------------------------------------------------------- K4 interpolation
-template <int PS, int PT, int PP, bool LAP>
+// Thread = one run of <= R consecutive (Morton-sorted) points of one box
+// (Level::chunk), clipped to [b0, e0).  They share the cousin list, and per
+// cousin they nearly always fall into the same cone: that block is loaded once
+// and evaluated at all R points (eval_block_multi), which takes the evaluation
+// off the L1->register bandwidth limit.  Points that land in another cone of
+// the cousin are evaluated singly.  Per point, cousins are summed in list
+// order.
+template <int PS, int PT, int PP, bool LAP, int R>
 __global__ void __launch_bounds__(128, IFGF_INTERP_MINB)
-    k_interp(const __grid_constant__ LevelDev L, const uint32_t* __restrict__ ptbox, const double* __restrict__ xs,
+    k_interp(const __grid_constant__ LevelDev L, const uint2* __restrict__ chunk,
+             const uint32_t* __restrict__ nchunk, const double* __restrict__ xs,
              const double* __restrict__ ys, const double* __restrict__ zs, double kappa,
              size_t b0, size_t e0, const double2* __restrict__ blocks, double* ir, double* ii,
              int* err) {
-  constexpr int P = PS * PT * PP;
+  using BL = BlockLayout<PS, PT, PP>;
   __shared__ double2 trig[kTrigEntries];
   stage_trig(trig, L.trig);
   __syncthreads();
-  const size_t i = b0 + blockIdx.x * (size_t)blockDim.x + threadIdx.x;
-  if (i >= e0) return;
-  const uint32_t b = ptbox[i];
-  const double x = xs[i], y = ys[i], z = zs[i];
-  double acr = 0.0, aci = 0.0;
+  const size_t t = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
+  if (t >= *nchunk) return;
+  const uint2 ch = chunk[t];
+  const uint32_t b = ch.y;
+  const size_t lo = max((size_t)ch.x, b0);
+  const size_t hi = min(min((size_t)ch.x + R, (size_t)L.first[b] + L.count[b]), e0);
+  if (lo >= hi) return;
+  const size_t i0 = lo;
+  const int n = (int)(hi - lo);
+  double px[R], py[R], pz[R], acr[R], aci[R];
+#pragma unroll
+  for (int j = 0; j < R; ++j) {
+    const size_t i = i0 + (j < n ? j : 0);
+    px[j] = xs[i];
+    py[j] = ys[i];
+    pz[j] = zs[i];
+    acr[j] = aci[j] = 0.0;
+  }
   const uint32_t k0 = L.cous_off[b], k1 = L.cous_off[b + 1];
   for (uint32_t k = k0; k < k1; ++k) {
     const uint32_t cb = L.cous[k];
-    Loc o;
-    const int e = locate_fast(L, trig, L.cx[cb], L.cy[cb], L.cz[cb], x, y, z, o);
+    const double cx = L.cx[cb], cy = L.cy[cb], cz = L.cz[cb];
+    Loc o[R];
+    int e = 0;
+#pragma unroll
+    for (int j = 0; j < R; ++j) {
+      const int ej = locate_fast(L, trig, cx, cy, cz, px[j], py[j], pz[j], o[j]);
+      e = e ? e : ej;
+    }
     if (e) {
       raise_err(err, e);
       return;
     }
-    const uint32_t q = find_cone(L, cb, o.gamma);
+    const uint32_t q = find_cone(L, cb, o[0].gamma);
     if (q == 0xffffffffu) {
       raise_err(err, kErrInterpCover);
       return;
     }
-    double vr, vi;
-    eval_block<PS, PT, PP>(blocks + (size_t)q * BlockLayout<PS, PT, PP>::Pst, o.ts, o.tt, o.tp, vr, vi);
-    const double inv = kQuarterInvPi * o.rinv;
-    if (LAP) {
-      acr = fma(vr, inv, acr);
-      aci = fma(vi, inv, aci);
-    } else {
-      double sn, cn;
-      sincos_fast(kappa * o.r, sn, cn);
-      const double gr = cn * inv, gi = sn * inv;
-      acr = fma(vr, gr, fma(-vi, gi, acr));
-      aci = fma(vr, gi, fma(vi, gr, aci));
+    double ts[R], tt[R], tp[R], vr[R], vi[R];
+#pragma unroll
+    for (int j = 0; j < R; ++j) {
+      ts[j] = o[j].ts;
+      tt[j] = o[j].tt;
+      tp[j] = o[j].tp;
+    }
+    eval_block_multi<PS, PT, PP, R>(blocks + (size_t)q * BL::Pst, ts, tt, tp, vr, vi);
+#pragma unroll
+    for (int j = 1; j < R; ++j) {
+      if (j < n && o[j].gamma != o[0].gamma) {  // another cone of this cousin
+        const uint32_t qj = find_cone(L, cb, o[j].gamma);
+        if (qj == 0xffffffffu) {
+          raise_err(err, kErrInterpCover);
+          return;
+        }
+        eval_block<PS, PT, PP>(blocks + (size_t)qj * BL::Pst, o[j].ts, o[j].tt, o[j].tp, vr[j],
+                               vi[j]);
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < R; ++j) {
+      const double inv = kQuarterInvPi * o[j].rinv;
+      if (LAP) {
+        acr[j] = fma(vr[j], inv, acr[j]);
+        aci[j] = fma(vi[j], inv, aci[j]);
+      } else {
+        double sn, cn;
+        sincos_fast(kappa * o[j].r, sn, cn);
+        const double gr = cn * inv, gi = sn * inv;
+        acr[j] = fma(vr[j], gr, fma(-vi[j], gi, acr[j]));
+        aci[j] = fma(vr[j], gi, fma(vi[j], gr, aci[j]));
+      }
     }
   }
-  ir[i] += acr;
-  ii[i] += aci;
+#pragma unroll
+  for (int j = 0; j < R; ++j)
+    if (j < n) {
+      ir[i0 + j] += acr[j];
+      ii[i0 + j] += aci[j];
+    }
 }
 
 // --------------------------------------------------------------- K6 permutes
@@ -379,15 +433,14 @@ void launch_interpolation(ifgf_plan* P, int d, size_t b, size_t e, const double2
   if (e <= b) return;
   const Level& L = P->lv[d];
   const InterpConsts& K = P->K;
-  const unsigned g = blocks_for(e - b, 128);
   dispatch_orders(K.ps, K.pt, K.pp, [&](auto o) {
     using O = decltype(o);
-    if (P->kappa == 0.0)
-      k_interp<O::PS, O::PT, O::PP, true><<<g, 128, 0, s>>>(
-          L.dev(), L.ptbox, P->xs, P->ys, P->zs, P->kappa, b, e, blocks, P->ir, P->ii, P->err);
-    else
-      k_interp<O::PS, O::PT, O::PP, false><<<g, 128, 0, s>>>(
-          L.dev(), L.ptbox, P->xs, P->ys, P->zs, P->kappa, b, e, blocks, P->ir, P->ii, P->err);
+    constexpr int R = interp_points(O::P);
+    const unsigned g = blocks_for(L.chunk_cap, 128);
+    auto kern = P->kappa == 0.0 ? k_interp<O::PS, O::PT, O::PP, true, R>
+                                : k_interp<O::PS, O::PT, O::PP, false, R>;
+    kern<<<g, 128, 0, s>>>(L.dev(), L.chunk, L.nchunk, P->xs, P->ys, P->zs, P->kappa, b, e,
+                           blocks, P->ir, P->ii, P->err);
   });
   ++P->launches;
 }

@@ -46,6 +46,10 @@ struct Level {
   size_t n_cous = 0;
   size_t n_nbr = 0;
   uint32_t* ptbox = nullptr;  // box ordinal of every sorted point at this level
+  // K4 work items: runs of <= interp_points(P) points of one box, {first point, box}
+  uint2* chunk = nullptr;
+  const uint32_t* nchunk = nullptr;  // device count
+  size_t chunk_cap = 0;              // upper bound n / R + nb (launch size)
   // cone set
   int n0 = 0, n1 = 0, n2 = 0;
   double w0 = 0, w1 = 0, w2 = 0, iw0 = 0, iw1 = 0, iw2 = 0, rad = 0;
@@ -105,6 +109,14 @@ struct Level {
 // node) are computed once per plan.  Entries within kIdxMargin of a segment
 // boundary are flagged and recomputed per box exactly (the reference's
 // absolute-coordinate rounding could move them).
+// Points per K4 thread (register blocking of the interpolant evaluation;
+// C2: R = 1 23.2 ms, 2 21.5 ms, 3 24.2 ms -- K4 is load-latency bound, and
+// the extra registers of R = 3 cost more occupancy than the loads it saves).
+#ifndef IFGF_INTERP_R
+#define IFGF_INTERP_R 2
+#endif
+constexpr int interp_points(int P) { return P <= 100 ? IFGF_INTERP_R : 2; }
+
 struct PropTiles {
   bool enabled = false;
   uint32_t ngamma = 0;          // distinct parent gammas in use

@@ -236,6 +236,21 @@ __global__ void k_neighbors(uint32_t nb, int d, const uint64_t* __restrict__ cod
 
 // Cousins: children of parent-neighbours at Chebyshev distance > 1, visited in
 // Morton order (octree.cpp:127-147).  fill == nullptr: count only.
+// K4 work items: box b -> ceil(count / R) runs of <= R points.
+__global__ void k_chunk_count(const uint32_t* __restrict__ count, uint32_t nb, int R,
+                              uint32_t* c) {
+  const uint32_t b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b < nb) c[b] = (count[b] + R - 1) / R;
+}
+
+__global__ void k_chunk_fill(const uint32_t* __restrict__ first, const uint32_t* __restrict__ count,
+                             uint32_t nb, int R, const uint32_t* __restrict__ off, uint2* chunk) {
+  const uint32_t b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= nb) return;
+  const uint32_t f = first[b], m = (count[b] + R - 1) / R;
+  for (uint32_t k = 0; k < m; ++k) chunk[off[b] + k] = make_uint2(f + k * R, b);
+}
+
 __global__ void k_cousins(const __grid_constant__ LevelDev L, const __grid_constant__ LevelDev U, uint32_t* cnt_or_off, uint32_t* fill) {
   const uint32_t b = blockIdx.x * blockDim.x + threadIdx.x;
   if (b >= L.nb) return;
@@ -531,6 +546,25 @@ void build_plan(ifgf_plan* P, const double* d_x, const double* d_y, const double
         cub::DeviceScan::ExclusiveSum(scratch.get(tb), tb, cnt, L.cous_off, (int)(L.nb + 1), s));
     IFGF_CUDA(cudaMemcpyAsync(&cous_total[d], L.cous_off + L.nb, sizeof(uint32_t),
                               cudaMemcpyDeviceToHost, s));
+  }
+  // K4 work items per level
+  {
+    const int R = interp_points(P->K.P);
+    for (int d = 3; d <= D; ++d) {
+      Level& L = P->lv[d];
+      uint32_t* cnt = P->alloc<uint32_t>(L.nb + 1);
+      uint32_t* off = P->alloc<uint32_t>(L.nb + 1);
+      IFGF_CUDA(cudaMemsetAsync(cnt + L.nb, 0, sizeof(uint32_t), s));
+      k_chunk_count<<<grid_for(L.nb), kT, 0, s>>>(L.count, L.nb, R, cnt);
+      size_t tb = 0;
+      cub::DeviceScan::ExclusiveSum(nullptr, tb, cnt, off, (int)(L.nb + 1), s);
+      IFGF_CUDA(cub::DeviceScan::ExclusiveSum(scratch.get(tb), tb, cnt, off, (int)(L.nb + 1), s));
+      L.chunk_cap = (n + R - 1) / R + L.nb;
+      L.chunk = P->alloc<uint2>(L.chunk_cap);
+      L.nchunk = off + L.nb;
+      k_chunk_fill<<<grid_for(L.nb), kT, 0, s>>>(L.first, L.count, L.nb, R, off, L.chunk);
+      P->launches += 3;
+    }
   }
   IFGF_CUDA(cudaStreamSynchronize(s));
   for (int d = 3; d <= D; ++d) {
