@@ -103,12 +103,21 @@ void ifgf_plan_destroy(ifgf_plan* plan);
  *   IFGF_PROP_DMMA  (2) FP64 tensor-core batched GEMM over cones sharing gamma;
  *   IFGF_PROP_ROWS  (3, default) thread per (parent cone, child, row of <= 3
  *                       nodes that share a child cone) from the precomputed
- *                       geometry, one block load per row.
+ *                       geometry, one block load per row; levels without
+ *                       the precomputed geometry run IFGF_PROP_FLY;
+ *   IFGF_PROP_FLY   (4) the same rows grouped per parent cone on the fly
+ *                       (no precomputed geometry).
  *   Where the precomputed geometry is not built (too few parent cones per
- *   gamma, P > 255) every setting runs IFGF_PROP_NODE.
+ *   gamma, P > 255) TILES and DMMA run IFGF_PROP_NODE.
  *   All agree to rounding; DESIGN.md records their measured times. */
 enum { IFGF_OPT_SERIAL = 1, IFGF_OPT_PROP_KERNEL = 2 };
-enum { IFGF_PROP_NODE = 0, IFGF_PROP_TILES = 1, IFGF_PROP_DMMA = 2, IFGF_PROP_ROWS = 3 };
+enum {
+  IFGF_PROP_NODE = 0,
+  IFGF_PROP_TILES = 1,
+  IFGF_PROP_DMMA = 2,
+  IFGF_PROP_ROWS = 3,
+  IFGF_PROP_FLY = 4
+};
 int ifgf_plan_set_option(ifgf_plan* plan, int option, int value);
 
 /* ---- operator application; i_* in the caller's original point order ---- */

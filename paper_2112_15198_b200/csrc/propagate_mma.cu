@@ -88,7 +88,9 @@ __global__ void k_gamma_mark(const __grid_constant__ LevelDev U, uint64_t* gbits
   const uint32_t q = blockIdx.x * blockDim.x + threadIdx.x;
   if (q >= U.nc) return;
   const uint32_t g = U.cone_gamma[q];
-  atomicOr((unsigned long long*)&gbits[g >> 6], 1ull << (g & 63));
+  const uint64_t m = 1ull << (g & 63);
+  // most cones of a level share few gammas: test before the atomic
+  if (!(gbits[g >> 6] & m)) atomicOr((unsigned long long*)&gbits[g >> 6], m);
 }
 
 __global__ void k_gamma_popc(const uint64_t* gbits, size_t nw, uint32_t* cnt) {
@@ -835,6 +837,159 @@ __global__ void __launch_bounds__(kRowThreads, IFGF_ROWS_MINB)
   }
 }
 
+// K3 rows without precomputed tiles (levels whose parent cones mostly have
+// distinct gammas, where tiles would cost more than they save): warp = one
+// parent cone at a time.  Per child box the warp locates all P nodes
+// (locate_fast, exact fallback near boundaries -- the reference's cone per
+// node), groups them by child cone in node order (warp min-reduction +
+// ballots) into rows of <= R, and evaluates each row with one block load
+// (eval_block_multi).  Children in Morton order, one contribution per node
+// and child: deterministic sums.  Then fit_cones_warp on the cone.
+template <int P>
+struct FlyWarp {
+  double2 sv[P], st[P];
+  double nx[P], ny[P], nz[P], nrp[P];      // node positions, distance to parent centre
+  double ts[P], tt[P], tp[P], tr[P], ti[P];  // per node for the current child
+  uint32_t key[P];                         // child gamma (kNone: error)
+  uint32_t rkey[P];                        // per row: child gamma
+  uint8_t rcnt[P];
+  uint8_t rnode[P][4];
+};
+
+template <int PS, int PT, int PP, bool LAP, int R>
+__global__ void __launch_bounds__(kRowThreads, IFGF_ROWS_MINB)
+    k_propagate_fly(const __grid_constant__ LevelDev U, const __grid_constant__ LevelDev L,
+                    const __grid_constant__ InterpConsts K, double kappa, uint32_t qb,
+                    uint32_t qe, const double2* __restrict__ child, double2* parent, int* err) {
+  using BL = BlockLayout<PS, PT, PP>;
+  constexpr int P = PS * PT * PP;
+  static_assert(R <= 4, "rows hold <= 4 nodes");
+  const int NW = blockDim.x >> 5;
+  extern __shared__ __align__(16) unsigned char fly_smem[];
+  __shared__ double2 trig[kTrigEntries];
+  __shared__ double sM[PP * PP + PT * PT + PS * PS];
+  stage_trig(trig, L.trig);
+  stage_fit_matrices<PS, PT, PP>(K, sM);
+  __syncthreads();
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  FlyWarp<P>& F = reinterpret_cast<FlyWarp<P>*>(fly_smem)[w];
+  const uint32_t nwarps = gridDim.x * NW;
+  for (uint32_t q = qb + blockIdx.x * NW + w; q < qe; q += nwarps) {
+    const uint32_t pb = U.cone_box[q];
+    const SegMid sg = segment_mid(U, U.cone_gamma[q]);
+    const double pcx = U.cx[pb], pcy = U.cy[pb], pcz = U.cz[pb];
+    for (int m = lane; m < P; m += 32) {
+      const int jp = m % PP, jt = (m / PP) % PT, js = m / (PP * PT);
+      double x, y, z;
+      node_position(sg, U.rad, pcx, pcy, pcz, K.ns[js], K.nt[jt], K.np[jp], x, y, z);
+      const double ux = x - pcx, uy = y - pcy, uz = z - pcz;
+      F.nx[m] = x;
+      F.ny[m] = y;
+      F.nz[m] = z;
+      F.nrp[m] = sqrt(fma(uz, uz, fma(uy, uy, ux * ux)));
+      F.sv[m] = make_double2(0.0, 0.0);
+    }
+    __syncwarp();
+    for (uint32_t cb = U.child_begin[pb]; cb < U.child_begin[pb + 1]; ++cb) {
+      const double cx = L.cx[cb], cy = L.cy[cb], cz = L.cz[cb];
+      // a. locate every node in the child box
+      for (int m = lane; m < P; m += 32) {
+        Loc o;
+        const int e = locate_fast(L, trig, cx, cy, cz, F.nx[m], F.ny[m], F.nz[m], o);
+        if (e) {
+          raise_err(err, e);
+          F.key[m] = kNone;
+          continue;
+        }
+        F.key[m] = o.gamma;
+        F.ts[m] = o.ts;
+        F.tt[m] = o.tt;
+        F.tp[m] = o.tp;
+        const double rp = F.nrp[m], ratio = rp * o.rinv;
+        double sn = 0.0, cn = 1.0;
+        if (!LAP) sincos_fast(kappa * (o.r - rp), sn, cn);
+        F.tr[m] = ratio * cn;
+        F.ti[m] = ratio * sn;
+      }
+      __syncwarp();
+      // b. rows: nodes grouped by child gamma (ascending), node order within
+      constexpr int NS = (P + 31) / 32;
+      uint32_t k[NS];
+      bool done[NS];
+#pragma unroll
+      for (int sl = 0; sl < NS; ++sl) {
+        const int m = lane + 32 * sl;
+        k[sl] = m < P ? F.key[m] : kNone;
+        done[sl] = k[sl] == kNone;
+      }
+      int nrows = 0;
+      for (;;) {
+        uint32_t mn = kNone;
+#pragma unroll
+        for (int sl = 0; sl < NS; ++sl)
+          if (!done[sl]) mn = min(mn, k[sl]);
+        mn = __reduce_min_sync(0xffffffffu, mn);
+        if (mn == kNone) break;
+        int below = 0, total = 0;
+        const uint32_t lt = (1u << lane) - 1u;
+#pragma unroll
+        for (int sl = 0; sl < NS; ++sl) {
+          const bool mine = !done[sl] && k[sl] == mn;
+          const uint32_t bal = __ballot_sync(0xffffffffu, mine);
+          if (mine) {
+            const int rank = total + __popc(bal & lt);
+            const int row = nrows + rank / R;
+            F.rnode[row][rank % R] = (uint8_t)(lane + 32 * sl);
+            done[sl] = true;
+          }
+          total += __popc(bal);
+        }
+        const int nr = (total + R - 1) / R;
+        for (int r = lane; r < nr; r += 32) {
+          F.rkey[nrows + r] = mn;
+          F.rcnt[nrows + r] = (uint8_t)min(R, total - r * R);
+        }
+        nrows += nr;
+      }
+      __syncwarp();
+      // c. one block load per row
+      for (int r = lane; r < nrows; r += 32) {
+        const uint32_t cq = find_cone(L, cb, F.rkey[r]);
+        if (cq == kNone) {
+          raise_err(err, kErrPropCover);
+          continue;
+        }
+        const int cnt = F.rcnt[r];
+        double ts[R], tt[R], tp[R];
+        int nd[R];
+#pragma unroll
+        for (int j = 0; j < R; ++j) {
+          nd[j] = j < cnt ? F.rnode[r][j] : 0;
+          ts[j] = j < cnt ? F.ts[nd[j]] : 0.0;
+          tt[j] = j < cnt ? F.tt[nd[j]] : 0.0;
+          tp[j] = j < cnt ? F.tp[nd[j]] : 0.0;
+        }
+        double vr[R], vi[R];
+        eval_block_multi<PS, PT, PP, R>(child + (size_t)cq * BL::Pst, ts, tt, tp, vr, vi);
+#pragma unroll
+        for (int j = 0; j < R; ++j) {
+          if (j < cnt) {
+            const int m = nd[j];
+            const double tr = F.tr[m], ti = F.ti[m];
+            double2 v = F.sv[m];
+            v.x = fma(vr[j], tr, fma(-vi[j], ti, v.x));
+            v.y = fma(vr[j], ti, fma(vi[j], tr, v.y));
+            F.sv[m] = v;
+          }
+        }
+      }
+      __syncwarp();
+    }
+    fit_cones_warp<PS, PT, PP>(sM, F.sv, F.st, 1, parent + (size_t)q * BL::Pst, err);
+    __syncwarp();
+  }
+}
+
 template <class F>
 bool dispatch_mma_orders(int ps, int pt, int pp, F&& f) {
 #define IFGF_MMA_CASE(a, b, c)          \
@@ -907,7 +1062,11 @@ void build_prop_tiles(ifgf_plan* P, int d, void* (*scratch)(void*, size_t), void
   // worth it only if a (gamma, octant) tile serves several parent cones
   const double uses = (double)U.nc / ng;
   P->launches += 2;
-  if (uses < 3.0) return;
+  static const double min_uses = [] {
+    const char* v = std::getenv("IFGF_TILE_MIN_USES");
+    return v ? std::atof(v) : 3.0;
+  }();
+  if (uses < min_uses) return;
   T.ngamma = ng;
   T.cone_gidx = P->alloc<uint32_t>(U.nc);
   T.gamma_of = P->alloc<uint32_t>(ng);
@@ -1013,9 +1172,41 @@ void launch_mark_nodes_tiles(ifgf_plan* P, int d, uint64_t* bits) {
   ++P->launches;
 }
 
+bool launch_propagation_fly(ifgf_plan* P, int d, uint32_t qb, uint32_t qe, const double2* child,
+                            double2* parent, cudaStream_t s) {
+  const Level& U = P->lv[d - 1];
+  const Level& L = P->lv[d];
+  const InterpConsts& K = P->K;
+  if (K.P > 255) return false;
+  return dispatch_rows_orders(K.ps, K.pt, K.pp, [&](auto A, auto B, auto C) {
+    constexpr int PS = decltype(A)::value, PT = decltype(B)::value, PP = decltype(C)::value;
+    constexpr int Pn = PS * PT * PP;
+    // warps per CTA: kRowThreads / 32, fewer when the per-warp scratch
+    // would exceed ~200 KB of shared memory (large orders)
+    const int NW = (int)std::max<size_t>(
+        1, std::min<size_t>(kRowThreads / 32, 200 * 1024 / sizeof(FlyWarp<Pn>)));
+    const size_t sm = NW * sizeof(FlyWarp<Pn>);
+    const uint32_t nq = qe - qb;
+    const unsigned grid = (unsigned)std::max<size_t>(
+        1, std::min<size_t>((nq + NW - 1) / NW, (size_t)148 * 8));
+    auto launch = [&](auto kern) {
+      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+      kern<<<grid, NW * 32, sm, s>>>(U.dev(), L.dev(), K, P->kappa, qb, qe, child, parent,
+                                     P->err);
+    };
+    const bool lap = P->kappa == 0.0;
+    constexpr int R = Pn <= 100 ? 3 : 2;
+    lap ? launch(k_propagate_fly<PS, PT, PP, true, R>)
+        : launch(k_propagate_fly<PS, PT, PP, false, R>);
+    ++P->launches;
+  });
+}
+
 bool launch_propagation_mma(ifgf_plan* P, int d, uint32_t qb, uint32_t qe, const double2* child,
                             double2* parent, cudaStream_t s) {
   const PropTiles& T = P->tiles[d];
+  if (P->prop_kernel == IFGF_PROP_FLY || (P->prop_kernel == IFGF_PROP_ROWS && !T.enabled))
+    return launch_propagation_fly(P, d, qb, qe, child, parent, s);
   if (!T.enabled || T.nchunks == 0) return false;
   const bool full = qb == 0 && qe == P->lv[d - 1].nc;
   if (P->prop_kernel == IFGF_PROP_ROWS) {

@@ -21,6 +21,8 @@
 
 #include <algorithm>
 #include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <cmath>
 #include <vector>
 
@@ -243,12 +245,18 @@ __global__ void k_chunk_count(const uint32_t* __restrict__ count, uint32_t nb, i
   if (b < nb) c[b] = (count[b] + R - 1) / R;
 }
 
-__global__ void k_chunk_fill(const uint32_t* __restrict__ first, const uint32_t* __restrict__ count,
-                             uint32_t nb, int R, const uint32_t* __restrict__ off, uint2* chunk) {
-  const uint32_t b = blockIdx.x * blockDim.x + threadIdx.x;
-  if (b >= nb) return;
-  const uint32_t f = first[b], m = (count[b] + R - 1) / R;
-  for (uint32_t k = 0; k < m; ++k) chunk[off[b] + k] = make_uint2(f + k * R, b);
+// One thread per work item: its box is the last b with off[b] <= t.
+__global__ void k_chunk_fill(const uint32_t* __restrict__ first, uint32_t nb, int R,
+                             const uint32_t* __restrict__ off, size_t cap, uint2* chunk) {
+  const size_t t = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
+  if (t >= cap || t >= off[nb]) return;
+  uint32_t lo = 0, hi = nb;  // off[lo] <= t < off[hi]
+  while (hi - lo > 1) {
+    const uint32_t mid = (lo + hi) >> 1;
+    if (off[mid] <= t) lo = mid;
+    else hi = mid;
+  }
+  chunk[t] = make_uint2(first[lo] + (uint32_t)(t - off[lo]) * R, lo);
 }
 
 __global__ void k_cousins(const __grid_constant__ LevelDev L, const __grid_constant__ LevelDev U, uint32_t* cnt_or_off, uint32_t* fill) {
@@ -291,6 +299,9 @@ __device__ __forceinline__ void set_bit(uint64_t* bits, uint64_t idx) {
 __global__ void k_mark_points(const __grid_constant__ LevelDev L, const uint32_t* __restrict__ ptbox,
                               const double* __restrict__ xs, const double* __restrict__ ys,
                               const double* __restrict__ zs, size_t n, uint64_t* bits, int* err) {
+  __shared__ double2 trig[kTrigEntries];
+  stage_trig(trig, L.trig);
+  __syncthreads();
   const size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
   if (i >= n) return;
   const uint32_t b = ptbox[i];
@@ -298,7 +309,7 @@ __global__ void k_mark_points(const __grid_constant__ LevelDev L, const uint32_t
   for (uint32_t ci = L.cous_off[b]; ci < L.cous_off[b + 1]; ++ci) {
     const uint32_t cb = L.cous[ci];
     uint32_t g;
-    const int e = cone_of_point_fast(L, L.cx[cb], L.cy[cb], L.cz[cb], x, y, z, g);
+    const int e = cone_of_point_fast(L, trig, L.cx[cb], L.cy[cb], L.cz[cb], x, y, z, g);
     if (e) {
       raise_err(err, e);
       return;
@@ -311,6 +322,9 @@ __global__ void k_mark_points(const __grid_constant__ LevelDev L, const uint32_t
 // mark the containing segment of each child box.
 __global__ void k_mark_nodes(const __grid_constant__ LevelDev L, const __grid_constant__ LevelDev U,
                              const __grid_constant__ InterpConsts K, uint64_t* bits, int* err) {
+  __shared__ double2 trig[kTrigEntries];
+  stage_trig(trig, L.trig);
+  __syncthreads();
   const size_t t = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
   if (t >= (size_t)U.nc * K.P) return;
   const uint32_t q = (uint32_t)(t / K.P);
@@ -322,7 +336,7 @@ __global__ void k_mark_nodes(const __grid_constant__ LevelDev L, const __grid_co
   node_position(sm, U.rad, U.cx[pb], U.cy[pb], U.cz[pb], K.ns[js], K.nt[jt], K.np[jp], x, y, z);
   for (uint32_t cb = U.child_begin[pb]; cb < U.child_begin[pb + 1]; ++cb) {
     uint32_t g;
-    const int e = cone_of_point_fast(L, L.cx[cb], L.cy[cb], L.cz[cb], x, y, z, g);
+    const int e = cone_of_point_fast(L, trig, L.cx[cb], L.cy[cb], L.cz[cb], x, y, z, g);
     if (e) {
       raise_err(err, e);
       return;
@@ -410,6 +424,14 @@ void build_plan(ifgf_plan* P, const double* d_x, const double* d_y, const double
   cudaStream_t s = P->s_main;
   const size_t n = P->n;
   Scratch scratch{P};
+  // IFGF_SETUP_TRACE=1: synchronise and print the elapsed time at each phase
+  static const bool trace = std::getenv("IFGF_SETUP_TRACE") != nullptr;
+  auto mark = [&](const char* what) {
+    if (!trace) return;
+    cudaStreamSynchronize(s);
+    std::fprintf(stderr, "[setup] %-28s %8.3f ms\n", what,
+                 std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count() * 1e3);
+  };
 
   // -- bounding cube (geometry.cpp:95-114)
   const int nparts = 296;
@@ -427,6 +449,7 @@ void build_plan(ifgf_plan* P, const double* d_x, const double* d_y, const double
   P->cube[3] = side;
   for (int c = 0; c < 3; ++c) P->cube[c] = 0.5 * (bb[c] + bb[3 + c]) - 0.5 * side;
 
+  mark("bounding cube");
   // -- depth (engine.cpp:55-72)
   int D = 0;
   {
@@ -460,6 +483,7 @@ void build_plan(ifgf_plan* P, const double* d_x, const double* d_y, const double
                                    " needs cone indices beyond 32 bits (unsupported)");
   }
 
+  mark("trig table");
   // -- Morton codes + stable sort (morton.cpp:70-95)
   const uint32_t ngrid = 1u << (D - 1);
   const double hD = side / static_cast<double>(ngrid);
@@ -483,6 +507,7 @@ void build_plan(ifgf_plan* P, const double* d_x, const double* d_y, const double
   k_gather3<<<grid_for(n), kT, 0, s>>>(P->perm, d_x, d_y, d_z, n, P->xs, P->ys, P->zs);
   ++P->launches;
 
+  mark("morton sort");
   // -- octree levels (octree.cpp:18-94)
   uint8_t* start = P->alloc<uint8_t>(n);
   uint32_t* hist = P->alloc<uint32_t>(32);
@@ -562,7 +587,8 @@ void build_plan(ifgf_plan* P, const double* d_x, const double* d_y, const double
       L.chunk_cap = (n + R - 1) / R + L.nb;
       L.chunk = P->alloc<uint2>(L.chunk_cap);
       L.nchunk = off + L.nb;
-      k_chunk_fill<<<grid_for(L.nb), kT, 0, s>>>(L.first, L.count, L.nb, R, off, L.chunk);
+      k_chunk_fill<<<grid_for(L.chunk_cap), kT, 0, s>>>(L.first, L.nb, R, off, L.chunk_cap,
+                                                         L.chunk);
       P->launches += 3;
     }
   }
@@ -575,6 +601,7 @@ void build_plan(ifgf_plan* P, const double* d_x, const double* d_y, const double
     ++P->launches;
   }
 
+  mark("octree + cousins");
   // -- relevant cones, d = 3..D (cones.cpp:90-150)
   const ifgf_params& p = P->params;
   for (int d = 3; d <= D; ++d) {
@@ -598,9 +625,11 @@ void build_plan(ifgf_plan* P, const double* d_x, const double* d_y, const double
     k_mark_points<<<grid_for(n), kT, 0, s>>>(L.dev(), L.ptbox, P->xs, P->ys, P->zs, n, L.bits,
                                              P->err);
     ++P->launches;
+    mark("  mark points");
     if (d > 3 && P->lv[d - 1].nc > 0) {
       build_prop_tiles(
           P, d, [](void* ctx, size_t b) { return static_cast<Scratch*>(ctx)->get(b); }, &scratch);
+      mark("  tiles");
       if (P->tiles[d].enabled) {
         launch_mark_nodes_tiles(P, d, L.bits);
       } else {
@@ -610,6 +639,7 @@ void build_plan(ifgf_plan* P, const double* d_x, const double* d_y, const double
         ++P->launches;
       }
     }
+    mark("  mark nodes");
     uint32_t* cnt = P->alloc<uint32_t>(L.nwords + 1);
     k_popc<<<grid_for(L.nwords + 1), kT, 0, s>>>(L.bits, L.nwords, cnt);
     ++P->launches;
@@ -629,6 +659,7 @@ void build_plan(ifgf_plan* P, const double* d_x, const double* d_y, const double
     k_compact<<<grid_for(L.nwords), kT, 0, s>>>(L.dev(), L.nwords, L.cone_box, L.cone_gamma);
     k_box_cone<<<grid_for(L.nb + 1), kT, 0, s>>>(L.dev(), L.box_cone);
     P->launches += 2;
+    mark("  compact");
   }
   IFGF_CUDA(cudaStreamSynchronize(s));
   check_device_error(P);

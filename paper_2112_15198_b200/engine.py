@@ -286,11 +286,11 @@ class Plan:
         """Run all apply kernels on one stream (exclusive per-pass timings)."""
         check(lib.ifgf_plan_set_option(self._h, 1, 1 if on else 0))
 
-    PROP_NODE, PROP_TILES, PROP_DMMA, PROP_ROWS = 0, 1, 2, 3
+    PROP_NODE, PROP_TILES, PROP_DMMA, PROP_ROWS, PROP_FLY = 0, 1, 2, 3, 4
 
     def set_option(self, option: int, value: int):
         """IFGF_OPT_* (include/ifgf_b200.h): 1 serial streams, 2 propagation
-        kernel (PROP_NODE, PROP_TILES, PROP_DMMA, PROP_ROWS default)."""
+        kernel (PROP_NODE, PROP_TILES, PROP_DMMA, PROP_ROWS default, PROP_FLY)."""
         check(lib.ifgf_plan_set_option(self._h, option, value))
 
     def set_prop_kernel(self, kind: int):

@@ -145,11 +145,11 @@ def test_direct_eval(built, gpu, oracle):
 
 def test_propagation_kernels_agree(built):
     """The K3 implementations (per-node locate, precomputed tiles, FP64 DMMA
-    batched GEMM, register-blocked node rows) compute the same operator up to
-    rounding."""
+    batched GEMM, register-blocked node rows from the tiles and grouped on the
+    fly) compute the same operator up to rounding."""
     case, pc, cfg, ep, op, plan, prob = built
     res = []
-    for kind in (plan.PROP_NODE, plan.PROP_TILES, plan.PROP_DMMA, plan.PROP_ROWS):
+    for kind in (plan.PROP_NODE, plan.PROP_TILES, plan.PROP_DMMA, plan.PROP_ROWS, plan.PROP_FLY):
         plan.set_prop_kernel(kind)
         res.append(plan.apply(pc.a_re, pc.a_im)[:2])
     plan.set_prop_kernel(plan.PROP_ROWS)
