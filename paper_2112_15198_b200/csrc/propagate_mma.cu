@@ -49,6 +49,10 @@ constexpr uint32_t kFlag = 0x80000000u;
 #define IFGF_ROWS_MINB 1
 #endif
 constexpr int kRowThreads = IFGF_ROWS_THREADS;
+// L1 prefetch of the next task's child block (1) and row entries (2)
+#ifndef IFGF_ROWS_PF
+#define IFGF_ROWS_PF 1
+#endif
 constexpr int kRowMaxCpw = 16;  // parent cones per warp
 
 struct TilesDev {
@@ -215,46 +219,108 @@ __global__ void k_tile_rows(uint32_t ntiles, int P, const uint32_t* e_gc, uint32
   }
 }
 
-// One thread per tile: rows of <= rmax consecutive nodes of one child
-// gamma group, in e_perm order (flagged nodes, which e_perm lists last, are
-// not in any row).  Pass 1 (rw == nullptr) counts.
-__global__ void k_tile_rows_n(uint32_t ntiles, int P, int rmax, const uint32_t* e_gc,
-                              const uint8_t* e_perm, uint32_t* cnt, const uint32_t* off,
-                              uint2* rw) {
-  const uint32_t tile = blockIdx.x * blockDim.x + threadIdx.x;
+// Warp per tile: nodes ordered by raw e_gc (child gamma ascending, flagged
+// ones last), node order within a gamma -- ranks by all-pairs comparison in
+// registers (no serial scans).  Pass 1 counts rows of <= R nodes and flagged
+// nodes; pass 2 writes e_perm, the rows {gamma, position | count << 16 |
+// first-of-group << 24}, the flagged list (node order) and the row-ordered
+// entries.
+template <int NS>
+__global__ void __launch_bounds__(256)
+    k_tile_sort(uint32_t ntiles, int P, int R, const uint32_t* __restrict__ e_gc,
+                const double* __restrict__ e_t, const double2* __restrict__ e_T,
+                uint32_t* rw_cnt, uint32_t* fl_cnt, const uint32_t* __restrict__ rw_off,
+                const uint32_t* __restrict__ fl_off, uint2* rw, uint16_t* fl_node,
+                uint8_t* e_perm, PropTiles::Ent* ent) {
+  const uint32_t tile = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
   if (tile >= ntiles) return;
-  const uint32_t* g = e_gc + (size_t)tile * P;
-  const uint8_t* pm = e_perm + (size_t)tile * P;
-  uint32_t n = 0, w = rw ? off[tile] : 0;
-  int p = 0;
-  while (p < P) {
-    const uint32_t gc = g[pm[p]];
-    if (gc & kFlag) break;
-    int k = 1;
-    while (k < rmax && p + k < P && g[pm[p + k]] == gc) ++k;
-    if (rw) rw[w++] = make_uint2(gc, (uint32_t)p | ((uint32_t)k << 16));
-    ++n;
-    p += k;
+  const size_t base = (size_t)tile * P;
+  uint32_t key[NS];
+  int less[NS], eqb[NS], eqn[NS];
+#pragma unroll
+  for (int sl = 0; sl < NS; ++sl) {
+    const int m = lane + 32 * sl;
+    key[sl] = m < P ? e_gc[base + m] : 0xffffffffu;
+    less[sl] = eqb[sl] = eqn[sl] = 0;
   }
-  if (cnt) cnt[tile] = n;
-}
-
-// One thread per (tile, permuted position): entry data in row order.
-__global__ void k_tile_ent(size_t ne, int P, const uint8_t* e_perm, const double* e_t,
-                           const double2* e_T, PropTiles::Ent* ent) {
-  const size_t t = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
-  if (t >= ne) return;
-  const int m = e_perm[t];
-  const size_t e = (t / P) * P + m;
-  PropTiles::Ent x;
-  x.ts = e_t[3 * e];
-  x.tt = e_t[3 * e + 1];
-  x.tp = e_t[3 * e + 2];
-  x.tr = e_T[e].x;
-  x.ti = e_T[e].y;
-  x.node = (uint32_t)m;
-  x.pad = 0;
-  ent[t] = x;
+#pragma unroll
+  for (int s2 = 0; s2 < NS; ++s2)
+    for (int l2 = 0; l2 < 32; ++l2) {
+      const uint32_t kj = __shfl_sync(0xffffffffu, key[s2], l2);
+      const int j = 32 * s2 + l2;
+      if (j >= P) break;
+#pragma unroll
+      for (int sl = 0; sl < NS; ++sl) {
+        const int m = lane + 32 * sl;
+        less[sl] += kj < key[sl];
+        const bool eq = kj == key[sl];
+        eqn[sl] += eq;
+        eqb[sl] += eq && j < m;
+      }
+    }
+  // rows start at every R-th node of a gamma group
+  bool valid[NS], flag[NS], start[NS];
+  int nrows = 0, nflag = 0;
+#pragma unroll
+  for (int sl = 0; sl < NS; ++sl) {
+    valid[sl] = lane + 32 * sl < P;
+    flag[sl] = valid[sl] && (key[sl] & kFlag);
+    start[sl] = valid[sl] && !flag[sl] && eqb[sl] % R == 0;
+    nrows += __popc(__ballot_sync(0xffffffffu, start[sl]));
+    nflag += __popc(__ballot_sync(0xffffffffu, flag[sl]));
+  }
+  if (rw_cnt) {
+    if (lane == 0) {
+      rw_cnt[tile] = (uint32_t)nrows;
+      fl_cnt[tile] = (uint32_t)nflag;
+    }
+    return;
+  }
+  // row index = rows of smaller gammas + rows before this node in its group
+  int rows_before[NS];
+#pragma unroll
+  for (int sl = 0; sl < NS; ++sl) rows_before[sl] = eqb[sl] / R;
+#pragma unroll
+  for (int s2 = 0; s2 < NS; ++s2) {
+    const bool lead = valid[s2] && !flag[s2] && eqb[s2] == 0;
+    const int nr = lead ? (eqn[s2] + R - 1) / R : 0;
+    for (int l2 = 0; l2 < 32; ++l2) {
+      const uint32_t kj = __shfl_sync(0xffffffffu, key[s2], l2);
+      const int rj = __shfl_sync(0xffffffffu, nr, l2);
+#pragma unroll
+      for (int sl = 0; sl < NS; ++sl) rows_before[sl] += (rj && kj < key[sl]) ? rj : 0;
+    }
+  }
+  const uint32_t r0 = rw_off[tile], f0 = fl_off[tile];
+  int fbase = 0;
+#pragma unroll
+  for (int sl = 0; sl < NS; ++sl) {
+    const int m = lane + 32 * sl;
+    const uint32_t fb = __ballot_sync(0xffffffffu, flag[sl]);
+    if (valid[sl]) {
+      const int rank = less[sl] + eqb[sl];
+      e_perm[base + rank] = (uint8_t)m;
+      const size_t e = base + m;
+      PropTiles::Ent x;
+      x.ts = e_t[3 * e];
+      x.tt = e_t[3 * e + 1];
+      x.tp = e_t[3 * e + 2];
+      x.tr = e_T[e].x;
+      x.ti = e_T[e].y;
+      x.node = (uint32_t)m;
+      x.pad = 0;
+      ent[base + rank] = x;
+      if (start[sl]) {
+        const int cnt = min(R, eqn[sl] - eqb[sl]);
+        rw[r0 + rows_before[sl]] =
+            make_uint2(key[sl], (uint32_t)rank | ((uint32_t)cnt << 16) |
+                                    ((eqb[sl] == 0 ? 1u : 0u) << 24));
+      }
+      if (flag[sl]) fl_node[f0 + fbase + __popc(fb & ((1u << lane) - 1u))] = (uint16_t)m;
+    }
+    fbase += __popc(fb);
+  }
 }
 
 __global__ void k_chunk_flags(const uint32_t* gsorted, uint32_t n, uint32_t* flag) {
@@ -296,9 +362,9 @@ __global__ void k_mark_nodes_tiles(const __grid_constant__ LevelDev L,
   const uint32_t gi = T.cone_gidx[q];
   for (uint32_t cb = U.child_begin[pb]; cb < U.child_begin[pb + 1]; ++cb) {
     const uint32_t tile = gi * 8 + (uint32_t)(L.code[cb] & 7);
-    for (uint32_t r = T.rt_off[tile]; r < T.rt_off[tile + 1]; ++r) {
-      const uint4 R = T.rt[r];
-      if (R.w == 0) continue;  // not the first row tile of its group
+    for (uint32_t r = T.rw_off[tile]; r < T.rw_off[tile + 1]; ++r) {
+      const uint2 R = T.rw[r];
+      if (!(R.y >> 24)) continue;  // not the first row of its gamma group
       const uint64_t idx = (uint64_t)cb * L.G + R.x;
       const uint64_t msk = 1ull << (idx & 63);
       uint64_t* w = bits + (idx >> 6);
@@ -754,12 +820,20 @@ __global__ void __launch_bounds__(kRowThreads, IFGF_ROWS_MINB)
         const uint32_t cq = ncq, rwy = nrwy;
         if (t + 32 < total) {
           row_of(t + 32, nc_, ncq, nrwy);
+#if IFGF_ROWS_PF >= 1
           if (ncq != kNone) {
             const char* pf = (const char*)(child + (size_t)ncq * BL::Pst);
 #pragma unroll
             for (int l = 0; l < (BL::Pst * 16 + 127) / 128; ++l)
               asm volatile("prefetch.global.L1 [%0];" ::"l"(pf + 128 * l));
+#if IFGF_ROWS_PF >= 2
+            const char* pe = (const char*)(T.ent + (size_t)s_tile[w][nc_] * P + (nrwy & 0xffffu));
+#pragma unroll
+            for (int l = 0; l < (R * (int)sizeof(PropTiles::Ent) + 127) / 128 + 1; ++l)
+              asm volatile("prefetch.global.L1 [%0];" ::"l"(pe + 128 * l));
+#endif
           }
+#endif
         }
         const uint32_t tl = s_tile[w][c], cb = s_cb0[w][c] + kc, loc = t - s_pre[w][c];
         double2* acc = sv + c * P;
@@ -768,7 +842,7 @@ __global__ void __launch_bounds__(kRowThreads, IFGF_ROWS_MINB)
             raise_err(err, kErrPropCover);
             continue;
           }
-          const int pos = (int)(rwy & 0xffffu), cnt = (int)(rwy >> 16);
+          const int pos = (int)(rwy & 0xffffu), cnt = (int)((rwy >> 16) & 0xffu);
           const PropTiles::Ent* en = T.ent + (size_t)tl * P + pos;
           double ts[R], tt[R], tp[R];
 #pragma unroll
@@ -1078,32 +1152,7 @@ void build_prop_tiles(ifgf_plan* P, int d, void* (*scratch)(void*, size_t), void
   T.e_gc = P->alloc<uint32_t>(ne);
   k_tile_entries<<<nblk(ne, 128), 128, 0, s>>>(U.dev(), L.dev(), K, T.gamma_of, ng, P->kappa, T.e_t,
                                           T.e_T, T.e_gc);
-  uint32_t* rt_cnt = P->alloc<uint32_t>(ntiles + 1);
-  uint32_t* fl_cnt = P->alloc<uint32_t>(ntiles + 1);
-  IFGF_CUDA(cudaMemsetAsync(rt_cnt + ntiles, 0, 4, s));
-  IFGF_CUDA(cudaMemsetAsync(fl_cnt + ntiles, 0, 4, s));
-  k_tile_rows<<<nblk(ntiles, 64), 64, 0, s>>>(ntiles, K.P, T.e_gc, rt_cnt, fl_cnt, nullptr,
-                                              nullptr, nullptr, nullptr, nullptr);
-  T.rt_off = P->alloc<uint32_t>(ntiles + 1);
-  T.fl_off = P->alloc<uint32_t>(ntiles + 1);
-  {
-    size_t tb = 0;
-    cub::DeviceScan::ExclusiveSum(nullptr, tb, rt_cnt, T.rt_off, (int)(ntiles + 1), s);
-    IFGF_CUDA(cub::DeviceScan::ExclusiveSum(scratch(sctx, tb), tb, rt_cnt, T.rt_off,
-                                            (int)(ntiles + 1), s));
-    IFGF_CUDA(cub::DeviceScan::ExclusiveSum(scratch(sctx, tb), tb, fl_cnt, T.fl_off,
-                                            (int)(ntiles + 1), s));
-  }
-  uint32_t tot[2];
-  IFGF_CUDA(cudaMemcpyAsync(&tot[0], T.rt_off + ntiles, 4, cudaMemcpyDeviceToHost, s));
-  IFGF_CUDA(cudaMemcpyAsync(&tot[1], T.fl_off + ntiles, 4, cudaMemcpyDeviceToHost, s));
-  IFGF_CUDA(cudaStreamSynchronize(s));
-  T.rt = P->alloc<uint4>(tot[0] + 1);
-  T.fl_node = P->alloc<uint16_t>(tot[1] + 1);
-  T.e_perm = P->alloc<uint8_t>(ne);
-  k_tile_rows<<<nblk(ntiles, 64), 64, 0, s>>>(ntiles, K.P, T.e_gc, nullptr, nullptr, T.rt_off,
-                                              T.rt, T.fl_off, T.fl_node, T.e_perm);
-  // rows of <= row_nodes (IFGF_PROP_ROWS) and the entries in row order
+  // order, rows of <= row_nodes (IFGF_PROP_ROWS), flagged lists, row-ordered entries
   {
     static const int rn_env = [] {
       const char* v = std::getenv("IFGF_ROWS_R");
@@ -1111,56 +1160,52 @@ void build_prop_tiles(ifgf_plan* P, int d, void* (*scratch)(void*, size_t), void
     }();
     // nodes per row: register budget of eval_block_multi (~17 doubles per node)
     T.row_nodes = rn_env >= 2 && rn_env <= 3 ? rn_env : (K.P <= 100 ? 3 : 2);
-    k_tile_rows_n<<<nblk(ntiles, 64), 64, 0, s>>>(ntiles, K.P, T.row_nodes, T.e_gc, T.e_perm,
-                                                  rt_cnt, nullptr, nullptr);
-    T.rw_off = P->alloc<uint32_t>(ntiles + 1);
+  }
+  uint32_t* rw_cnt = P->alloc<uint32_t>(ntiles + 1);
+  uint32_t* fl_cnt = P->alloc<uint32_t>(ntiles + 1);
+  IFGF_CUDA(cudaMemsetAsync(rw_cnt + ntiles, 0, 4, s));
+  IFGF_CUDA(cudaMemsetAsync(fl_cnt + ntiles, 0, 4, s));
+  const int NS = (K.P + 31) / 32;
+  auto sort_pass = [&](bool count) {
+    const unsigned g = nblk((size_t)ntiles * 32, 256);
+    auto go = [&](auto kern) {
+      kern<<<g, 256, 0, s>>>(ntiles, K.P, T.row_nodes, T.e_gc, T.e_t, T.e_T,
+                             count ? rw_cnt : nullptr, count ? fl_cnt : nullptr, T.rw_off,
+                             T.fl_off, T.rw, T.fl_node, T.e_perm, T.ent);
+    };
+    switch (NS) {
+      case 1: go(k_tile_sort<1>); break;
+      case 2: go(k_tile_sort<2>); break;
+      case 3: go(k_tile_sort<3>); break;
+      case 4: go(k_tile_sort<4>); break;
+      case 5: go(k_tile_sort<5>); break;
+      case 6: go(k_tile_sort<6>); break;
+      case 7: go(k_tile_sort<7>); break;
+      default: go(k_tile_sort<8>); break;
+    }
+  };
+  sort_pass(true);
+  T.rw_off = P->alloc<uint32_t>(ntiles + 1);
+  T.fl_off = P->alloc<uint32_t>(ntiles + 1);
+  {
     size_t tb = 0;
-    cub::DeviceScan::ExclusiveSum(nullptr, tb, rt_cnt, T.rw_off, (int)(ntiles + 1), s);
-    IFGF_CUDA(cub::DeviceScan::ExclusiveSum(scratch(sctx, tb), tb, rt_cnt, T.rw_off,
+    cub::DeviceScan::ExclusiveSum(nullptr, tb, rw_cnt, T.rw_off, (int)(ntiles + 1), s);
+    IFGF_CUDA(cub::DeviceScan::ExclusiveSum(scratch(sctx, tb), tb, rw_cnt, T.rw_off,
                                             (int)(ntiles + 1), s));
-    uint32_t nrw = 0;
-    IFGF_CUDA(cudaMemcpyAsync(&nrw, T.rw_off + ntiles, 4, cudaMemcpyDeviceToHost, s));
-    IFGF_CUDA(cudaStreamSynchronize(s));
-    T.rw = P->alloc<uint2>(nrw + 1);
-    k_tile_rows_n<<<nblk(ntiles, 64), 64, 0, s>>>(ntiles, K.P, T.row_nodes, T.e_gc, T.e_perm,
-                                                  nullptr, T.rw_off, T.rw);
-    T.ent = P->alloc<PropTiles::Ent>(ne);
-    k_tile_ent<<<nblk(ne, 256), 256, 0, s>>>(ne, K.P, T.e_perm, T.e_t, T.e_T, T.ent);
-    P->launches += 4;
+    IFGF_CUDA(cub::DeviceScan::ExclusiveSum(scratch(sctx, tb), tb, fl_cnt, T.fl_off,
+                                            (int)(ntiles + 1), s));
   }
-  // parent cones sorted by gamma index (stable) -> chunks of <= kChunk
-  uint32_t* qidx = P->alloc<uint32_t>(U.nc);
-  uint32_t* gsorted = P->alloc<uint32_t>(U.nc);
-  T.qsorted = P->alloc<uint32_t>(U.nc);
-  {
-    std::vector<uint32_t> iota(U.nc);
-    for (uint32_t i = 0; i < U.nc; ++i) iota[i] = i;
-    IFGF_CUDA(cudaMemcpyAsync(qidx, iota.data(), U.nc * 4, cudaMemcpyHostToDevice, s));
-    size_t tb = 0;
-    int bits = 1;
-    while ((1u << bits) < ng && bits < 32) ++bits;
-    cub::DeviceRadixSort::SortPairs(nullptr, tb, T.cone_gidx, gsorted, qidx, T.qsorted,
-                                    (int)U.nc, 0, bits, s);
-    IFGF_CUDA(cub::DeviceRadixSort::SortPairs(scratch(sctx, tb), tb, T.cone_gidx, gsorted, qidx,
-                                              T.qsorted, (int)U.nc, 0, bits, s));
-    IFGF_CUDA(cudaStreamSynchronize(s));
-  }
-  uint32_t* flag = P->alloc<uint32_t>(U.nc + 1);
-  uint32_t* pos = P->alloc<uint32_t>(U.nc + 1);
-  k_chunk_flags<<<nblk(U.nc + 1), 256, 0, s>>>(gsorted, U.nc, flag);
-  {
-    size_t tb = 0;
-    cub::DeviceScan::ExclusiveSum(nullptr, tb, flag, pos, (int)(U.nc + 1), s);
-    IFGF_CUDA(cub::DeviceScan::ExclusiveSum(scratch(sctx, tb), tb, flag, pos, (int)(U.nc + 1), s));
-  }
-  uint32_t nch = 0;
-  IFGF_CUDA(cudaMemcpyAsync(&nch, pos + U.nc, 4, cudaMemcpyDeviceToHost, s));
+  uint32_t tot[2];
+  IFGF_CUDA(cudaMemcpyAsync(&tot[0], T.rw_off + ntiles, 4, cudaMemcpyDeviceToHost, s));
+  IFGF_CUDA(cudaMemcpyAsync(&tot[1], T.fl_off + ntiles, 4, cudaMemcpyDeviceToHost, s));
   IFGF_CUDA(cudaStreamSynchronize(s));
-  T.nchunks = nch;
-  T.chunk_start = P->alloc<uint32_t>(nch + 1);
-  k_chunk_starts<<<nblk(U.nc + 1), 256, 0, s>>>(flag, pos, U.nc, T.chunk_start, nch);
+  T.rw = P->alloc<uint2>(tot[0] + 1);
+  T.fl_node = P->alloc<uint16_t>(tot[1] + 1);
+  T.e_perm = P->alloc<uint8_t>(ne);
+  T.ent = P->alloc<PropTiles::Ent>(ne);
+  sort_pass(false);
   IFGF_CUDA(cudaGetLastError());
-  P->launches += 7;
+  P->launches += 3;
   T.enabled = true;
 }
 
@@ -1202,12 +1247,74 @@ bool launch_propagation_fly(ifgf_plan* P, int d, uint32_t qb, uint32_t qe, const
   });
 }
 
+// Row tiles of 8 and gamma-sorted cone chunks for IFGF_PROP_DMMA, built on
+// first use (the default kernels do not need them).
+void build_dmma_extras(ifgf_plan* P, int d, cudaStream_t s) {
+  PropTiles& T = P->tiles[d];
+  const Level& U = P->lv[d - 1];
+  const InterpConsts& K = P->K;
+  const uint32_t ntiles = T.ngamma * 8;
+  uint32_t* rt_cnt = P->alloc<uint32_t>(ntiles + 1);
+  uint32_t* fl_cnt = P->alloc<uint32_t>(ntiles + 1);
+  IFGF_CUDA(cudaMemsetAsync(rt_cnt + ntiles, 0, 4, s));
+  k_tile_rows<<<nblk(ntiles, 64), 64, 0, s>>>(ntiles, K.P, T.e_gc, rt_cnt, fl_cnt, nullptr,
+                                              nullptr, nullptr, nullptr, nullptr);
+  T.rt_off = P->alloc<uint32_t>(ntiles + 1);
+  auto tmp = [&](size_t b) { return (void*)P->alloc<char>(b); };
+  {
+    size_t tb = 0;
+    cub::DeviceScan::ExclusiveSum(nullptr, tb, rt_cnt, T.rt_off, (int)(ntiles + 1), s);
+    IFGF_CUDA(cub::DeviceScan::ExclusiveSum(tmp(tb), tb, rt_cnt, T.rt_off, (int)(ntiles + 1), s));
+  }
+  uint32_t nrt = 0;
+  IFGF_CUDA(cudaMemcpyAsync(&nrt, T.rt_off + ntiles, 4, cudaMemcpyDeviceToHost, s));
+  IFGF_CUDA(cudaStreamSynchronize(s));
+  T.rt = P->alloc<uint4>(nrt + 1);
+  k_tile_rows<<<nblk(ntiles, 64), 64, 0, s>>>(ntiles, K.P, T.e_gc, nullptr, nullptr, T.rt_off,
+                                              T.rt, nullptr, nullptr, nullptr);
+  // parent cones sorted by gamma index (stable) -> chunks of <= kChunk
+  uint32_t* qidx = P->alloc<uint32_t>(U.nc);
+  uint32_t* gsorted = P->alloc<uint32_t>(U.nc);
+  T.qsorted = P->alloc<uint32_t>(U.nc);
+  {
+    std::vector<uint32_t> iota(U.nc);
+    for (uint32_t i = 0; i < U.nc; ++i) iota[i] = i;
+    IFGF_CUDA(cudaMemcpyAsync(qidx, iota.data(), U.nc * 4, cudaMemcpyHostToDevice, s));
+    size_t tb = 0;
+    int bits = 1;
+    while ((1u << bits) < T.ngamma && bits < 32) ++bits;
+    cub::DeviceRadixSort::SortPairs(nullptr, tb, T.cone_gidx, gsorted, qidx, T.qsorted,
+                                    (int)U.nc, 0, bits, s);
+    IFGF_CUDA(cub::DeviceRadixSort::SortPairs(tmp(tb), tb, T.cone_gidx, gsorted, qidx,
+                                              T.qsorted, (int)U.nc, 0, bits, s));
+    IFGF_CUDA(cudaStreamSynchronize(s));
+  }
+  uint32_t* flag = P->alloc<uint32_t>(U.nc + 1);
+  uint32_t* pos = P->alloc<uint32_t>(U.nc + 1);
+  k_chunk_flags<<<nblk(U.nc + 1), 256, 0, s>>>(gsorted, U.nc, flag);
+  {
+    size_t tb = 0;
+    cub::DeviceScan::ExclusiveSum(nullptr, tb, flag, pos, (int)(U.nc + 1), s);
+    IFGF_CUDA(cub::DeviceScan::ExclusiveSum(tmp(tb), tb, flag, pos, (int)(U.nc + 1), s));
+  }
+  uint32_t nch = 0;
+  IFGF_CUDA(cudaMemcpyAsync(&nch, pos + U.nc, 4, cudaMemcpyDeviceToHost, s));
+  IFGF_CUDA(cudaStreamSynchronize(s));
+  T.nchunks = nch;
+  T.chunk_start = P->alloc<uint32_t>(nch + 1);
+  k_chunk_starts<<<nblk(U.nc + 1), 256, 0, s>>>(flag, pos, U.nc, T.chunk_start, nch);
+  IFGF_CUDA(cudaGetLastError());
+  P->launches += 5;
+}
+
 bool launch_propagation_mma(ifgf_plan* P, int d, uint32_t qb, uint32_t qe, const double2* child,
                             double2* parent, cudaStream_t s) {
-  const PropTiles& T = P->tiles[d];
+  PropTiles& T = P->tiles[d];
   if (P->prop_kernel == IFGF_PROP_FLY || (P->prop_kernel == IFGF_PROP_ROWS && !T.enabled))
     return launch_propagation_fly(P, d, qb, qe, child, parent, s);
-  if (!T.enabled || T.nchunks == 0) return false;
+  if (!T.enabled) return false;
+  if (P->prop_kernel == IFGF_PROP_DMMA && !T.rt) build_dmma_extras(P, d, s);
+  if (T.nchunks == 0 && P->prop_kernel == IFGF_PROP_DMMA) return false;
   const bool full = qb == 0 && qe == P->lv[d - 1].nc;
   if (P->prop_kernel == IFGF_PROP_ROWS) {
     const Level& U = P->lv[d - 1];

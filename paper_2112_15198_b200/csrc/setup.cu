@@ -293,6 +293,14 @@ __device__ __forceinline__ void set_bit(uint64_t* bits, uint64_t idx) {
   if (!(*w & m)) atomicOr((unsigned long long*)w, (unsigned long long)m);
 }
 
+// set_bit with the lanes of a warp that mark the same segment merged (nodes
+// of one cone, and neighbouring points, mostly fall into the same segment).
+__device__ __forceinline__ void set_bit_warp(uint64_t* bits, uint64_t idx) {
+  const unsigned act = __activemask();
+  const unsigned peers = __match_any_sync(act, idx);
+  if ((threadIdx.x & 31) == (unsigned)(__ffs(peers) - 1)) set_bit(bits, idx);
+}
+
 // Clause 1 (cones.cpp:100-106), transposed: every sorted point marks, in each
 // cousin box of its own box (the cousin relation is symmetric), the segment
 // containing it.
@@ -314,7 +322,7 @@ __global__ void k_mark_points(const __grid_constant__ LevelDev L, const uint32_t
       raise_err(err, e);
       return;
     }
-    set_bit(bits, (uint64_t)cb * L.G + g);
+    set_bit_warp(bits, (uint64_t)cb * L.G + g);
   }
 }
 
@@ -341,7 +349,7 @@ __global__ void k_mark_nodes(const __grid_constant__ LevelDev L, const __grid_co
       raise_err(err, e);
       return;
     }
-    set_bit(bits, (uint64_t)cb * L.G + g);
+    set_bit_warp(bits, (uint64_t)cb * L.G + g);
   }
 }
 
