@@ -126,17 +126,19 @@ struct PropTiles {
   double* e_t = nullptr;        // ts, tt, tp
   double2* e_T = nullptr;       // transfer factor (rp/rc) e^{i kappa (rc - rp)}
   uint32_t* e_gc = nullptr;     // child gamma; bit 31 = flagged (exact per-box path)
-  // row tiles: 8 nodes sharing one child gamma; CSR over (gidx * 8 + octant)
-  uint32_t* rt_off = nullptr;
-  uint4* rt = nullptr;          // {child gamma, nodes 0-3 (u8), nodes 4-7 (u8), unused}
-  uint32_t* fl_off = nullptr;   // flagged nodes CSR over tiles
+  // per tile (gidx * 8 + octant), fixed stride P: nodes ordered by child
+  // gamma (flagged last), flagged nodes, rows of <= row_nodes nodes sharing a
+  // child gamma (IFGF_PROP_ROWS) {child gamma, first permuted position |
+  // count << 16 | first-of-group << 24}; entry data permuted into row order
+  uint8_t* e_perm = nullptr;
+  uint32_t* fl_cnt = nullptr;
   uint16_t* fl_node = nullptr;
-  uint8_t* e_perm = nullptr;    // per tile: nodes ordered by child gamma (flagged last)
-  // rows of <= row_nodes nodes sharing one child gamma (IFGF_PROP_ROWS);
-  // CSR over tiles; entry data permuted into row order
   int row_nodes = 3;
-  uint32_t* rw_off = nullptr;
-  uint2* rw = nullptr;          // {child gamma, first permuted position | count << 16}
+  uint32_t* rw_cnt = nullptr;
+  uint2* rw = nullptr;
+  // IFGF_PROP_DMMA only (built on first use): row tiles of 8, CSR over tiles
+  uint32_t* rt_off = nullptr;
+  uint4* rt = nullptr;          // {child gamma, nodes 0-3 (u8), nodes 4-7 (u8), group rows}
   struct Ent {
     double ts, tt;  // local coordinates (16-byte aligned pairs)
     double tr, ti;  // transfer factor

@@ -64,20 +64,20 @@ struct TilesDev {
   const uint32_t* e_gc;
   const uint32_t* rt_off;
   const uint4* rt;
-  const uint32_t* fl_off;
+  const uint32_t* fl_cnt;   // flagged nodes of tile t: fl_node[t * P + i], i < fl_cnt[t]
   const uint16_t* fl_node;
   const uint32_t* qsorted;
   const uint32_t* chunk_start;
   const uint8_t* e_perm;
-  const uint32_t* rw_off;
+  const uint32_t* rw_cnt;   // rows of tile t: rw[t * P + i], i < rw_cnt[t]
   const uint2* rw;
   const PropTiles::Ent* ent;
 };
 
 TilesDev tiles_dev(const PropTiles& t) {
   return {t.ngamma,   t.cone_gidx,   t.gamma_of, t.e_t,    t.e_T,  t.e_gc, t.rt_off,
-          t.rt,       t.fl_off,      t.fl_node,  t.qsorted, t.chunk_start, t.e_perm,
-          t.rw_off,   t.rw,          t.ent};
+          t.rt,       t.fl_cnt,      t.fl_node,  t.qsorted, t.chunk_start, t.e_perm,
+          t.rw_cnt,   t.rw,          t.ent};
 }
 
 inline unsigned nblk(size_t n, int t = 256) { return (unsigned)((n + t - 1) / t); }
@@ -119,6 +119,9 @@ __global__ void k_tile_entries(const __grid_constant__ LevelDev U, const __grid_
                                const __grid_constant__ InterpConsts K, const uint32_t* gamma_of,
                                uint32_t ngamma, double kappa, double* e_t, double2* e_T,
                                uint32_t* e_gc) {
+  __shared__ double2 trig[kTrigEntries];
+  stage_trig(trig, L.trig);
+  __syncthreads();
   const size_t t = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
   if (t >= (size_t)ngamma * 8 * K.P) return;
   const int m = (int)(t % K.P);
@@ -139,7 +142,7 @@ __global__ void k_tile_entries(const __grid_constant__ LevelDev U, const __grid_
   const double rho2 = fma(dy, dy, dx * dx), r2 = fma(dz, dz, rho2);
   const double rinv = rsqrt(r2), s = L.rad * rinv, rho_inv = rsqrt(rho2);
   double theta, phi;
-  fast_angles(L.trig, dx, dy, dz, rho2 * rho_inv, rinv, rho_inv, theta, phi);
+  fast_angles(trig, dx, dy, dz, rho2 * rho_inv, rinv, rho_inv, theta, phi);
   const double fs = s * L.iw0, ft = theta * L.iw1, fp = phi * L.iw2;
   const bool flag = !(rho2 > 0.0) || s > kSMaxTol * (1.0 - 1e-12) || near_boundary(fs) ||
                     near_boundary(ft) || near_boundary(fp);
@@ -221,16 +224,15 @@ __global__ void k_tile_rows(uint32_t ntiles, int P, const uint32_t* e_gc, uint32
 
 // Warp per tile: nodes ordered by raw e_gc (child gamma ascending, flagged
 // ones last), node order within a gamma -- ranks by all-pairs comparison in
-// registers (no serial scans).  Pass 1 counts rows of <= R nodes and flagged
-// nodes; pass 2 writes e_perm, the rows {gamma, position | count << 16 |
-// first-of-group << 24}, the flagged list (node order) and the row-ordered
-// entries.
+// registers (no serial scans).  Writes e_perm, the rows of <= R nodes
+// {gamma, position | count << 16 | first-of-group << 24}, the flagged list
+// (node order), both at a fixed stride of P per tile with their counts, and
+// the row-ordered entries.
 template <int NS>
 __global__ void __launch_bounds__(256)
     k_tile_sort(uint32_t ntiles, int P, int R, const uint32_t* __restrict__ e_gc,
                 const double* __restrict__ e_t, const double2* __restrict__ e_T,
-                uint32_t* rw_cnt, uint32_t* fl_cnt, const uint32_t* __restrict__ rw_off,
-                const uint32_t* __restrict__ fl_off, uint2* rw, uint16_t* fl_node,
+                uint32_t* rw_cnt, uint32_t* fl_cnt, uint2* rw, uint16_t* fl_node,
                 uint8_t* e_perm, PropTiles::Ent* ent) {
   const uint32_t tile = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
@@ -270,12 +272,9 @@ __global__ void __launch_bounds__(256)
     nrows += __popc(__ballot_sync(0xffffffffu, start[sl]));
     nflag += __popc(__ballot_sync(0xffffffffu, flag[sl]));
   }
-  if (rw_cnt) {
-    if (lane == 0) {
-      rw_cnt[tile] = (uint32_t)nrows;
-      fl_cnt[tile] = (uint32_t)nflag;
-    }
-    return;
+  if (lane == 0) {
+    rw_cnt[tile] = (uint32_t)nrows;
+    fl_cnt[tile] = (uint32_t)nflag;
   }
   // row index = rows of smaller gammas + rows before this node in its group
   int rows_before[NS];
@@ -292,7 +291,7 @@ __global__ void __launch_bounds__(256)
       for (int sl = 0; sl < NS; ++sl) rows_before[sl] += (rj && kj < key[sl]) ? rj : 0;
     }
   }
-  const uint32_t r0 = rw_off[tile], f0 = fl_off[tile];
+  const size_t r0 = base, f0 = base;  // fixed stride P per tile
   int fbase = 0;
 #pragma unroll
   for (int sl = 0; sl < NS; ++sl) {
@@ -362,16 +361,16 @@ __global__ void k_mark_nodes_tiles(const __grid_constant__ LevelDev L,
   const uint32_t gi = T.cone_gidx[q];
   for (uint32_t cb = U.child_begin[pb]; cb < U.child_begin[pb + 1]; ++cb) {
     const uint32_t tile = gi * 8 + (uint32_t)(L.code[cb] & 7);
-    for (uint32_t r = T.rw_off[tile]; r < T.rw_off[tile + 1]; ++r) {
-      const uint2 R = T.rw[r];
+    for (uint32_t r = 0; r < T.rw_cnt[tile]; ++r) {
+      const uint2 R = T.rw[(size_t)tile * K.P + r];
       if (!(R.y >> 24)) continue;  // not the first row of its gamma group
       const uint64_t idx = (uint64_t)cb * L.G + R.x;
       const uint64_t msk = 1ull << (idx & 63);
       uint64_t* w = bits + (idx >> 6);
       if (!(*w & msk)) atomicOr((unsigned long long*)w, (unsigned long long)msk);
     }
-    for (uint32_t f = T.fl_off[tile]; f < T.fl_off[tile + 1]; ++f) {
-      const int m = T.fl_node[f];
+    for (uint32_t f = 0; f < T.fl_cnt[tile]; ++f) {
+      const int m = T.fl_node[(size_t)tile * K.P + f];
       const int jp = m % K.pp, jt = (m / K.pp) % K.pt, js = m / (K.pp * K.pt);
       const SegMid sg = segment_mid(U, U.cone_gamma[q]);
       double x, y, z;
@@ -575,8 +574,9 @@ __global__ void __launch_bounds__(kMmaWarps * 32)
       ga = gb;
     }
     // flagged nodes: per-box exact locate + evaluation (rare)
-    const uint32_t f0 = T.fl_off[tile], f1 = T.fl_off[tile + 1];
-    for (uint32_t i = threadIdx.x; i < (f1 - f0) * (uint32_t)nq; i += blockDim.x) {
+    const size_t f0 = (size_t)tile * P;
+    const uint32_t nfl = T.fl_cnt[tile];
+    for (uint32_t i = threadIdx.x; i < nfl * (uint32_t)nq; i += blockDim.x) {
       const int c = (int)(i % nq);
       const int m = T.fl_node[f0 + i / nq];
       const uint32_t cb = cbox[c][o];
@@ -779,9 +779,8 @@ __global__ void __launch_bounds__(kRowThreads, IFGF_ROWS_MINB)
       if (lane < nw && kc < nch) {
         const uint32_t cb = cb0 + kc;
         tile = tbase + (uint32_t)(L.code[cb] & 7);
-        const uint32_t r0 = T.rw_off[tile];
-        nrow = T.rw_off[tile + 1] - r0;
-        n = nrow + T.fl_off[tile + 1] - T.fl_off[tile];
+        nrow = T.rw_cnt[tile];
+        n = nrow + T.fl_cnt[tile];
       }
       uint32_t incl = n;
 #pragma unroll
@@ -807,7 +806,7 @@ __global__ void __launch_bounds__(kRowThreads, IFGF_ROWS_MINB)
         cq = kNone;
         rwy = 0;
         if (loc < s_nrow[w][c]) {
-          const uint2 rw = T.rw[T.rw_off[tl] + loc];
+          const uint2 rw = T.rw[(size_t)tl * P + loc];
           rwy = rw.y;
           cq = find_cone(L, s_cb0[w][c] + kc, rw.x);
         }
@@ -872,7 +871,7 @@ __global__ void __launch_bounds__(kRowThreads, IFGF_ROWS_MINB)
         } else {
           // flagged node: the exact per-box path
           const uint32_t q = q0 + c;
-          const int m = T.fl_node[T.fl_off[tl] + (loc - s_nrow[w][c])];
+          const int m = T.fl_node[(size_t)tl * P + (loc - s_nrow[w][c])];
           const uint32_t pb = U.cone_box[q];
           const int jp = m % PP, jt = (m / PP) % PT, js = m / (PP * PT);
           const SegMid sg = segment_mid(U, U.cone_gamma[q]);
@@ -1150,7 +1149,7 @@ void build_prop_tiles(ifgf_plan* P, int d, void* (*scratch)(void*, size_t), void
   T.e_t = P->alloc<double>(3 * ne);
   T.e_T = P->alloc<double2>(ne);
   T.e_gc = P->alloc<uint32_t>(ne);
-  k_tile_entries<<<nblk(ne, 128), 128, 0, s>>>(U.dev(), L.dev(), K, T.gamma_of, ng, P->kappa, T.e_t,
+  k_tile_entries<<<nblk(ne, 256), 256, 0, s>>>(U.dev(), L.dev(), K, T.gamma_of, ng, P->kappa, T.e_t,
                                           T.e_T, T.e_gc);
   // order, rows of <= row_nodes (IFGF_PROP_ROWS), flagged lists, row-ordered entries
   {
@@ -1161,19 +1160,19 @@ void build_prop_tiles(ifgf_plan* P, int d, void* (*scratch)(void*, size_t), void
     // nodes per row: register budget of eval_block_multi (~17 doubles per node)
     T.row_nodes = rn_env >= 2 && rn_env <= 3 ? rn_env : (K.P <= 100 ? 3 : 2);
   }
-  uint32_t* rw_cnt = P->alloc<uint32_t>(ntiles + 1);
-  uint32_t* fl_cnt = P->alloc<uint32_t>(ntiles + 1);
-  IFGF_CUDA(cudaMemsetAsync(rw_cnt + ntiles, 0, 4, s));
-  IFGF_CUDA(cudaMemsetAsync(fl_cnt + ntiles, 0, 4, s));
-  const int NS = (K.P + 31) / 32;
-  auto sort_pass = [&](bool count) {
+  T.rw_cnt = P->alloc<uint32_t>(ntiles);
+  T.fl_cnt = P->alloc<uint32_t>(ntiles);
+  T.rw = P->alloc<uint2>(ne);
+  T.fl_node = P->alloc<uint16_t>(ne);
+  T.e_perm = P->alloc<uint8_t>(ne);
+  T.ent = P->alloc<PropTiles::Ent>(ne);
+  {
     const unsigned g = nblk((size_t)ntiles * 32, 256);
     auto go = [&](auto kern) {
-      kern<<<g, 256, 0, s>>>(ntiles, K.P, T.row_nodes, T.e_gc, T.e_t, T.e_T,
-                             count ? rw_cnt : nullptr, count ? fl_cnt : nullptr, T.rw_off,
-                             T.fl_off, T.rw, T.fl_node, T.e_perm, T.ent);
+      kern<<<g, 256, 0, s>>>(ntiles, K.P, T.row_nodes, T.e_gc, T.e_t, T.e_T, T.rw_cnt, T.fl_cnt,
+                             T.rw, T.fl_node, T.e_perm, T.ent);
     };
-    switch (NS) {
+    switch ((K.P + 31) / 32) {
       case 1: go(k_tile_sort<1>); break;
       case 2: go(k_tile_sort<2>); break;
       case 3: go(k_tile_sort<3>); break;
@@ -1183,29 +1182,9 @@ void build_prop_tiles(ifgf_plan* P, int d, void* (*scratch)(void*, size_t), void
       case 7: go(k_tile_sort<7>); break;
       default: go(k_tile_sort<8>); break;
     }
-  };
-  sort_pass(true);
-  T.rw_off = P->alloc<uint32_t>(ntiles + 1);
-  T.fl_off = P->alloc<uint32_t>(ntiles + 1);
-  {
-    size_t tb = 0;
-    cub::DeviceScan::ExclusiveSum(nullptr, tb, rw_cnt, T.rw_off, (int)(ntiles + 1), s);
-    IFGF_CUDA(cub::DeviceScan::ExclusiveSum(scratch(sctx, tb), tb, rw_cnt, T.rw_off,
-                                            (int)(ntiles + 1), s));
-    IFGF_CUDA(cub::DeviceScan::ExclusiveSum(scratch(sctx, tb), tb, fl_cnt, T.fl_off,
-                                            (int)(ntiles + 1), s));
   }
-  uint32_t tot[2];
-  IFGF_CUDA(cudaMemcpyAsync(&tot[0], T.rw_off + ntiles, 4, cudaMemcpyDeviceToHost, s));
-  IFGF_CUDA(cudaMemcpyAsync(&tot[1], T.fl_off + ntiles, 4, cudaMemcpyDeviceToHost, s));
-  IFGF_CUDA(cudaStreamSynchronize(s));
-  T.rw = P->alloc<uint2>(tot[0] + 1);
-  T.fl_node = P->alloc<uint16_t>(tot[1] + 1);
-  T.e_perm = P->alloc<uint8_t>(ne);
-  T.ent = P->alloc<PropTiles::Ent>(ne);
-  sort_pass(false);
   IFGF_CUDA(cudaGetLastError());
-  P->launches += 3;
+  P->launches += 1;
   T.enabled = true;
 }
 
