@@ -40,6 +40,7 @@ constexpr int kChunk = IFGF_MMA_CHUNK;    // parent cones per CTA (column tiles 
 constexpr int kMmaWarps = IFGF_MMA_WARPS;  // warps per CTA
 constexpr uint32_t kNone = 0xffffffffu;
 constexpr uint32_t kFlag = 0x80000000u;
+constexpr uint32_t kFlagTask = 0xfffffffeu;  // task meta: flagged node (exact path)
 // 12 warps of <= 168 registers per SM (measured best at C2 among 256/320/384
 // threads and 1-2 CTAs per SM)
 #ifndef IFGF_ROWS_THREADS
@@ -755,8 +756,10 @@ __global__ void __launch_bounds__(kRowThreads, IFGF_ROWS_MINB)
   stage_fit_matrices<PS, PT, PP>(K, sM);
   __syncthreads();
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  double2* sv = smem + (size_t)w * 2 * cpw * P;
+  // per warp: sv, st (cpw * P values each), task meta (<= cpw * P tasks)
+  double2* sv = smem + (size_t)w * 3 * cpw * P;
   double2* st = sv + cpw * P;
+  uint2* meta = reinterpret_cast<uint2*>(st + cpw * P);
   for (int g = 0; g < groups; ++g) {
     const uint32_t q0 = qb + (((uint32_t)blockIdx.x * groups + g) * NW + w) * cpw;
     if (q0 >= qe) break;
@@ -797,46 +800,52 @@ __global__ void __launch_bounds__(kRowThreads, IFGF_ROWS_MINB)
       }
       if (lane == 0) s_pre[w][0] = 0;
       __syncwarp();
-      // task t -> (cone c, row) and its child block; the next task's block is
-      // prefetched into L1 while the current one is evaluated
-      auto row_of = [&](uint32_t t, int& c, uint32_t& cq, uint32_t& rwy) {
-        c = 0;
+      // phase A: every task's child cone ordinal and row (independent loads
+      // across lanes), into shared memory: {cq, c << 24 | cnt << 16 | pos},
+      // flagged tasks {kFlagTask, c << 24 | index}
+      for (uint32_t t = lane; t < total; t += 32) {
+        int c = 0;
         while (s_pre[w][c + 1] <= t) ++c;
         const uint32_t tl = s_tile[w][c], loc = t - s_pre[w][c];
-        cq = kNone;
-        rwy = 0;
+        uint2 mt;
         if (loc < s_nrow[w][c]) {
           const uint2 rw = T.rw[(size_t)tl * P + loc];
-          rwy = rw.y;
-          cq = find_cone(L, s_cb0[w][c] + kc, rw.x);
+          mt = make_uint2(find_cone(L, s_cb0[w][c] + kc, rw.x),
+                          ((uint32_t)c << 24) | (rw.y & 0xffffffu));
+        } else {
+          mt = make_uint2(kFlagTask, ((uint32_t)c << 24) | (loc - s_nrow[w][c]));
         }
-      };
-      int nc_ = 0;
-      uint32_t ncq = kNone, nrwy = 0;
-      if (lane < total) row_of(lane, nc_, ncq, nrwy);
+        meta[t] = mt;
+      }
+      __syncwarp();
+      // phase B: evaluate; the next task's block and entries are prefetched
+      // into L1 while the current one is evaluated
       for (uint32_t t = lane; t < total; t += 32) {
-        const int c = nc_;
-        const uint32_t cq = ncq, rwy = nrwy;
-        if (t + 32 < total) {
-          row_of(t + 32, nc_, ncq, nrwy);
+        const uint2 mt = meta[t];
+        const int c = (int)(mt.y >> 24);
+        const uint32_t cq = mt.x;
 #if IFGF_ROWS_PF >= 1
-          if (ncq != kNone) {
-            const char* pf = (const char*)(child + (size_t)ncq * BL::Pst);
+        if (t + 32 < total) {
+          const uint2 mn = meta[t + 32];
+          if (mn.x < kFlagTask) {
+            const char* pf = (const char*)(child + (size_t)mn.x * BL::Pst);
 #pragma unroll
             for (int l = 0; l < (BL::Pst * 16 + 127) / 128; ++l)
               asm volatile("prefetch.global.L1 [%0];" ::"l"(pf + 128 * l));
 #if IFGF_ROWS_PF >= 2
-            const char* pe = (const char*)(T.ent + (size_t)s_tile[w][nc_] * P + (nrwy & 0xffffu));
+            const char* pe = (const char*)(T.ent + (size_t)s_tile[w][mn.y >> 24] * P +
+                                           (mn.y & 0xffffu));
 #pragma unroll
             for (int l = 0; l < (R * (int)sizeof(PropTiles::Ent) + 127) / 128 + 1; ++l)
               asm volatile("prefetch.global.L1 [%0];" ::"l"(pe + 128 * l));
 #endif
           }
-#endif
         }
-        const uint32_t tl = s_tile[w][c], cb = s_cb0[w][c] + kc, loc = t - s_pre[w][c];
+#endif
+        const uint32_t rwy = mt.y;
+        const uint32_t tl = s_tile[w][c], cb = s_cb0[w][c] + kc;
         double2* acc = sv + c * P;
-        if (loc < s_nrow[w][c]) {
+        if (cq != kFlagTask) {
           if (cq == kNone) {
             raise_err(err, kErrPropCover);
             continue;
@@ -871,7 +880,7 @@ __global__ void __launch_bounds__(kRowThreads, IFGF_ROWS_MINB)
         } else {
           // flagged node: the exact per-box path
           const uint32_t q = q0 + c;
-          const int m = T.fl_node[(size_t)tl * P + (loc - s_nrow[w][c])];
+          const int m = T.fl_node[(size_t)tl * P + (mt.y & 0xffffffu)];
           const uint32_t pb = U.cone_box[q];
           const int jp = m % PP, jt = (m / PP) % PT, js = m / (PP * PT);
           const SegMid sg = segment_mid(U, U.cone_gamma[q]);
@@ -1307,15 +1316,15 @@ bool launch_propagation_mma(ifgf_plan* P, int d, uint32_t qb, uint32_t qe, const
         const char* v = std::getenv("IFGF_ROWS_CPW");
         return v ? std::atoi(v) : 0;
       }();
-      // shared memory for sv + st: ~64 KB per CTA (the rest of the SM's SRAM is L1)
-      const int cpw_fit = (int)(64 * 1024 / IFGF_ROWS_MINB / (2 * Pn * sizeof(double2)) / NW);
+      // shared memory for sv + st + task meta: ~96 KB per CTA (the rest of the SRAM is L1)
+      const int cpw_fit = (int)(96 * 1024 / IFGF_ROWS_MINB / (3 * Pn * sizeof(double2)) / NW);
       const int cpw = std::max(1, std::min(kRowMaxCpw, cpw_env > 0 ? cpw_env : std::max(1, cpw_fit)));
       const int cpb = NW * cpw;
       const uint32_t nq = qe - qb;
       const int groups =
           (int)std::min<size_t>(8, std::max<size_t>(1, nq / ((size_t)cpb * 148 * 4)));
       const unsigned grid = (unsigned)((nq + (size_t)cpb * groups - 1) / ((size_t)cpb * groups));
-      const size_t sm = 2 * (size_t)cpb * Pn * sizeof(double2);
+      const size_t sm = 3 * (size_t)cpb * Pn * sizeof(double2);
       auto launch = [&](auto kern) {
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
         kern<<<grid, kRowThreads, sm, s>>>(U.dev(), L.dev(), K, tiles_dev(T), P->kappa, qb, qe,
