@@ -246,9 +246,18 @@ __global__ void __launch_bounds__(128, IFGF_INTERP_MINB)
     acr[j] = aci[j] = 0.0;
   }
   const uint32_t k0 = L.cous_off[b], k1 = L.cous_off[b + 1];
+  // cousin index and centre loaded one iteration ahead
+  uint32_t cbn = k0 < k1 ? L.cous[k0] : 0;
+  double cxn = L.cx[cbn], cyn = L.cy[cbn], czn = L.cz[cbn];
   for (uint32_t k = k0; k < k1; ++k) {
-    const uint32_t cb = L.cous[k];
-    const double cx = L.cx[cb], cy = L.cy[cb], cz = L.cz[cb];
+    const uint32_t cb = cbn;
+    const double cx = cxn, cy = cyn, cz = czn;
+    if (k + 1 < k1) {
+      cbn = L.cous[k + 1];
+      cxn = L.cx[cbn];
+      cyn = L.cy[cbn];
+      czn = L.cz[cbn];
+    }
     Loc o[R];
     int e = 0;
 #pragma unroll
@@ -272,7 +281,12 @@ __global__ void __launch_bounds__(128, IFGF_INTERP_MINB)
       tt[j] = o[j].tt;
       tp[j] = o[j].tp;
     }
+#if IFGF_K4_NOEVAL  // experiment: locate + factor only
+#pragma unroll
+    for (int j = 0; j < R; ++j) vr[j] = ts[j] + q, vi[j] = tt[j] + tp[j];
+#else
     eval_block_multi<PS, PT, PP, R>(blocks + (size_t)q * BL::Pst, ts, tt, tp, vr, vi);
+#endif
 #pragma unroll
     for (int j = 1; j < R; ++j) {
       if (j < n && o[j].gamma != o[0].gamma) {  // another cone of this cousin

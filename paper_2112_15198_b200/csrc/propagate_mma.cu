@@ -1149,6 +1149,17 @@ void build_prop_tiles(ifgf_plan* P, int d, void* (*scratch)(void*, size_t), void
     return v ? std::atof(v) : 3.0;
   }();
   if (uses < min_uses) return;
+  // memory: ~103 B per (gamma, octant, node) entry; above min(8 GB, free / 4)
+  // the on-the-fly rows are the better deal (a Laplace or high-kappa coarse
+  // level can have millions of distinct gammas)
+  {
+    size_t fr = 0, tot = 0;
+    IFGF_CUDA(cudaMemGetInfo(&fr, &tot));
+    const double bytes = (double)ng * 8.0 * K.P *
+                         (sizeof(PropTiles::Ent) + 3 * sizeof(double) + sizeof(double2) +
+                          sizeof(uint32_t) + sizeof(uint2) + sizeof(uint16_t) + 1);
+    if (bytes > std::min(8.0 * (1ull << 30), 0.25 * (double)fr)) return;
+  }
   T.ngamma = ng;
   T.cone_gidx = P->alloc<uint32_t>(U.nc);
   T.gamma_of = P->alloc<uint32_t>(ng);
