@@ -58,11 +58,15 @@ void require_device(int device) {
                                    (e == cudaSuccess ? "0 devices" : cudaGetErrorString(e)) +
                                    "); libifgf_b200 has no CPU path");
   if (device < 0 || device >= count) throw Error(IFGF_EINVAL, "device ordinal out of range");
-  cudaDeviceProp prop;
-  IFGF_CUDA(cudaGetDeviceProperties(&prop, device));
-  if (prop.major != 10)
+  // cudaGetDeviceProperties costs ~1 ms per call: query the major version only
+  int major = 0;
+  IFGF_CUDA(cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, device));
+  if (major != 10) {
+    cudaDeviceProp prop;
+    IFGF_CUDA(cudaGetDeviceProperties(&prop, device));
     throw Error(IFGF_ERUNTIME, std::string("device ") + prop.name +
                                    " is not sm_100 (this build targets sm_100a only)");
+  }
   IFGF_CUDA(cudaSetDevice(device));
   static bool pool_tuned = false;
   if (!pool_tuned) {
@@ -599,13 +603,7 @@ int ifgf_plan_get_info(const ifgf_plan* P, ifgf_plan_info* info) {
       info->cousin_entries[d] = d >= 3 ? L.n_cous : 0;
       info->h[d] = L.h;
     }
-    // neighbour totals need the counts
-    for (int d = 1; d <= P->depth; ++d) {
-      const auto cnt = d2h(P->lv[d].nbr_cnt, P->lv[d].nb, P->s_main);
-      size_t t = 0;
-      for (auto c : cnt) t += c;
-      info->nbr_entries[d] = t;
-    }
+    for (int d = 1; d <= P->depth; ++d) info->nbr_entries[d] = P->lv[d].n_nbr;
     info->setup_seconds = P->setup_seconds;
     info->device_bytes = P->bytes;
     info->setup_launches = P->setup_launches;

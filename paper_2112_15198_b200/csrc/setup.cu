@@ -432,13 +432,50 @@ void build_plan(ifgf_plan* P, const double* d_x, const double* d_y, const double
   cudaStream_t s = P->s_main;
   const size_t n = P->n;
   Scratch scratch{P};
-  // IFGF_SETUP_TRACE=1: synchronise and print the elapsed time at each phase
-  static const bool trace = std::getenv("IFGF_SETUP_TRACE") != nullptr;
+  // IFGF_SETUP_TRACE=1: synchronise and print the elapsed time at each phase;
+  // IFGF_SETUP_TRACE=2: no extra syncs -- record an event per phase on the
+  // main stream and print, per phase, when the host passed it and when the
+  // GPU did (a GPU time just after the host time means the GPU was waiting).
+  static const int trace = [] {
+    const char* v = std::getenv("IFGF_SETUP_TRACE");
+    return v ? std::atoi(v) : 0;
+  }();
+  struct Mark {
+    const char* what;
+    double host_ms;
+    cudaEvent_t ev;
+  };
+  std::vector<Mark> marks;
+  cudaEvent_t ev0 = nullptr;
+  if (trace == 2) {
+    cudaEventCreate(&ev0);
+    cudaEventRecord(ev0, s);
+  }
   auto mark = [&](const char* what) {
-    if (!trace) return;
+    const double hm =
+        std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count() * 1e3;
+    if (trace == 1) {
+      cudaStreamSynchronize(s);
+      std::fprintf(stderr, "[setup] %-28s %8.3f ms\n", what,
+                   std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count() *
+                       1e3);
+    } else if (trace == 2) {
+      cudaEvent_t e;
+      cudaEventCreate(&e);
+      cudaEventRecord(e, s);
+      marks.push_back({what, hm, e});
+    }
+  };
+  auto dump_marks = [&] {
+    if (trace != 2) return;
     cudaStreamSynchronize(s);
-    std::fprintf(stderr, "[setup] %-28s %8.3f ms\n", what,
-                 std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count() * 1e3);
+    for (auto& m : marks) {
+      float g = 0.f;
+      cudaEventElapsedTime(&g, ev0, m.ev);
+      std::fprintf(stderr, "[setup] %-28s host %8.3f ms  gpu %8.3f ms\n", m.what, m.host_ms, g);
+      cudaEventDestroy(m.ev);
+    }
+    cudaEventDestroy(ev0);
   };
 
   // -- bounding cube (geometry.cpp:95-114)
@@ -525,6 +562,7 @@ void build_plan(ifgf_plan* P, const double* d_x, const double* d_y, const double
   uint32_t h_hist[32];
   IFGF_CUDA(cudaMemcpyAsync(h_hist, hist, sizeof h_hist, cudaMemcpyDeviceToHost, s));
   IFGF_CUDA(cudaStreamSynchronize(s));
+  mark("level sizes sync");
   {
     uint32_t acc = 0;
     for (int d = 1; d <= D; ++d) {
@@ -552,6 +590,7 @@ void build_plan(ifgf_plan* P, const double* d_x, const double* d_y, const double
                                        P->cube[2], L.h, L.first, L.code, L.cx, L.cy, L.cz);
     ++P->launches;
   }
+  mark("boxes");
   for (int d = 1; d <= D; ++d) {
     Level& L = P->lv[d];
     L.parent = P->alloc<uint32_t>(L.nb);
@@ -580,6 +619,20 @@ void build_plan(ifgf_plan* P, const double* d_x, const double* d_y, const double
     IFGF_CUDA(cudaMemcpyAsync(&cous_total[d], L.cous_off + L.nb, sizeof(uint32_t),
                               cudaMemcpyDeviceToHost, s));
   }
+  // neighbour-list totals (ifgf_plan_info), read back with the cousin totals
+  std::vector<unsigned long long> nbr_total(D + 1, 0);
+  {
+    unsigned long long* d_tot = P->alloc<unsigned long long>(D + 1);
+    for (int d = 1; d <= D; ++d) {
+      size_t tb = 0;
+      cub::DeviceReduce::Sum(nullptr, tb, P->lv[d].nbr_cnt, d_tot + d, (int)P->lv[d].nb, s);
+      IFGF_CUDA(cub::DeviceReduce::Sum(scratch.get(tb), tb, P->lv[d].nbr_cnt, d_tot + d,
+                                       (int)P->lv[d].nb, s));
+    }
+    IFGF_CUDA(cudaMemcpyAsync(nbr_total.data() + 1, d_tot + 1, D * sizeof(unsigned long long),
+                              cudaMemcpyDeviceToHost, s));
+  }
+  mark("neighbours + cousin counts");
   // K4 work items per level
   {
     const int R = interp_points(P->K.P);
@@ -600,7 +653,10 @@ void build_plan(ifgf_plan* P, const double* d_x, const double* d_y, const double
       P->launches += 3;
     }
   }
+  mark("K4 work items");
   IFGF_CUDA(cudaStreamSynchronize(s));
+  mark("cousin sync");
+  for (int d = 1; d <= D; ++d) P->lv[d].n_nbr = (size_t)nbr_total[d];
   for (int d = 3; d <= D; ++d) {
     Level& L = P->lv[d];
     L.n_cous = cous_total[d];
@@ -611,7 +667,14 @@ void build_plan(ifgf_plan* P, const double* d_x, const double* d_y, const double
 
   mark("octree + cousins");
   // -- relevant cones, d = 3..D (cones.cpp:90-150)
+  // Clause 1 (points) of every level depends only on the octree: all levels
+  // are marked up front on the aux stream, overlapping clause 2 (parent
+  // nodes, level by level, which needs the parent level's cones), the tile
+  // builds and the host round trips for the cone counts on the main stream.
   const ifgf_params& p = P->params;
+  cudaStream_t sa = P->s_aux;
+  cudaEvent_t ev_tree, ev_pts[IFGF_MAX_LEVELS];
+  IFGF_CUDA(cudaEventCreateWithFlags(&ev_tree, cudaEventDisableTiming));
   for (int d = 3; d <= D; ++d) {
     Level& L = P->lv[d];
     const int f = 1 << (D - d);
@@ -629,10 +692,21 @@ void build_plan(ifgf_plan* P, const double* d_x, const double* d_y, const double
     L.nwords = ((uint64_t)L.nb * L.G + 63) / 64;
     L.bits = P->alloc<uint64_t>(L.nwords);
     L.rank = P->alloc<uint32_t>(L.nwords + 1);
-    IFGF_CUDA(cudaMemsetAsync(L.bits, 0, L.nwords * sizeof(uint64_t), s));
-    k_mark_points<<<grid_for(n), kT, 0, s>>>(L.dev(), L.ptbox, P->xs, P->ys, P->zs, n, L.bits,
-                                             P->err);
+  }
+  IFGF_CUDA(cudaEventRecord(ev_tree, s));
+  IFGF_CUDA(cudaStreamWaitEvent(sa, ev_tree, 0));
+  for (int d = 3; d <= D; ++d) {
+    Level& L = P->lv[d];
+    IFGF_CUDA(cudaMemsetAsync(L.bits, 0, L.nwords * sizeof(uint64_t), sa));
+    k_mark_points<<<grid_for(n), kT, 0, sa>>>(L.dev(), L.ptbox, P->xs, P->ys, P->zs, n, L.bits,
+                                              P->err);
     ++P->launches;
+    IFGF_CUDA(cudaEventCreateWithFlags(&ev_pts[d], cudaEventDisableTiming));
+    IFGF_CUDA(cudaEventRecord(ev_pts[d], sa));
+  }
+  for (int d = 3; d <= D; ++d) {
+    Level& L = P->lv[d];
+    IFGF_CUDA(cudaStreamWaitEvent(s, ev_pts[d], 0));
     mark("  mark points");
     if (d > 3 && P->lv[d - 1].nc > 0) {
       build_prop_tiles(
@@ -659,7 +733,7 @@ void build_plan(ifgf_plan* P, const double* d_x, const double* d_y, const double
     IFGF_CUDA(
         cudaMemcpyAsync(&nc, L.rank + L.nwords, sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
     IFGF_CUDA(cudaStreamSynchronize(s));
-    check_device_error(P);
+    mark("  count sync");
     L.nc = nc;
     L.cone_box = P->alloc<uint32_t>(nc + 1);
     L.cone_gamma = P->alloc<uint32_t>(nc + 1);
@@ -670,6 +744,10 @@ void build_plan(ifgf_plan* P, const double* d_x, const double* d_y, const double
     mark("  compact");
   }
   IFGF_CUDA(cudaStreamSynchronize(s));
+  cudaEventDestroy(ev_tree);
+  for (int d = 3; d <= D; ++d) cudaEventDestroy(ev_pts[d]);
+  mark("end");
+  dump_marks();
   check_device_error(P);
   P->setup_seconds =
       std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
