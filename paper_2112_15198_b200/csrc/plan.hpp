@@ -139,13 +139,9 @@ struct PropTiles {
   // IFGF_PROP_DMMA only (built on first use): row tiles of 8, CSR over tiles
   uint32_t* rt_off = nullptr;
   uint4* rt = nullptr;          // {child gamma, nodes 0-3 (u8), nodes 4-7 (u8), group rows}
-  struct Ent {
-    double ts, tt;  // local coordinates (16-byte aligned pairs)
-    double tr, ti;  // transfer factor
-    double tp;
-    uint32_t node, pad;
-  };
-  Ent* ent = nullptr;           // [(gidx * 8 + octant) * P + permuted position]
+  double* rdat = nullptr;       // row data (ts, tt, tp, tr, ti per slot), 32-row chunks,
+                                // SoA inside (propagate_mma.cu row_field)
+  uint32_t* rnode = nullptr;    // per row (tile * P + r): node of slot j in byte j
   // CTA chunks of <= kChunk parent cones sharing one gamma
   uint32_t nchunks = 0;
   uint32_t* qsorted = nullptr;

@@ -50,7 +50,7 @@ constexpr uint32_t kFlagTask = 0xfffffffeu;  // task meta: flagged node (exact p
 #define IFGF_ROWS_MINB 1
 #endif
 constexpr int kRowThreads = IFGF_ROWS_THREADS;
-// L1 prefetch of the next task's child block (1) and row entries (2)
+// L1 prefetch of the next task's child block
 #ifndef IFGF_ROWS_PF
 #define IFGF_ROWS_PF 1
 #endif
@@ -72,13 +72,14 @@ struct TilesDev {
   const uint8_t* e_perm;
   const uint32_t* rw_cnt;   // rows of tile t: rw[t * P + i], i < rw_cnt[t]
   const uint2* rw;
-  const PropTiles::Ent* ent;
+  const double* rdat;
+  const uint32_t* rnode;
 };
 
 TilesDev tiles_dev(const PropTiles& t) {
   return {t.ngamma,   t.cone_gidx,   t.gamma_of, t.e_t,    t.e_T,  t.e_gc, t.rt_off,
           t.rt,       t.fl_cnt,      t.fl_node,  t.qsorted, t.chunk_start, t.e_perm,
-          t.rw_cnt,   t.rw,          t.ent};
+          t.rw_cnt,   t.rw,          t.rdat,     t.rnode};
 }
 
 inline unsigned nblk(size_t n, int t = 256) { return (unsigned)((n + t - 1) / t); }
@@ -223,18 +224,28 @@ __global__ void k_tile_rows(uint32_t ntiles, int P, const uint32_t* e_gc, uint32
   }
 }
 
+// Row data layout: the rows of a tile in chunks of 32; inside a chunk one
+// 32-double column per field, so the lanes of a warp (consecutive rows)
+// read every field with one coalesced 256-byte access, and a tile's rows
+// stay within a few contiguous kilobytes (tiles are re-read by every parent
+// cone of their gamma).
+__host__ __device__ __forceinline__ size_t row_field(size_t tile, int P, int nf, int r, int f) {
+  const size_t chunks = (size_t)(P + 31) / 32;
+  return (((tile * chunks + (size_t)(r >> 5)) * nf + f) << 5) + (r & 31);
+}
+
 // Warp per tile: nodes ordered by raw e_gc (child gamma ascending, flagged
 // ones last), node order within a gamma -- ranks by all-pairs comparison in
 // registers (no serial scans).  Writes e_perm, the rows of <= R nodes
 // {gamma, position | count << 16 | first-of-group << 24}, the flagged list
 // (node order), both at a fixed stride of P per tile with their counts, and
-// the row-ordered entries.
+// the rows' node data (local coordinates, transfer factors, node ids).
 template <int NS>
 __global__ void __launch_bounds__(256)
     k_tile_sort(uint32_t ntiles, int P, int R, const uint32_t* __restrict__ e_gc,
                 const double* __restrict__ e_t, const double2* __restrict__ e_T,
                 uint32_t* rw_cnt, uint32_t* fl_cnt, uint2* rw, uint16_t* fl_node,
-                uint8_t* e_perm, PropTiles::Ent* ent) {
+                uint8_t* e_perm, double* rdat, uint8_t* rnode) {
   const uint32_t tile = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (tile >= ntiles) return;
@@ -301,16 +312,19 @@ __global__ void __launch_bounds__(256)
     if (valid[sl]) {
       const int rank = less[sl] + eqb[sl];
       e_perm[base + rank] = (uint8_t)m;
-      const size_t e = base + m;
-      PropTiles::Ent x;
-      x.ts = e_t[3 * e];
-      x.tt = e_t[3 * e + 1];
-      x.tp = e_t[3 * e + 2];
-      x.tr = e_T[e].x;
-      x.ti = e_T[e].y;
-      x.node = (uint32_t)m;
-      x.pad = 0;
-      ent[base + rank] = x;
+      if (!flag[sl]) {
+        // row data: slot j of row r, field f (ts, tt, tp, tr, ti) at
+        // rdat[row_field(tile, r, f * R + j)] -- 32-row chunks, SoA inside
+        const size_t e = base + m;
+        const int r = rows_before[sl], j = eqb[sl] % R;
+        const int nf = 5 * R;
+        rdat[row_field(tile, P, nf, r, 0 * R + j)] = e_t[3 * e];
+        rdat[row_field(tile, P, nf, r, 1 * R + j)] = e_t[3 * e + 1];
+        rdat[row_field(tile, P, nf, r, 2 * R + j)] = e_t[3 * e + 2];
+        rdat[row_field(tile, P, nf, r, 3 * R + j)] = e_T[e].x;
+        rdat[row_field(tile, P, nf, r, 4 * R + j)] = e_T[e].y;
+        rnode[4 * (base + r) + j] = (uint8_t)m;
+      }
       if (start[sl]) {
         const int cnt = min(R, eqn[sl] - eqb[sl]);
         rw[r0 + rows_before[sl]] =
@@ -801,7 +815,7 @@ __global__ void __launch_bounds__(kRowThreads, IFGF_ROWS_MINB)
       if (lane == 0) s_pre[w][0] = 0;
       __syncwarp();
       // phase A: every task's child cone ordinal and row (independent loads
-      // across lanes), into shared memory: {cq, c << 24 | cnt << 16 | pos},
+      // across lanes), into shared memory: {cq, c << 24 | cnt << 16 | row},
       // flagged tasks {kFlagTask, c << 24 | index}
       for (uint32_t t = lane; t < total; t += 32) {
         int c = 0;
@@ -811,15 +825,15 @@ __global__ void __launch_bounds__(kRowThreads, IFGF_ROWS_MINB)
         if (loc < s_nrow[w][c]) {
           const uint2 rw = T.rw[(size_t)tl * P + loc];
           mt = make_uint2(find_cone(L, s_cb0[w][c] + kc, rw.x),
-                          ((uint32_t)c << 24) | (rw.y & 0xffffffu));
+                          ((uint32_t)c << 24) | (rw.y & 0xff0000u) | loc);
         } else {
           mt = make_uint2(kFlagTask, ((uint32_t)c << 24) | (loc - s_nrow[w][c]));
         }
         meta[t] = mt;
       }
       __syncwarp();
-      // phase B: evaluate; the next task's block and entries are prefetched
-      // into L1 while the current one is evaluated
+      // phase B: evaluate; the next task's block is prefetched into L1 while
+      // the current one is evaluated
       for (uint32_t t = lane; t < total; t += 32) {
         const uint2 mt = meta[t];
         const int c = (int)(mt.y >> 24);
@@ -832,13 +846,6 @@ __global__ void __launch_bounds__(kRowThreads, IFGF_ROWS_MINB)
 #pragma unroll
             for (int l = 0; l < (BL::Pst * 16 + 127) / 128; ++l)
               asm volatile("prefetch.global.L1 [%0];" ::"l"(pf + 128 * l));
-#if IFGF_ROWS_PF >= 2
-            const char* pe = (const char*)(T.ent + (size_t)s_tile[w][mn.y >> 24] * P +
-                                           (mn.y & 0xffffu));
-#pragma unroll
-            for (int l = 0; l < (R * (int)sizeof(PropTiles::Ent) + 127) / 128 + 1; ++l)
-              asm volatile("prefetch.global.L1 [%0];" ::"l"(pe + 128 * l));
-#endif
           }
         }
 #endif
@@ -850,30 +857,30 @@ __global__ void __launch_bounds__(kRowThreads, IFGF_ROWS_MINB)
             raise_err(err, kErrPropCover);
             continue;
           }
-          const int pos = (int)(rwy & 0xffffu), cnt = (int)((rwy >> 16) & 0xffu);
-          const PropTiles::Ent* en = T.ent + (size_t)tl * P + pos;
+          const int r = (int)(rwy & 0xffffu), cnt = (int)((rwy >> 16) & 0xffu);
+          const double* rd = T.rdat + row_field(tl, P, 5 * R, r, 0);
           double ts[R], tt[R], tp[R];
 #pragma unroll
           for (int j = 0; j < R; ++j) {
             if (j < cnt) {
-              const double2 a = __ldg((const double2*)&en[j].ts);
-              ts[j] = a.x;
-              tt[j] = a.y;
-              tp[j] = __ldg(&en[j].tp);
+              ts[j] = __ldg(rd + 32 * (0 * R + j));
+              tt[j] = __ldg(rd + 32 * (1 * R + j));
+              tp[j] = __ldg(rd + 32 * (2 * R + j));
             } else {
               ts[j] = tt[j] = tp[j] = 0.0;
             }
           }
           double vr[R], vi[R];
           eval_block_multi<PS, PT, PP, R>(child + (size_t)cq * BL::Pst, ts, tt, tp, vr, vi);
+          const uint32_t nodes = __ldg(T.rnode + (size_t)tl * P + r);
 #pragma unroll
           for (int j = 0; j < R; ++j) {
             if (j < cnt) {
-              const double2 b = __ldg((const double2*)&en[j].tr);  // tr, ti
-              const int m = (int)__ldg(&en[j].node);
+              const double tr = __ldg(rd + 32 * (3 * R + j)), ti = __ldg(rd + 32 * (4 * R + j));
+              const int m = (int)((nodes >> (8 * j)) & 0xffu);
               double2 v = acc[m];
-              v.x = fma(vr[j], b.x, fma(-vi[j], b.y, v.x));
-              v.y = fma(vr[j], b.y, fma(vi[j], b.x, v.y));
+              v.x = fma(vr[j], tr, fma(-vi[j], ti, v.x));
+              v.y = fma(vr[j], ti, fma(vi[j], tr, v.y));
               acc[m] = v;
             }
           }
@@ -1155,9 +1162,10 @@ void build_prop_tiles(ifgf_plan* P, int d, void* (*scratch)(void*, size_t), void
   {
     size_t fr = 0, tot = 0;
     IFGF_CUDA(cudaMemGetInfo(&fr, &tot));
+    const double rows_bytes = (double)((K.P + 31) / 32 * 32) / K.P * 15.0 * sizeof(double);
     const double bytes = (double)ng * 8.0 * K.P *
-                         (sizeof(PropTiles::Ent) + 3 * sizeof(double) + sizeof(double2) +
-                          sizeof(uint32_t) + sizeof(uint2) + sizeof(uint16_t) + 1);
+                         (rows_bytes + 3 * sizeof(double) + sizeof(double2) +
+                          2 * sizeof(uint32_t) + sizeof(uint2) + sizeof(uint16_t) + 1);
     if (bytes > std::min(8.0 * (1ull << 30), 0.25 * (double)fr)) return;
   }
   T.ngamma = ng;
@@ -1185,12 +1193,14 @@ void build_prop_tiles(ifgf_plan* P, int d, void* (*scratch)(void*, size_t), void
   T.rw = P->alloc<uint2>(ne);
   T.fl_node = P->alloc<uint16_t>(ne);
   T.e_perm = P->alloc<uint8_t>(ne);
-  T.ent = P->alloc<PropTiles::Ent>(ne);
+  T.rdat = P->alloc<double>(row_field(ntiles, K.P, 5 * T.row_nodes, 0, 0));
+  T.rnode = P->alloc<uint32_t>(ne);
   {
     const unsigned g = nblk((size_t)ntiles * 32, 256);
     auto go = [&](auto kern) {
       kern<<<g, 256, 0, s>>>(ntiles, K.P, T.row_nodes, T.e_gc, T.e_t, T.e_T, T.rw_cnt, T.fl_cnt,
-                             T.rw, T.fl_node, T.e_perm, T.ent);
+                             T.rw, T.fl_node, T.e_perm, T.rdat,
+                             reinterpret_cast<uint8_t*>(T.rnode));
     };
     switch ((K.P + 31) / 32) {
       case 1: go(k_tile_sort<1>); break;
