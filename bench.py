@@ -357,24 +357,35 @@ def run_ours_dist(args):
     from paper_2112_15198_b200.dist import DistributedPlan
 
     rank, local, world = dist_env()
-    torch.cuda.set_device(local)
-    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    # IFGF_BENCH_BACKEND=gloo: functional check of this path with all ranks on
+    # the visible GPU(s) and host-staged exchanges -- not a performance number
+    backend = os.environ.get("IFGF_BENCH_BACKEND", "nccl")
+    dev_index = local if backend == "nccl" else local % torch.cuda.device_count()
+    torch.cuda.set_device(dev_index)
+    if backend == "nccl":
+        dist.init_process_group("nccl", device_id=torch.device("cuda", dev_index))
+    else:
+        dist.init_process_group(backend)
+    wire = torch.device("cuda", dev_index) if backend == "nccl" else torch.device("cpu")
     cfgd = ifgf.configs.CONFIGS[args.config]
     kcfg = ifgf.KernelConfig(ifgf.KernelKind(cfgd.kind), cfgd.kappa)
     n = cfgd.n
     pc = ifgf.generate(n, cfgd.shape, cfgd.c, cfgd.dens, cfgd.seed)
 
+    launches = [0]
+
     def step():
         dp = DistributedPlan(pc.x1, pc.x2, pc.x3, kcfg, ifgf.EngineParams(depth=cfgd.depth))
         out = dp.apply(pc.a_re, pc.a_im)
         vol = dp.ex.volume_blocks()
-        dp.plan.close()
+        launches[0] = int(dp.plan._info().launches)  # this rank's kernels in the step
+        dp.close()
         return out, vol
 
     for _ in range(args.warmup):
         step()
     times = []
-    with ClockSampler(local) as clocks:
+    with ClockSampler(dev_index) as clocks:
         for _ in range(args.steps):
             torch.cuda.synchronize()
             dist.barrier()
@@ -384,7 +395,7 @@ def run_ours_dist(args):
             e1.record()
             torch.cuda.synchronize()
             times.append(e0.elapsed_time(e1) / 1e3)
-    t = torch.tensor([statistics.mean(times)], device="cuda", dtype=torch.float64)
+    t = torch.tensor([statistics.mean(times)], device=wire, dtype=torch.float64)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     t_step = float(t.item())
     if rank == 0:
@@ -399,7 +410,7 @@ def run_ours_dist(args):
                        "step": "plan build (replicated) + distributed apply, host in/out"},
             "e2e": {"value": n / t_step / 1e6, "unit": UNIT, "h2d_bytes_per_step": 5 * n * 8,
                     "d2h_bytes_per_step": 2 * n * 8, "note": "the step is host-to-host"},
-            "gpu_launches": None, "roofline": None, "cpu_baseline": None,
+            "gpu_launches": launches[0], "roofline": None, "cpu_baseline": None,
             "clocks": clocks.summary(),
         }), flush=True)
     dist.destroy_process_group()

@@ -146,6 +146,7 @@ typedef struct ifgf_plan_info {
   double setup_seconds;
   size_t device_bytes;
   size_t setup_launches; /* our kernels launched by the plan's setup */
+  size_t launches;       /* our kernels launched by the plan so far (setup + passes) */
 } ifgf_plan_info;
 
 int ifgf_plan_get_info(const ifgf_plan* plan, ifgf_plan_info* info);

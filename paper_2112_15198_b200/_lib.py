@@ -40,7 +40,8 @@ class CPlanInfo(C.Structure):
                 ("nbr_entries", C.c_size_t * MAX_LEVELS),
                 ("cousin_entries", C.c_size_t * MAX_LEVELS), ("h", C.c_double * MAX_LEVELS),
                 ("setup_seconds", C.c_double), ("device_bytes", C.c_size_t),
-                ("setup_launches", C.c_size_t)]
+                ("setup_launches", C.c_size_t),
+                ("launches", C.c_size_t)]
 
 
 _dp = np.ctypeslib.ndpointer(dtype=np.float64, flags="C_CONTIGUOUS")

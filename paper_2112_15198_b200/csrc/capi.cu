@@ -607,6 +607,7 @@ int ifgf_plan_get_info(const ifgf_plan* P, ifgf_plan_info* info) {
     info->setup_seconds = P->setup_seconds;
     info->device_bytes = P->bytes;
     info->setup_launches = P->setup_launches;
+    info->launches = P->launches;
   });
 }
 

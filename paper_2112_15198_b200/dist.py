@@ -85,16 +85,60 @@ def build_exchange_plan(layout: Layout, depth: int, need) -> ExchangePlan:
     return ex
 
 
+def build_exchange_plan_rank(layout: Layout, depth: int, rank: int, need_self, group=None,
+                             device=None) -> ExchangePlan:
+    """This rank's rows of the exchange plan without computing anyone else's
+    needs: the rank computes its own foreign-cone sets (need_self(d, kind)),
+    tells every owner which of its cones it needs (one all-to-all of counts and
+    one of indices per level and kind) and learns what it must send.  Only
+    row `rank` of recv/send is filled."""
+    import torch
+    import torch.distributed as dist
+    R = layout.n_ranks
+    dev = device if device is not None else torch.device("cpu")
+    ex = ExchangePlan(depth, R)
+    empty = np.zeros(0, np.uint32)
+    for d in range(3, depth + 1):
+        for kind in (INTERP, PROP):
+            if kind == PROP and d < 4:
+                continue
+            cones = np.asarray(need_self(d, kind), dtype=np.uint32)
+            owner = layout.cone_owner(d, cones) if len(cones) else np.zeros(0, np.int64)
+            mine = [cones[owner == p] for p in range(R)]
+            if len(mine[rank]):
+                raise AssertionError("a rank never fetches its own cones")
+            cnt = torch.tensor([len(a) for a in mine], dtype=torch.int64, device=dev)
+            cnt_in = torch.empty_like(cnt)
+            dist.all_to_all_single(cnt_in, cnt, group=group)
+            sizes_out, sizes_in = cnt.tolist(), cnt_in.tolist()
+            flat = torch.as_tensor(np.concatenate(mine).astype(np.int64) if len(cones) else
+                                   np.zeros(0, np.int64), device=dev)
+            got = torch.empty(sum(sizes_in), dtype=torch.int64, device=dev)
+            dist.all_to_all_single(got, flat, sizes_in, sizes_out, group=group)
+            got = got.cpu().numpy().astype(np.uint32)
+            off = np.concatenate([[0], np.cumsum(sizes_in)])
+            recv = [[empty] * R for _ in range(R)]
+            send = [[empty] * R for _ in range(R)]
+            recv[rank] = mine
+            send[rank] = [got[off[p]:off[p + 1]] for p in range(R)]
+            ex.recv[(d, kind)] = recv
+            ex.send[(d, kind)] = send
+    return ex
+
+
 class TorchExchanger:
     """Moves blocks between ranks with torch.distributed batched P2P.
 
     `store` provides block_doubles (2 * Pst), pack(d, idx_tensor, buf) and
-    unpack(d, idx_tensor, buf) over tensors on `device`."""
+    unpack(d, idx_tensor, buf) over tensors on `device`.  With a backend that
+    moves host tensors only (gloo) the packed buffers are staged through host
+    memory (`wire` = cpu); with NCCL they travel device to device."""
 
-    def __init__(self, store, ex: ExchangePlan, rank: int, device, group=None):
+    def __init__(self, store, ex: ExchangePlan, rank: int, device, group=None, wire=None):
         import torch
         self.torch = torch
         self.store, self.ex, self.rank, self.device, self.group = store, ex, rank, device, group
+        self.wire = wire if wire is not None else device
         self._idx = {}
         for key in ex.recv:
             for p in range(ex.n_ranks):
@@ -119,10 +163,13 @@ class TorchExchanger:
             if si is not None:
                 buf = torch.empty(len(si) * bd, dtype=torch.float64, device=self.device)
                 self.store.pack(d, si, buf)
+                if self.wire != self.device:
+                    torch.cuda.synchronize()
+                    buf = buf.to(self.wire)
                 ops.append(dist.P2POp(dist.isend, buf, p, group=self.group))
             ri = self._idx.get((key, "recv", p))
             if ri is not None:
-                buf = torch.empty(len(ri) * bd, dtype=torch.float64, device=self.device)
+                buf = torch.empty(len(ri) * bd, dtype=torch.float64, device=self.wire)
                 recv_bufs.append((ri, buf))
                 ops.append(dist.P2POp(dist.irecv, buf, p, group=self.group))
         if ops:
@@ -130,7 +177,7 @@ class TorchExchanger:
                 w.wait()
         moved = 0
         for ri, buf in recv_bufs:
-            self.store.unpack(d, ri, buf)
+            self.store.unpack(d, ri, buf.to(self.device))
             moved += len(ri)
         return moved
 
@@ -184,7 +231,10 @@ def run_rank_share(plan, layout: Layout, rank: int, a_re, a_im, exchange):
 
 class DistributedPlan:
     """One plan per rank (this process's GPU); apply() returns the full
-    result in the caller's order on every rank."""
+    result in the caller's order on every rank.  Every rank builds the same
+    plan (setup is cheap on the GPU); each rank computes only its own
+    exchange sets and learns its send sets with one all-to-all per level and
+    kind (build_exchange_plan_rank)."""
 
     def __init__(self, x1, x2, x3, cfg, params=None, group=None):
         import torch
@@ -195,15 +245,19 @@ class DistributedPlan:
         self.rank = dist.get_rank(group)
         self.world = dist.get_world_size(group)
         self.device = torch.device("cuda", torch.cuda.current_device())
+        # NCCL moves device tensors; gloo (CPU tests, shared-GPU checks) host ones
+        self.wire = self.device if dist.get_backend(group) == "nccl" else torch.device("cpu")
         p = params or EngineParams()
         p.device = torch.cuda.current_device()
         self.plan = Plan(x1, x2, x3, cfg, p)
         self.layout = rank_layout(self.plan, self.world)
-        self.ex = build_exchange_plan(
-            self.layout, self.plan.depth,
-            lambda r, d, kind: self.plan.exchange_set(self.world, r, d, kind))
+        self.ex = build_exchange_plan_rank(
+            self.layout, self.plan.depth, self.rank,
+            lambda d, kind: self.plan.exchange_set(self.world, self.rank, d, kind),
+            group=group, device=self.wire)
         self.store = PlanStore(self.plan)
-        self.xch = TorchExchanger(self.store, self.ex, self.rank, self.device, group)
+        self.xch = TorchExchanger(self.store, self.ex, self.rank, self.device, group,
+                                  wire=self.wire)
         self.perm = self.plan.perm()
 
     def apply(self, a_re, a_im=None):
@@ -211,22 +265,25 @@ class DistributedPlan:
         a_im = np.zeros_like(a_re) if a_im is None else a_im
         part = run_rank_share(self.plan, self.layout, self.rank, a_re, a_im, self.xch.exchange)
         n = self.plan.n
-        pieces = torch.zeros((self.world, 2, int(np.max(np.diff(self.layout.point_begin)))),
-                             dtype=torch.float64, device=self.device)
-        mine = torch.zeros_like(pieces[0])
-        mine[0, :len(part[0])] = torch.as_tensor(part[0], device=self.device)
-        mine[1, :len(part[1])] = torch.as_tensor(part[1], device=self.device)
-        self.dist.all_gather_into_tensor(pieces, mine, group=self.group)
-        pieces = pieces.cpu().numpy()
+        m = int(np.max(np.diff(self.layout.point_begin)))
+        mine = torch.zeros((2, m), dtype=torch.float64, device=self.wire)
+        mine[0, :len(part[0])] = torch.as_tensor(part[0], device=self.wire)
+        mine[1, :len(part[1])] = torch.as_tensor(part[1], device=self.wire)
+        pieces = [torch.empty_like(mine) for _ in range(self.world)]
+        self.dist.all_gather(pieces, mine, group=self.group)
         s_re, s_im = np.zeros(n), np.zeros(n)
         for r in range(self.world):
             b, e = self.layout.points(r)
-            s_re[b:e] = pieces[r, 0, :e - b]
-            s_im[b:e] = pieces[r, 1, :e - b]
+            pr = pieces[r].cpu().numpy()
+            s_re[b:e] = pr[0, :e - b]
+            s_im[b:e] = pr[1, :e - b]
         i_re, i_im = np.zeros(n), np.zeros(n)
         i_re[self.perm] = s_re
         i_im[self.perm] = s_im
         return i_re, i_im
+
+    def close(self):
+        self.plan.close()
 
 
 def simulate(plans, a_re, a_im):

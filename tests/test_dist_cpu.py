@@ -140,3 +140,42 @@ def test_block_exchange_over_gloo_world2(oracle):
     assert all(ok for _, ok, _ in res), res
     total = sum(len(a) for lists in ex.recv.values() for row in lists for a in row)
     assert sum(m for _, _, m in res) == total
+
+
+def _plan_worker(rank, world, port, lay, depth, needs, out):
+    import torch.distributed as dist
+
+    from paper_2112_15198_b200.dist import build_exchange_plan_rank
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    ex = build_exchange_plan_rank(lay, depth, rank, lambda d, k: needs[rank][(d, k)])
+    out.put((rank, {k: ([a.tolist() for a in ex.recv[k][rank]],
+                        [a.tolist() for a in ex.send[k][rank]]) for k in ex.recv}))
+    dist.destroy_process_group()
+
+
+def test_rank_local_exchange_plan_over_gloo(oracle):
+    """build_exchange_plan_rank (own needs + all-to-all) gives every rank the
+    same rows as the full plan computed from everyone's needs."""
+    import torch.multiprocessing as mp
+    prob = _problem(oracle, n=5000, seed=47)
+    R = 2
+    lay, ex = _layout_and_plan(prob, R)
+    needs = [{k: np.concatenate(ex.recv[k][r]).astype(np.uint32) for k in ex.recv}
+             for r in range(R)]
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    ps = [ctx.Process(target=_plan_worker, args=(r, R, port, lay, prob.depth, needs, q))
+          for r in range(R)]
+    for p in ps:
+        p.start()
+    res = dict(q.get(timeout=120) for _ in ps)
+    for p in ps:
+        p.join(timeout=60)
+    for r in range(R):
+        for k in ex.recv:
+            recv, send = res[r][k]
+            assert recv == [a.tolist() for a in ex.recv[k][r]]
+            assert send == [a.tolist() for a in ex.send[k][r]]
