@@ -109,8 +109,15 @@ void ifgf_plan_destroy(ifgf_plan* plan);
  *                       (no precomputed geometry).
  *   Where the precomputed geometry is not built (too few parent cones per
  *   gamma, P > 255) TILES and DMMA run IFGF_PROP_NODE.
- *   All agree to rounding; DESIGN.md records their measured times. */
-enum { IFGF_OPT_SERIAL = 1, IFGF_OPT_PROP_KERNEL = 2 };
+ *   All agree to rounding; DESIGN.md records their measured times.
+ * IFGF_OPT_NEAR_KERNEL selects the near-field kernel:
+ *   IFGF_NEAR_POINT (0) thread per target point, neighbour sources in order;
+ *   IFGF_NEAR_BOX   (1, default) warp per target box, the box's neighbour
+ *                       sources staged in shared memory and split across
+ *                       lanes, several targets per pass.
+ *   Both agree to rounding. */
+enum { IFGF_OPT_SERIAL = 1, IFGF_OPT_PROP_KERNEL = 2, IFGF_OPT_NEAR_KERNEL = 3 };
+enum { IFGF_NEAR_POINT = 0, IFGF_NEAR_BOX = 1 };
 enum {
   IFGF_PROP_NODE = 0,
   IFGF_PROP_TILES = 1,

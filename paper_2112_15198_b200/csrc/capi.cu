@@ -17,6 +17,7 @@
 #include <cmath>
 #include <cstring>
 #include <memory>
+#include <mutex>
 #include <new>
 #include <random>
 #include <string>
@@ -114,6 +115,40 @@ InterpConsts make_consts(const ifgf_params* p) {
   return K;
 }
 
+// Streams are recycled per device instead of created per plan: blocks a plan
+// frees into the stream-ordered pool are reused without new physical
+// mappings only when the next plan allocates on the same stream (a fresh
+// stream per plan made the pool grow and remap: 20-80 ms setup spikes).
+struct StreamCache {
+  std::mutex mu;
+  std::vector<std::pair<int, cudaStream_t>> free;
+};
+StreamCache& stream_cache() {
+  static StreamCache* c = new StreamCache;  // leaked: streams outlive static destructors
+  return *c;
+}
+cudaStream_t take_stream(int device) {
+  {
+    StreamCache& c = stream_cache();
+    std::lock_guard<std::mutex> g(c.mu);
+    for (size_t k = c.free.size(); k-- > 0;)
+      if (c.free[k].first == device) {
+        cudaStream_t s = c.free[k].second;
+        c.free.erase(c.free.begin() + k);
+        return s;
+      }
+  }
+  cudaStream_t s = nullptr;
+  IFGF_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+  return s;
+}
+void give_stream(int device, cudaStream_t s) {
+  if (!s) return;
+  StreamCache& c = stream_cache();
+  std::lock_guard<std::mutex> g(c.mu);
+  c.free.emplace_back(device, s);
+}
+
 void plan_free(ifgf_plan* P) {
   if (!P) return;
   cudaSetDevice(P->device);
@@ -125,8 +160,10 @@ void plan_free(ifgf_plan* P) {
     else cudaFree(a);
   }
   if (P->s_main) cudaStreamSynchronize(P->s_main);
-  if (P->s_main) cudaStreamDestroy(P->s_main);
-  if (P->s_aux) cudaStreamDestroy(P->s_aux);
+  // aux first, main last: take_stream pops from the back, so the next plan
+  // gets this plan's main stream back as its main stream
+  give_stream(P->device, P->s_aux);
+  give_stream(P->device, P->s_main);
   delete P;
 }
 
@@ -146,9 +183,10 @@ ifgf_plan* new_plan(size_t n, int kind, double wavenumber, const ifgf_params* p)
   P->params = *p;
   P->K = make_consts(p);
   try {
-    IFGF_CUDA(cudaStreamCreateWithFlags(&P->s_main, cudaStreamNonBlocking));
-    IFGF_CUDA(cudaStreamCreateWithFlags(&P->s_aux, cudaStreamNonBlocking));
+    P->s_main = take_stream(P->device);
+    P->s_aux = take_stream(P->device);
     P->err = P->alloc<int>(1);
+    P->work_ctr = P->alloc<uint32_t>(ifgf_plan::kWorkCtrs);
     IFGF_CUDA(cudaMemsetAsync(P->err, 0, sizeof(int), P->s_main));
   } catch (...) {
     plan_free(P);
@@ -515,6 +553,10 @@ int ifgf_plan_set_option(ifgf_plan* P, int option, int value) {
       if (value < IFGF_PROP_NODE || value > IFGF_PROP_FLY)
         throw Error(IFGF_EINVAL, "unknown propagation kernel");
       P->prop_kernel = value;
+    } else if (option == IFGF_OPT_NEAR_KERNEL) {
+      if (value < IFGF_NEAR_POINT || value > IFGF_NEAR_BOX)
+        throw Error(IFGF_EINVAL, "unknown near-field kernel");
+      P->near_kernel = value;
     } else {
       throw Error(IFGF_EINVAL, "unknown option");
     }

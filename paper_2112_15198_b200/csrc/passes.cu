@@ -72,7 +72,7 @@ __global__ void __launch_bounds__(128) k_singular(const __grid_constant__ LevelD
       if (m == i) continue;
       const double dx = tx - __ldg(&xs[m]), dy = ty - __ldg(&ys[m]), dz = tz - __ldg(&zs[m]);
       const double r2 = fma(dz, dz, fma(dy, dy, dx * dx));
-      const double rinv = rsqrt(r2);
+      const double rinv = rsqrt_nr(r2);
       const double inv = kQuarterInvPi * rinv;
       const double a_r = __ldg(&ar[m]), a_i = __ldg(&ai[m]);
       if (LAP) {
@@ -89,6 +89,191 @@ __global__ void __launch_bounds__(128) k_singular(const __grid_constant__ LevelD
   }
   ir[i] += sr;
   ii[i] += si;
+}
+
+// K1, box form (default): warps of a persistent grid take target boxes of
+// level D from a work counter.  A box's neighbour sources (the same list for
+// every target of the box) are staged once in shared memory, in chunks of
+// CH, with the density pre-scaled by 1/(4 pi).  The lanes split the sources
+// (lane k takes sources k, k+32, ...) and each pass carries T = 4, 2 or 1
+// targets, so every staged source feeds T pairs and all 32 lanes stay busy
+// whatever the box population (the thread-per-target form runs 2-3 boxes per
+// warp with divergent neighbour loops).  The pair is branch-free: rsqrt_nr,
+// and e^{i kappa r} from sincos_tab.  Rounds that hold a self pair or tail
+// lanes take a masked copy of the body.  The T complex partial sums are
+// combined with a transposing butterfly and written by 2T lanes.  Sums run
+// in a fixed order, so results are bitwise reproducible; they differ from
+// the reference's sequential green_sum (kernels_scalar.cpp:12-30) by
+// rounding only.
+constexpr int kNearWarps = 4;
+
+// One near-field pair: (vr, vi) += q e^{i kappa r} / r for the offset
+// (dx, dy, dz); q carries the 1/(4 pi).  A skipped pair passes q = 0 with a
+// unit offset.  (Laplace: q / r.)
+template <bool LAP>
+__device__ __forceinline__ void near_pair(const double2* ptab, double dx, double dy, double dz,
+                                          double qr, double qi, double kappa, double& vr,
+                                          double& vi) {
+  const double r2 = fma(dz, dz, fma(dy, dy, dx * dx));
+  const double rinv = rsqrt_nr(r2);
+  const double br = qr * rinv, bi = qi * rinv;
+  if (LAP) {
+    vr += br;
+    vi += bi;
+  } else {
+    double sn, cs;
+    sincos_tab(ptab, kappa * (r2 * rinv), sn, cs);  // kappa carries kPhaseScale
+    vr = fma(br, cs, fma(-bi, sn, vr));
+    vi = fma(br, sn, fma(bi, cs, vi));
+  }
+}
+
+// Sum NV values per lane over the warp.  Each step halves the values a lane
+// carries (the half it keeps is picked by its lane bit), so NV values cost
+// NV - 1 + log2(32 / NV) shuffles instead of 5 NV.  On return lanes with
+// lane % (32 / NV) == 0 hold the sum of value `idx` in v[0].
+template <int NV>
+__device__ __forceinline__ void warp_transpose_sum(double* v, int lane, int& idx) {
+  idx = 0;
+#pragma unroll
+  for (int m = 16, h = NV / 2; h >= 1; m >>= 1, h >>= 1) {
+    const bool up = lane & m;
+#pragma unroll
+    for (int q = 0; q < h; ++q) {
+      const double send = up ? v[q] : v[q + h], keep = up ? v[q + h] : v[q];
+      v[q] = keep + __shfl_xor_sync(0xffffffffu, send, m);
+    }
+    if (up) idx += h;
+  }
+#pragma unroll
+  for (int m = 16 / NV; m >= 1; m >>= 1) v[0] += __shfl_xor_sync(0xffffffffu, v[0], m);
+}
+
+// One pass: targets t0 .. t0+T-1 of the box against the cn staged sources.
+template <bool LAP, int T>
+__device__ __forceinline__ void near_pass(const double* sx, const double* sy, const double* sz,
+                                          const double* sar, const double* sai,
+                                          const double2* ptab, uint32_t cn, uint32_t js0,
+                                          const double* __restrict__ xs,
+                                          const double* __restrict__ ys,
+                                          const double* __restrict__ zs, size_t t0,
+                                          double kappa, int lane, double* ir, double* ii) {
+  double tx[T], ty[T], tz[T], v[2 * T];
+#pragma unroll
+  for (int u = 0; u < T; ++u) {
+    tx[u] = xs[t0 + u];
+    ty[u] = ys[t0 + u];
+    tz[u] = zs[t0 + u];
+    v[2 * u] = 0.0;
+    v[2 * u + 1] = 0.0;
+  }
+  for (uint32_t kb = 0; kb < cn; kb += 32) {
+    const uint32_t k = kb + lane;
+    const bool valid = k < cn;
+    const uint32_t kk = valid ? k : cn - 1;
+    const double px = sx[kk], py = sy[kk], pz = sz[kk], qr = sar[kk], qi = sai[kk];
+    // own slot of target u in this chunk is js0 + u (wrapped when outside)
+    const bool hit = !valid || (k - js0 < (uint32_t)T);
+    if (!__any_sync(0xffffffffu, hit)) {
+#pragma unroll
+      for (int u = 0; u < T; ++u)
+        near_pair<LAP>(ptab, tx[u] - px, ty[u] - py, tz[u] - pz, qr, qi, kappa, v[2 * u],
+                       v[2 * u + 1]);
+    } else {
+#pragma unroll
+      for (int u = 0; u < T; ++u) {
+        const bool skip = !valid || k == js0 + u;
+        near_pair<LAP>(ptab, skip ? 1.0 : tx[u] - px, ty[u] - py, tz[u] - pz, skip ? 0.0 : qr,
+                       skip ? 0.0 : qi, kappa, v[2 * u], v[2 * u + 1]);
+      }
+    }
+  }
+  int idx;
+  warp_transpose_sum<2 * T>(v, lane, idx);
+  if ((lane & (16 / T - 1)) == 0) {
+    const size_t i = t0 + (idx >> 1);
+    (idx & 1 ? ii : ir)[i] += v[0];
+  }
+}
+
+template <bool LAP, int CH>
+__global__ void __launch_bounds__(kNearWarps * 32)
+    k_near_box(const __grid_constant__ LevelDev L, const double2* __restrict__ phase,
+               const double* __restrict__ xs, const double* __restrict__ ys,
+               const double* __restrict__ zs, const double* __restrict__ ar,
+               const double* __restrict__ ai, double kappa, size_t b0, size_t e0, double* ir,
+               double* ii, uint32_t* ctr) {
+  extern __shared__ double nsm[];
+  __shared__ double2 ptab[kPhaseEntries];
+  constexpr unsigned FULL = 0xffffffffu;
+  for (int k = threadIdx.x; k < kPhaseEntries; k += blockDim.x) ptab[k] = phase[k];
+  __syncthreads();
+  kappa *= kPhaseScale;  // sincos_tab takes the phase in units of pi/256
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  double* sx = nsm + (size_t)w * 5 * CH;
+  double* sy = sx + CH;
+  double* sz = sy + CH;
+  double* sar = sz + CH;
+  double* sai = sar + CH;
+  for (;;) {
+    uint32_t b = 0;
+    if (lane == 0) b = atomicAdd(ctr, 1u);
+    b = __shfl_sync(FULL, b, 0);
+    if (b >= L.nb) break;
+    const size_t tf = L.first[b];
+    const size_t lo = max(tf, b0), hi = min(tf + L.count[b], e0);
+    if (lo >= hi) continue;
+    // neighbour segments (ascending, own box included): lane a holds segment a
+    const uint32_t nn = L.nbr_cnt[b];
+    uint32_t o = 0, f = 0, c = 0;
+    if (lane < (int)nn) {
+      o = L.nbr[(size_t)b * 27 + lane];
+      f = L.first[o];
+      c = L.count[o];
+    }
+    uint32_t inc = c;
+#pragma unroll
+    for (int k = 1; k < 32; k <<= 1) {
+      const uint32_t v = __shfl_up_sync(FULL, inc, k);
+      if (lane >= k) inc += v;
+    }
+    const uint32_t off = inc - c;
+    const uint32_t S = __shfl_sync(FULL, inc, 31);
+    const unsigned selfm = __ballot_sync(FULL, lane < (int)nn && o == b);
+    const uint32_t self_off = __shfl_sync(FULL, off, __ffs(selfm) - 1);
+    for (uint32_t cs = 0; cs < S; cs += CH) {
+      const uint32_t cn = min((uint32_t)CH, S - cs);
+      __syncwarp();
+      for (uint32_t a = 0; a < nn; ++a) {
+        const uint32_t oa = __shfl_sync(FULL, off, a), ca = __shfl_sync(FULL, c, a),
+                       fa = __shfl_sync(FULL, f, a);
+        const uint32_t jl = max(oa, cs), jh = min(oa + ca, cs + cn);
+        for (uint32_t j = jl + lane; j < jh; j += 32) {
+          const uint32_t m = fa + (j - oa), k = j - cs;
+          sx[k] = __ldg(&xs[m]);
+          sy[k] = __ldg(&ys[m]);
+          sz[k] = __ldg(&zs[m]);
+          sar[k] = kQuarterInvPi * __ldg(&ar[m]);
+          sai[k] = kQuarterInvPi * __ldg(&ai[m]);
+        }
+      }
+      __syncwarp();
+      // own slot of target t in this chunk: self_off + (t - tf) - cs
+      const uint32_t jbase = self_off - (uint32_t)tf - cs;
+      size_t t0 = lo;
+      for (; t0 + 4 <= hi; t0 += 4)
+        near_pass<LAP, 4>(sx, sy, sz, sar, sai, ptab, cn, jbase + (uint32_t)t0, xs, ys, zs, t0,
+                          kappa, lane, ir, ii);
+      if (t0 + 2 <= hi) {
+        near_pass<LAP, 2>(sx, sy, sz, sar, sai, ptab, cn, jbase + (uint32_t)t0, xs, ys, zs, t0,
+                          kappa, lane, ir, ii);
+        t0 += 2;
+      }
+      if (t0 < hi)
+        near_pass<LAP, 1>(sx, sy, sz, sar, sai, ptab, cn, jbase + (uint32_t)t0, xs, ys, zs, t0,
+                          kappa, lane, ir, ii);
+    }
+  }
 }
 
 // ------------------------------------------------------- K2 level-D seeding
@@ -383,9 +568,43 @@ void launch_scatter_result(ifgf_plan* P, double* o_re, double* o_im, cudaStream_
   ++P->launches;
 }
 
+template <bool LAP, int CH>
+void launch_near_box(ifgf_plan* P, const Level& L, size_t b, size_t e, cudaStream_t s) {
+  const size_t smem = (size_t)kNearWarps * 5 * CH * sizeof(double);
+  static int ctas_per_sm = 0;  // per instantiation
+  if (!ctas_per_sm) {
+    IFGF_CUDA(cudaFuncSetAttribute(k_near_box<LAP, CH>,
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    IFGF_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ctas_per_sm, k_near_box<LAP, CH>,
+                                                            kNearWarps * 32, smem));
+    ctas_per_sm = std::max(ctas_per_sm, 1);
+  }
+  int sms = 0;
+  IFGF_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, P->device));
+  const unsigned grid =
+      std::min<unsigned>(blocks_for(L.nb, kNearWarps), (unsigned)(sms * ctas_per_sm));
+  uint32_t* ctr = P->work_ctr + ifgf_plan::kCtrNear;
+  IFGF_CUDA(cudaMemsetAsync(ctr, 0, sizeof(uint32_t), s));
+  k_near_box<LAP, CH><<<grid, kNearWarps * 32, smem, s>>>(
+      L.dev(), P->phase, P->xs, P->ys, P->zs, P->ar, P->ai, P->kappa, b, e, P->ir, P->ii, ctr);
+}
+
+#ifndef IFGF_NEAR_CHUNK
+#define IFGF_NEAR_CHUNK 192
+#endif
+
 void launch_singular(ifgf_plan* P, size_t b, size_t e, cudaStream_t s) {
   if (e <= b) return;
   const Level& L = P->lv[P->depth];
+  // the box form needs populated leaves: below ~12 points per box (Laplace
+  // depth rule, C3) its per-box staging and reductions cost more than the
+  // divergence they remove
+  if (P->near_kernel == IFGF_NEAR_BOX && P->n >= 12 * (size_t)L.nb) {
+    if (P->kappa == 0.0) launch_near_box<true, IFGF_NEAR_CHUNK>(P, L, b, e, s);
+    else launch_near_box<false, IFGF_NEAR_CHUNK>(P, L, b, e, s);
+    ++P->launches;
+    return;
+  }
   const unsigned g = blocks_for(e - b, 128);
   if (P->kappa == 0.0)
     k_singular<true><<<g, 128, 0, s>>>(L.dev(), L.ptbox, P->xs, P->ys, P->zs, P->ar, P->ai,

@@ -165,6 +165,9 @@ struct ifgf_plan {
   double *ar = nullptr, *ai = nullptr;                 // sorted densities
   double *ir = nullptr, *ii = nullptr;                 // sorted results
   int* err = nullptr;
+  const double2* phase = nullptr;  // sincos_tab table (kPhaseEntries), after the trig table
+  uint32_t* work_ctr = nullptr;    // persistent-kernel work counters (kWorkCtrs)
+  static constexpr int kCtrNear = 0, kWorkCtrs = 4;
   ifgf_b200::Level lv[IFGF_MAX_LEVELS];
   double2* stage_blocks[IFGF_MAX_LEVELS] = {};  // pass-level API storage
   double2* slots[IFGF_MAX_LEVELS] = {};         // apply rotation
@@ -177,6 +180,7 @@ struct ifgf_plan {
   size_t launches = 0;  // kernels launched by this plan since the last reset
   bool serial = false;  // IFGF_OPT_SERIAL
   int prop_kernel = IFGF_PROP_ROWS;  // IFGF_OPT_PROP_KERNEL
+  int near_kernel = IFGF_NEAR_BOX;   // IFGF_OPT_NEAR_KERNEL
   size_t setup_launches = 0;
 
   template <class T>

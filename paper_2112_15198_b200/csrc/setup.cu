@@ -513,10 +513,18 @@ void build_plan(ifgf_plan* P, const double* d_x, const double* d_y, const double
       const double a = (double)k * kTrigHTheta;
       trig[kTrigPhi + k] = make_double2(std::cos(a), std::sin(a));
     }
+    // phase table for sincos_tab: {cos, sin}(k 2 pi / kPhaseEntries), rounded
+    // from long double
+    for (int k = 0; k < kPhaseEntries; ++k) {
+      const long double a =
+          (long double)k * 6.28318530717958647692528676655900577L / (long double)kPhaseEntries;
+      trig.push_back(make_double2((double)cosl(a), (double)sinl(a)));
+    }
     double2* d_trig = P->alloc<double2>(trig.size());
     IFGF_CUDA(cudaMemcpyAsync(d_trig, trig.data(), trig.size() * sizeof(double2),
                               cudaMemcpyHostToDevice, s));
     for (int d = 0; d < IFGF_MAX_LEVELS; ++d) P->lv[d].trig = d_trig;
+    P->phase = d_trig + kTrigEntries;
     IFGF_CUDA(cudaStreamSynchronize(s));  // trig lives on the stack until copied
   }
   {

@@ -288,13 +288,19 @@ class Plan:
 
     PROP_NODE, PROP_TILES, PROP_DMMA, PROP_ROWS, PROP_FLY = 0, 1, 2, 3, 4
 
+    NEAR_POINT, NEAR_BOX = 0, 1
+
     def set_option(self, option: int, value: int):
         """IFGF_OPT_* (include/ifgf_b200.h): 1 serial streams, 2 propagation
-        kernel (PROP_NODE, PROP_TILES, PROP_DMMA, PROP_ROWS default, PROP_FLY)."""
+        kernel (PROP_NODE, PROP_TILES, PROP_DMMA, PROP_ROWS default, PROP_FLY),
+        3 near-field kernel (NEAR_POINT, NEAR_BOX default)."""
         check(lib.ifgf_plan_set_option(self._h, option, value))
 
     def set_prop_kernel(self, kind: int):
         self.set_option(2, kind)
+
+    def set_near_kernel(self, kind: int):
+        self.set_option(3, kind)
 
     def _info(self) -> _lib.CPlanInfo:
         info = _lib.CPlanInfo()
