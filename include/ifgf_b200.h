@@ -106,7 +106,13 @@ void ifgf_plan_destroy(ifgf_plan* plan);
  *                       geometry, one block load per row; levels without
  *                       the precomputed geometry run IFGF_PROP_FLY;
  *   IFGF_PROP_FLY   (4) the same rows grouped per parent cone on the fly
- *                       (no precomputed geometry).
+ *                       (no precomputed geometry);
+ *   IFGF_PROP_STREAM(5) the precomputed rows evaluated with the
+ *                       child block held in registers (one s-plane per
+ *                       lane of a 3-lane group) while the nodes of a run
+ *                       of rows sharing the child cone stream past; orders
+ *                       whose planes do not fit in registers run ROWS,
+ *                       levels without the precomputed geometry run FLY.
  *   Where the precomputed geometry is not built (too few parent cones per
  *   gamma, P > 255) TILES and DMMA run IFGF_PROP_NODE.
  *   All agree to rounding; DESIGN.md records their measured times.
@@ -123,7 +129,8 @@ enum {
   IFGF_PROP_TILES = 1,
   IFGF_PROP_DMMA = 2,
   IFGF_PROP_ROWS = 3,
-  IFGF_PROP_FLY = 4
+  IFGF_PROP_FLY = 4,
+  IFGF_PROP_STREAM = 5
 };
 int ifgf_plan_set_option(ifgf_plan* plan, int option, int value);
 

@@ -287,6 +287,12 @@ __global__ void __launch_bounds__(320)
   extern __shared__ double2 smem[];
   double2* sv = smem;
   double2* st = smem + cpb * P;
+  double2* ptab = st + cpb * P;  // sincos_tab phase table
+  if (!LAP) {
+    for (int k = threadIdx.x; k < kPhaseEntries; k += blockDim.x) ptab[k] = L.trig[kTrigEntries + k];
+    __syncthreads();
+  }
+  const double ks = kappa * kPhaseScale;
   const uint32_t q0 = qb + blockIdx.x * cpb;
   const int ncon = (int)min((uint32_t)cpb, qe - q0);
   const int c = threadIdx.x / P, m = threadIdx.x % P;
@@ -305,7 +311,7 @@ __global__ void __launch_bounds__(320)
     for (uint32_t j = f; j < e; ++j) {
       const double dx = tx - __ldg(&xs[j]), dy = ty - __ldg(&ys[j]), dz = tz - __ldg(&zs[j]);
       const double r2 = fma(dz, dz, fma(dy, dy, dx * dx));
-      const double rinv = rsqrt(r2);
+      const double rinv = rsqrt_nr(r2);
       const double ratio = rc * rinv;
       const double a_r = __ldg(&ar[j]), a_i = __ldg(&ai[j]);
       if (LAP) {
@@ -313,7 +319,7 @@ __global__ void __launch_bounds__(320)
         si = fma(a_i, ratio, si);
       } else {
         double sn, cs;
-        sincos_fast(kappa * (r2 * rinv - rc), sn, cs);
+        sincos_tab(ptab, ks * (r2 * rinv - rc), sn, cs);
         const double gr = cs * ratio, gi = sn * ratio;
         sr = fma(a_r, gr, fma(-a_i, gi, sr));
         si = fma(a_r, gi, fma(a_i, gr, si));
@@ -345,7 +351,7 @@ __global__ void __launch_bounds__(320, IFGF_PROP_MINB)
   const int c = threadIdx.x / P, m = threadIdx.x % P;
   const int jp = m % PP, jt = (m / PP) % PT, js = m / (PP * PT);
   for (int g = 0; g < groups; ++g) {
-    const uint32_t q0 = qb + ((uint32_t)blockIdx.x * groups + g) * cpb;
+    const uint32_t q0 = qb + ((uint32_t)g * gridDim.x + blockIdx.x) * cpb;
     if (q0 >= qe) break;
     const int ncon = (int)min((uint32_t)cpb, qe - q0);
     if (c < ncon) {
@@ -410,8 +416,12 @@ __global__ void __launch_bounds__(128, IFGF_INTERP_MINB)
              int* err) {
   using BL = BlockLayout<PS, PT, PP>;
   __shared__ double2 trig[kTrigEntries];
+  __shared__ double2 ptab[LAP ? 1 : kPhaseEntries];
   stage_trig(trig, L.trig);
+  if (!LAP)
+    for (int k = threadIdx.x; k < kPhaseEntries; k += blockDim.x) ptab[k] = L.trig[kTrigEntries + k];
   __syncthreads();
+  const double ks = kappa * kPhaseScale;
   const size_t t = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
   if (t >= *nchunk) return;
   const uint2 ch = chunk[t];
@@ -492,7 +502,7 @@ __global__ void __launch_bounds__(128, IFGF_INTERP_MINB)
         aci[j] = fma(vi[j], inv, aci[j]);
       } else {
         double sn, cn;
-        sincos_fast(kappa * o[j].r, sn, cn);
+        sincos_tab(ptab, ks * o[j].r, sn, cn);
         const double gr = cn * inv, gi = sn * inv;
         acr[j] = fma(vr[j], gr, fma(-vi[j], gi, acr[j]));
         aci[j] = fma(vr[j], gi, fma(vi[j], gr, aci[j]));
@@ -623,7 +633,7 @@ void launch_level_d(ifgf_plan* P, uint32_t qb, uint32_t qe, double2* out, cudaSt
     using O = decltype(o);
     const int cpb = cones_per_cta(O::P);
     const unsigned grid = blocks_for(qe - qb, cpb);
-    const size_t smem = 2 * (size_t)cpb * O::P * sizeof(double2);
+    const size_t smem = (2 * (size_t)cpb * O::P + kPhaseEntries) * sizeof(double2);
     if (P->kappa == 0.0)
       k_level_d<O::PS, O::PT, O::PP, true><<<grid, threads_for(cpb, O::P), smem, s>>>(
           L.dev(), K, P->xs, P->ys, P->zs, P->ar, P->ai, P->kappa, qb, qe, cpb, out, P->err);

@@ -142,11 +142,11 @@ __global__ void k_tile_entries(const __grid_constant__ LevelDev U, const __grid_
   // fast locate relative to the child centre; flag anything near a boundary
   const double dx = x - ox, dy = y - oy, dz = z - oz;
   const double rho2 = fma(dy, dy, dx * dx), r2 = fma(dz, dz, rho2);
-  const double rinv = rsqrt(r2), s = L.rad * rinv, rho_inv = rsqrt(rho2);
+  const double rinv = rsqrt_nr(r2), s = L.rad * rinv, rho_inv = rsqrt_nr(rho2);
   double theta, phi;
   fast_angles(trig, dx, dy, dz, rho2 * rho_inv, rinv, rho_inv, theta, phi);
   const double fs = s * L.iw0, ft = theta * L.iw1, fp = phi * L.iw2;
-  const bool flag = !(rho2 > 0.0) || s > kSMaxTol * (1.0 - 1e-12) || near_boundary(fs) ||
+  const bool flag = !(rho2 > 1e-300) || s > kSMaxTol * (1.0 - 1e-12) || near_boundary(fs) ||
                     near_boundary(ft) || near_boundary(fp);
   int is = (int)fs, it = (int)ft, ip = (int)fp;
   is = is < L.n0 - 1 ? is : L.n0 - 1;
@@ -654,7 +654,7 @@ __global__ void __launch_bounds__(320, 2)
   __shared__ int kmax_s;
   const int c = threadIdx.x / P, j = threadIdx.x % P;
   for (int g = 0; g < groups; ++g) {
-    const uint32_t q0 = qb + ((uint32_t)blockIdx.x * groups + g) * cpb;
+    const uint32_t q0 = qb + ((uint32_t)g * gridDim.x + blockIdx.x) * cpb;
     if (q0 >= qe) break;
     const int ncon = (int)min((uint32_t)cpb, qe - q0);
     if (threadIdx.x < cpb) {
@@ -775,7 +775,7 @@ __global__ void __launch_bounds__(kRowThreads, IFGF_ROWS_MINB)
   double2* st = sv + cpw * P;
   uint2* meta = reinterpret_cast<uint2*>(st + cpw * P);
   for (int g = 0; g < groups; ++g) {
-    const uint32_t q0 = qb + (((uint32_t)blockIdx.x * groups + g) * NW + w) * cpw;
+    const uint32_t q0 = qb + (((uint32_t)g * gridDim.x + blockIdx.x) * NW + w) * cpw;
     if (q0 >= qe) break;
     const int nw = (int)min((uint32_t)cpw, qe - q0);
     for (int i = lane; i < nw * P; i += 32) sv[i] = make_double2(0.0, 0.0);
@@ -918,6 +918,283 @@ __global__ void __launch_bounds__(kRowThreads, IFGF_ROWS_MINB)
           v.y = fma(vr, ti, fma(vi, tr, v.y));
           acc[m] = v;
         }
+      }
+      __syncwarp();
+    }
+    fit_cones_warp<PS, PT, PP>(sM, sv, st, nw, parent + (size_t)q0 * BL::Pst, err);
+    __syncwarp();
+  }
+}
+
+// K3 streaming (default where the orders allow it): the child block stays in
+// registers while the nodes that fall into it stream past.  A child cone of
+// a parent box collects ~25 nodes of each parent cone (the child's cone
+// grid is 2x coarser per axis), so a block loaded once serves a whole run
+// of rows instead of one row of <= 3 nodes: the rows kernel moves 1,248 B
+// from L1 into registers for every 3 evaluations and saturates the L1 data
+// path at ~35 % of the FP64 pipe.
+//
+// Warp = cpw parent cones, children in Morton order.  Lanes 0..29 form ten
+// groups of PS = 3; lane a of a group holds s-plane a of the current child
+// block (PT*PP complex coefficients in registers).  A child round's rows
+// (the tiles' rows of every owned cone, in cone then row order) are
+// concatenated and their nodes split evenly over the groups; a group walks
+// its node span, reloading its plane only where the child cone changes.
+// Per node every lane of the group contracts its plane (phi then theta),
+// weights it by T_a(ts), and the three partials are summed on the group's
+// first lane ((a0 + a1) + a2), which applies the transfer factor and adds
+// the contribution to the node's slot in shared memory.  Each slot gets one
+// contribution per child, children in order: deterministic sums.  Flagged
+// nodes (exact per-box path) follow each round, one lane each.
+// Node record of a streaming round (48 B): local coordinates, transfer
+// factor, child cone ordinal, accumulator slot (cone * P + node).
+struct SNode {
+  double t[3];
+  double tr, ti;
+  uint32_t cq, slot;
+};
+// shared memory per warp and owned parent cone, in double2 units of P:
+// sv + st (P each) + P node records (3 double2 each)
+constexpr int kStreamSmem = 5;
+
+template <int PS, int PT, int PP>
+struct StreamShape {
+  static constexpr int NG = 32 / PS;              // lane groups per warp
+  static constexpr int NR = PT * PP;              // complex coefficients per plane
+  static constexpr bool ok = PS <= 4 && NR <= 25;  // plane fits in registers
+};
+
+template <int PS, int PT, int PP, bool LAP, int R>
+__global__ void __launch_bounds__(kRowThreads, IFGF_ROWS_MINB)
+    k_propagate_stream(const __grid_constant__ LevelDev U, const __grid_constant__ LevelDev L,
+                       const __grid_constant__ InterpConsts K, const TilesDev T, double kappa,
+                       uint32_t qb, uint32_t qe, int cpw, int groups,
+                       const double2* __restrict__ child, double2* parent, int* err) {
+  using BL = BlockLayout<PS, PT, PP>;
+  using SS = StreamShape<PS, PT, PP>;
+  constexpr int P = PS * PT * PP;
+  constexpr int NW = kRowThreads / 32;
+  constexpr int NR = SS::NR;
+  constexpr unsigned FULL = 0xffffffffu;
+  extern __shared__ double2 smem[];
+  __shared__ uint32_t s_cb0[NW][kRowMaxCpw], s_tile[NW][kRowMaxCpw], s_nrow[NW][kRowMaxCpw],
+      s_nfl[NW][kRowMaxCpw], s_pre[NW][kRowMaxCpw + 1], s_fpre[NW][kRowMaxCpw + 1];
+  __shared__ double sM[PP * PP + PT * PT + PS * PS];
+  stage_fit_matrices<PS, PT, PP>(K, sM);
+  __syncthreads();
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int grp = lane / PS, pa = lane - grp * PS;  // group, plane
+  const int lead = grp * PS;
+  const bool in_grp = grp < SS::NG;
+  double2* sv = smem + (size_t)w * kStreamSmem * cpw * P;
+  double2* st = sv + cpw * P;
+  SNode* nd = reinterpret_cast<SNode*>(st + cpw * P);  // the round's nodes
+  for (int g = 0; g < groups; ++g) {
+    const uint32_t q0 = qb + (((uint32_t)g * gridDim.x + blockIdx.x) * NW + w) * cpw;
+    if (q0 >= qe) break;
+    const int nw = (int)min((uint32_t)cpw, qe - q0);
+    for (int i = lane; i < nw * P; i += 32) sv[i] = make_double2(0.0, 0.0);
+    uint32_t cb0 = 0, nch = 0, tbase = 0;
+    if (lane < nw) {
+      const uint32_t q = q0 + lane;
+      const uint32_t pb = U.cone_box[q];
+      cb0 = U.child_begin[pb];
+      nch = U.child_begin[pb + 1] - cb0;
+      tbase = T.cone_gidx[q] * 8;
+    }
+    if (lane < cpw) s_cb0[w][lane] = cb0;
+    uint32_t kmax = nch;
+#pragma unroll
+    for (int o = 16; o; o >>= 1) kmax = max(kmax, __shfl_xor_sync(FULL, kmax, o));
+    for (uint32_t kc = 0; kc < kmax; ++kc) {  // k-th child, ascending Morton order
+      uint32_t nrow = 0, nfl = 0, tile = 0;
+      if (lane < nw && kc < nch) {
+        const uint32_t cb = cb0 + kc;
+        tile = tbase + (uint32_t)(L.code[cb] & 7);
+        nrow = T.rw_cnt[tile];
+        nfl = T.fl_cnt[tile];
+      }
+      uint32_t incl = nrow, fincl = nfl;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t v = __shfl_up_sync(FULL, incl, o), f = __shfl_up_sync(FULL, fincl, o);
+        if (lane >= o) {
+          incl += v;
+          fincl += f;
+        }
+      }
+      const uint32_t rtot = __shfl_sync(FULL, incl, 31), ftot = __shfl_sync(FULL, fincl, 31);
+      __syncwarp();  // previous round's readers of s_* / meta are done
+      if (lane < cpw) {
+        s_tile[w][lane] = tile;
+        s_nrow[w][lane] = nrow;
+        s_nfl[w][lane] = nfl;
+        s_pre[w][lane + 1] = incl;
+        s_fpre[w][lane + 1] = fincl;
+      }
+      if (lane == 0) s_pre[w][0] = s_fpre[w][0] = 0;
+      __syncwarp();
+      // phase A: rows -> per-node records in shared memory, node order
+      // (lanes = rows: coalesced reads of the tiles' 32-row SoA chunks)
+      uint32_t carry = 0;
+      for (uint32_t t0 = 0; t0 < rtot; t0 += 32) {
+        const uint32_t t = t0 + lane;
+        uint32_t cnt = 0, c = 0, loc = 0, tl = 0;
+        uint2 rw = make_uint2(0, 0);
+        if (t < rtot) {
+          while (s_pre[w][c + 1] <= t) ++c;
+          tl = s_tile[w][c];
+          loc = t - s_pre[w][c];
+          rw = T.rw[(size_t)tl * P + loc];
+          cnt = (rw.y >> 16) & 0xffu;
+        }
+        uint32_t ci = cnt;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const uint32_t v = __shfl_up_sync(FULL, ci, o);
+          if (lane >= o) ci += v;
+        }
+        if (t < rtot) {
+          const uint32_t n0 = carry + ci - cnt;
+          const uint32_t cq = find_cone(L, s_cb0[w][c] + kc, rw.x);
+          const double* rd = T.rdat + row_field(tl, P, 5 * R, (int)loc, 0);
+          const uint32_t nodes = __ldg(T.rnode + (size_t)tl * P + loc);
+#pragma unroll
+          for (int j = 0; j < R; ++j)
+            if (j < (int)cnt) {
+              SNode& sn = nd[n0 + j];
+              sn.t[0] = __ldg(rd + 32 * (0 * R + j));
+              sn.t[1] = __ldg(rd + 32 * (1 * R + j));
+              sn.t[2] = __ldg(rd + 32 * (2 * R + j));
+              sn.tr = __ldg(rd + 32 * (3 * R + j));
+              sn.ti = __ldg(rd + 32 * (4 * R + j));
+              sn.cq = cq;
+              sn.slot = c * P + ((nodes >> (8 * j)) & 0xffu);
+            }
+        }
+        carry += __shfl_sync(FULL, ci, 31);
+      }
+      __syncwarp();
+      // phase B: the groups split the round's nodes evenly
+      const uint32_t ntot = carry;
+      const uint32_t per = (ntot + SS::NG - 1) / SS::NG;
+      const uint32_t n_lo = in_grp ? min(ntot, (uint32_t)grp * per) : ntot;
+      const uint32_t n_hi = in_grp ? min(ntot, n_lo + per) : ntot;
+      uint32_t cur = kNone;  // child cone ordinal held in registers
+      double pr[NR], pi[NR];
+      for (uint32_t it = 0; it < per; ++it) {
+        const uint32_t n = n_lo + it;
+        const bool act = n < n_hi;
+        const SNode* sn = nd + (act ? n : 0);
+        const uint32_t cq = act ? sn->cq : kNone;
+        if (act && cq == kNone && pa == 0) raise_err(err, kErrPropCover);
+        const bool ev = act && cq != kNone;
+        if (ev && cq != cur) {  // load plane pa of the child block
+          const double2* plane = child + (size_t)cq * BL::Pst + pa * BL::PL;
+#pragma unroll
+          for (int q = 0; q < BL::PL / 2; ++q) {
+            const double4 v = ldg256(plane + 2 * q);
+            if (2 * q < NR) {
+              pr[2 * q] = v.x;
+              pi[2 * q] = v.y;
+            }
+            if (2 * q + 1 < NR) {
+              pr[2 * q + 1] = v.z;
+              pi[2 * q + 1] = v.w;
+            }
+          }
+          cur = cq;
+        }
+        double vr = 0.0, vi = 0.0;
+        if (ev) {
+          const double ts = sn->t[0], tt = sn->t[1], tp = sn->t[2];
+          double Tt[PT], Tp[PP];
+          cheb_basis<PT>(tt, Tt);
+          cheb_basis<PP>(tp, Tp);
+          double cr = 0.0, ci = 0.0;
+#pragma unroll
+          for (int b = 0; b < PT; ++b) {
+            double rr = pr[b * PP], ri = pi[b * PP];
+#pragma unroll
+            for (int k = 1; k < PP; ++k) {
+              rr = fma(pr[b * PP + k], Tp[k], rr);
+              ri = fma(pi[b * PP + k], Tp[k], ri);
+            }
+            if (b == 0) {
+              cr = rr;
+              ci = ri;
+            } else {
+              cr = fma(rr, Tt[b], cr);
+              ci = fma(ri, Tt[b], ci);
+            }
+          }
+          // T_a(ts), the reference's recurrence
+          double Ta = 1.0, Tm = 1.0;
+#pragma unroll
+          for (int k = 1; k < PS; ++k) {
+            const double Tn = k == 1 ? ts : fma(2.0 * ts, Ta, -Tm);
+            Tm = Ta;
+            Ta = k <= pa ? Tn : Ta;
+          }
+          vr = cr * Ta;
+          vi = ci * Ta;
+        }
+        // group sum on the first lane: ((a0 + a1) + a2)
+#pragma unroll
+        for (int k = 1; k < PS; ++k) {
+          const int src = min(lead + k, 31);
+          const double ur = __shfl_sync(FULL, vr, src), ui = __shfl_sync(FULL, vi, src);
+          if (pa == 0) {
+            vr += ur;
+            vi += ui;
+          }
+        }
+        if (ev && pa == 0) {
+          const double tr = sn->tr, ti = sn->ti;
+          double2* acc = sv + sn->slot;
+          double2 v = *acc;
+          v.x = fma(vr, tr, fma(-vi, ti, v.x));
+          v.y = fma(vr, ti, fma(vi, tr, v.y));
+          *acc = v;
+        }
+      }
+      // flagged nodes: the exact per-box path, one lane each
+      for (uint32_t f = lane; f < ftot; f += 32) {
+        int c = 0;
+        while (s_fpre[w][c + 1] <= f) ++c;
+        const uint32_t tl = s_tile[w][c], cb = s_cb0[w][c] + kc;
+        const uint32_t q = q0 + c;
+        const int m = T.fl_node[(size_t)tl * P + (f - s_fpre[w][c])];
+        const uint32_t pb = U.cone_box[q];
+        const int jp = m % PP, jt = (m / PP) % PT, js = m / (PP * PT);
+        const SegMid sg = segment_mid(U, U.cone_gamma[q]);
+        const double pcx = U.cx[pb], pcy = U.cy[pb], pcz = U.cz[pb];
+        double x, y, z;
+        node_position(sg, U.rad, pcx, pcy, pcz, K.ns[js], K.nt[jt], K.np[jp], x, y, z);
+        const double ux = x - pcx, uy = y - pcy, uz = z - pcz;
+        const double rp = sqrt(fma(uz, uz, fma(uy, uy, ux * ux)));
+        Loc lo;
+        const int er = locate_fast(L, L.cx[cb], L.cy[cb], L.cz[cb], x, y, z, lo);
+        if (er) {
+          raise_err(err, er);
+          continue;
+        }
+        const uint32_t cq = find_cone(L, cb, lo.gamma);
+        if (cq == kNone) {
+          raise_err(err, kErrPropCover);
+          continue;
+        }
+        double vr, vi;
+        eval_block<PS, PT, PP>(child + (size_t)cq * BL::Pst, lo.ts, lo.tt, lo.tp, vr, vi);
+        const double ratio = rp * lo.rinv;
+        double sn = 0.0, cn = 1.0;
+        if (!LAP) sincos_fast(kappa * (lo.r - rp), sn, cn);
+        const double tr = ratio * cn, ti = ratio * sn;
+        double2* acc = sv + c * P;
+        double2 v = acc[m];
+        v.x = fma(vr, tr, fma(-vi, ti, v.x));
+        v.y = fma(vr, ti, fma(vi, tr, v.y));
+        acc[m] = v;
       }
       __syncwarp();
     }
@@ -1319,13 +1596,15 @@ void build_dmma_extras(ifgf_plan* P, int d, cudaStream_t s) {
 bool launch_propagation_mma(ifgf_plan* P, int d, uint32_t qb, uint32_t qe, const double2* child,
                             double2* parent, cudaStream_t s) {
   PropTiles& T = P->tiles[d];
-  if (P->prop_kernel == IFGF_PROP_FLY || (P->prop_kernel == IFGF_PROP_ROWS && !T.enabled))
+  if (P->prop_kernel == IFGF_PROP_FLY ||
+      ((P->prop_kernel == IFGF_PROP_ROWS || P->prop_kernel == IFGF_PROP_STREAM) && !T.enabled))
     return launch_propagation_fly(P, d, qb, qe, child, parent, s);
   if (!T.enabled) return false;
   if (P->prop_kernel == IFGF_PROP_DMMA && !T.rt) build_dmma_extras(P, d, s);
   if (T.nchunks == 0 && P->prop_kernel == IFGF_PROP_DMMA) return false;
   const bool full = qb == 0 && qe == P->lv[d - 1].nc;
-  if (P->prop_kernel == IFGF_PROP_ROWS) {
+  if (P->prop_kernel == IFGF_PROP_ROWS || P->prop_kernel == IFGF_PROP_STREAM) {
+    const bool stream = P->prop_kernel == IFGF_PROP_STREAM;
     const Level& U = P->lv[d - 1];
     const Level& L = P->lv[d];
     const InterpConsts& K = P->K;
@@ -1338,20 +1617,34 @@ bool launch_propagation_mma(ifgf_plan* P, int d, uint32_t qb, uint32_t qe, const
         return v ? std::atoi(v) : 0;
       }();
       // shared memory for sv + st + task meta: ~96 KB per CTA (the rest of the SRAM is L1)
-      const int cpw_fit = (int)(96 * 1024 / IFGF_ROWS_MINB / (3 * Pn * sizeof(double2)) / NW);
+      // stream: sv + st + node records, ~150 KB per CTA
+      const int per_cone = (stream ? kStreamSmem : 3) * Pn * (int)sizeof(double2);
+      const int cpw_fit = (int)((stream ? 150 : 96) * 1024 / IFGF_ROWS_MINB / per_cone / NW);
       const int cpw = std::max(1, std::min(kRowMaxCpw, cpw_env > 0 ? cpw_env : std::max(1, cpw_fit)));
       const int cpb = NW * cpw;
       const uint32_t nq = qe - qb;
       const int groups =
           (int)std::min<size_t>(8, std::max<size_t>(1, nq / ((size_t)cpb * 148 * 4)));
       const unsigned grid = (unsigned)((nq + (size_t)cpb * groups - 1) / ((size_t)cpb * groups));
-      const size_t sm = 3 * (size_t)cpb * Pn * sizeof(double2);
+      const size_t sm = (size_t)cpb * per_cone;
       auto launch = [&](auto kern) {
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
         kern<<<grid, kRowThreads, sm, s>>>(U.dev(), L.dev(), K, tiles_dev(T), P->kappa, qb, qe,
                                           cpw, groups, child, parent, P->err);
       };
       const bool lap = P->kappa == 0.0;
+      if constexpr (StreamShape<PS, PT, PP>::ok) {
+        if (stream) {
+          if (T.row_nodes == 2)
+            lap ? launch(k_propagate_stream<PS, PT, PP, true, 2>)
+                : launch(k_propagate_stream<PS, PT, PP, false, 2>);
+          else
+            lap ? launch(k_propagate_stream<PS, PT, PP, true, 3>)
+                : launch(k_propagate_stream<PS, PT, PP, false, 3>);
+          ++P->launches;
+          return;
+        }
+      }
       if (T.row_nodes == 2)
         lap ? launch(k_propagate_rows<PS, PT, PP, true, 2>)
             : launch(k_propagate_rows<PS, PT, PP, false, 2>);
