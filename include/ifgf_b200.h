@@ -122,8 +122,20 @@ void ifgf_plan_destroy(ifgf_plan* plan);
  *                       sources staged in shared memory and split across
  *                       lanes, several targets per pass.
  *   Both agree to rounding. */
-enum { IFGF_OPT_SERIAL = 1, IFGF_OPT_PROP_KERNEL = 2, IFGF_OPT_NEAR_KERNEL = 3 };
+enum { IFGF_OPT_SERIAL = 1, IFGF_OPT_PROP_KERNEL = 2, IFGF_OPT_NEAR_KERNEL = 3,
+       IFGF_OPT_PARTITION = 4 };
 enum { IFGF_NEAR_POINT = 0, IFGF_NEAR_BOX = 1 };
+/* IFGF_OPT_PARTITION selects the rank layout of ifgf_plan_partition and
+ * ifgf_plan_exchange_set:
+ *   IFGF_PARTITION_COUNT (0, default) the reference's: finest boxes balanced
+ *                        by point count, equal-count cone intervals
+ *                        (dist.cpp:90-128);
+ *   IFGF_PARTITION_WORK  (1) the same contiguous intervals balanced by
+ *                        evaluation work (near-field pairs + interpolation
+ *                        evaluations per box; seeding or propagation + fit
+ *                        per cone) -- the paper's proposed extension
+ *                        (PAPER.md:1648-1656). */
+enum { IFGF_PARTITION_COUNT = 0, IFGF_PARTITION_WORK = 1 };
 enum {
   IFGF_PROP_NODE = 0,
   IFGF_PROP_TILES = 1,

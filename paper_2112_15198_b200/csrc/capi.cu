@@ -358,10 +358,42 @@ std::vector<T> d2h(const T* d, size_t count, cudaStream_t s) {
 }
 
 // dist.cpp:78-130 (partition), on host arrays of the level-D boxes.
+// Cut [0, n) into R contiguous intervals of about equal weight (w: per unit,
+// prefix over units); every interval gets >= min_units units when possible.
+void cut_weighted(const std::vector<double>& w, int R, size_t min_units, uint32_t* begin) {
+  const size_t n = w.size();
+  std::vector<double> pre(n + 1, 0.0);
+  for (size_t i = 0; i < n; ++i) pre[i + 1] = pre[i] + w[i];
+  begin[0] = 0;
+  size_t b = 0;
+  for (int r = 0; r < R - 1; ++r) {
+    const double target = pre[n] * (r + 1) / R;
+    const size_t rest = (size_t)(R - 1 - r) * min_units;
+    const size_t max_end = n >= rest ? n - rest : b;
+    size_t e = std::min(b + min_units, max_end);
+    // first e with pre[e] >= target, then the nearer of e-1 / e
+    while (e < max_end && pre[e] < target) ++e;
+    if (e > b + min_units && e - 1 >= b + min_units && target - pre[e - 1] < pre[e] - target) --e;
+    begin[r + 1] = (uint32_t)e;
+    b = e;
+  }
+  begin[R] = (uint32_t)n;
+}
+
+// Rank layout (dist.cpp:78-130).  IFGF_PARTITION_COUNT (the reference):
+// contiguous Morton intervals of finest-level boxes balanced by point count,
+// equal-count cone intervals per level.  IFGF_PARTITION_WORK (the paper's
+// future work): the same contiguous intervals balanced by
+// evaluation work in the SURVEY.md 8(d) flop units -- per finest box its
+// points' near-field pairs (57) and interpolation evaluations over all
+// levels (429); per cone its block's construction: level-D seeding
+// (58 per node and source) or propagation (430 per node and child) + the
+// fit (3,900).
 void partition_host(ifgf_plan* P, int R, uint32_t* box_begin, uint32_t* point_begin,
                     uint32_t* cone_begin) {
   if (R < 1) throw Error(IFGF_EINVAL, "partition: need at least one rank");
-  const Level& L = P->lv[P->depth];
+  const int D = P->depth;
+  const Level& L = P->lv[D];
   const size_t nb = L.nb;
   if ((size_t)R > nb)
     throw Error(IFGF_EINVAL,
@@ -370,39 +402,88 @@ void partition_host(ifgf_plan* P, int R, uint32_t* box_begin, uint32_t* point_be
   const auto first = d2h(L.first, nb, P->s_main);
   const auto count = d2h(L.count, nb, P->s_main);
   const size_t npts = (size_t)first[nb - 1] + count[nb - 1];
-  box_begin[0] = point_begin[0] = 0;
-  uint32_t b = 0;
-  for (int r = 0; r < R - 1; ++r) {
-    const double target = static_cast<double>(npts) * (r + 1) / R;
-    const uint32_t max_end = (uint32_t)nb - (uint32_t)(R - 1 - r);
-    uint32_t e = b + 1;
-    while (e < max_end && static_cast<double>(first[e - 1] + count[e - 1]) < target) ++e;
-    box_begin[r + 1] = e;
-    point_begin[r + 1] = first[e - 1] + count[e - 1];
-    b = e;
+  const bool work = P->partition_mode == IFGF_PARTITION_WORK;
+  if (!work) {
+    box_begin[0] = point_begin[0] = 0;
+    uint32_t b = 0;
+    for (int r = 0; r < R - 1; ++r) {
+      const double target = static_cast<double>(npts) * (r + 1) / R;
+      const uint32_t max_end = (uint32_t)nb - (uint32_t)(R - 1 - r);
+      uint32_t e = b + 1;
+      while (e < max_end && static_cast<double>(first[e - 1] + count[e - 1]) < target) ++e;
+      box_begin[r + 1] = e;
+      point_begin[r + 1] = first[e - 1] + count[e - 1];
+      b = e;
+    }
+    box_begin[R] = (uint32_t)nb;
+    point_begin[R] = (uint32_t)npts;
+  } else {
+    // per finest box: sources seen by its near field, cousins per level
+    const auto nbr = d2h(L.nbr, nb * 27, P->s_main);
+    const auto nbr_cnt = d2h(L.nbr_cnt, nb, P->s_main);
+    std::vector<double> cous(nb, 0.0);  // sum over levels of the ancestor's cousins
+    std::vector<uint32_t> anc(nb);
+    for (size_t b = 0; b < nb; ++b) anc[b] = (uint32_t)b;
+    for (int d = D; d >= 3; --d) {
+      const Level& V = P->lv[d];
+      const auto off = d2h(V.cous_off, (size_t)V.nb + 1, P->s_main);
+      for (size_t b = 0; b < nb; ++b) cous[b] += off[anc[b] + 1] - off[anc[b]];
+      if (d > 3) {
+        const auto par = d2h(V.parent, V.nb, P->s_main);
+        for (size_t b = 0; b < nb; ++b) anc[b] = par[anc[b]];
+      }
+    }
+    std::vector<double> w(nb);
+    for (size_t b = 0; b < nb; ++b) {
+      double src = 0.0;
+      for (uint32_t a = 0; a < nbr_cnt[b]; ++a) src += count[nbr[b * 27 + a]];
+      w[b] = (double)count[b] * (57.0 * (src - 1.0) + 429.0 * cous[b]);
+    }
+    cut_weighted(w, R, 1, box_begin);
+    for (int r = 0; r <= R; ++r)
+      point_begin[r] =
+          box_begin[r] == nb ? (uint32_t)npts : first[box_begin[r]];
   }
-  box_begin[R] = (uint32_t)nb;
-  point_begin[R] = (uint32_t)npts;
   if (cone_begin)
-    for (int d = 3; d <= P->depth; ++d) {
+    for (int d = 3; d <= D; ++d) {
       uint32_t* cb = cone_begin + (size_t)(d - 3) * (R + 1);
-      const size_t nc = P->lv[d].nc, base = nc / R, extra = nc % R;
-      cb[0] = 0;
-      for (int r = 0; r < R; ++r) cb[r + 1] = cb[r] + (uint32_t)(base + ((size_t)r < extra ? 1 : 0));
+      const Level& V = P->lv[d];
+      const size_t nc = V.nc;
+      if (!work) {
+        const size_t base = nc / R, extra = nc % R;
+        cb[0] = 0;
+        for (int r = 0; r < R; ++r)
+          cb[r + 1] = cb[r] + (uint32_t)(base + ((size_t)r < extra ? 1 : 0));
+        continue;
+      }
+      const auto cbox = d2h(V.cone_box, nc, P->s_main);
+      std::vector<double> w(nc);
+      const double Pn = P->K.P;
+      if (d == D) {
+        const auto cnt = d2h(V.count, V.nb, P->s_main);
+        for (size_t q = 0; q < nc; ++q) w[q] = Pn * 58.0 * cnt[cbox[q]] + 3900.0;
+      } else {
+        const auto ch = d2h(V.child_begin, (size_t)V.nb + 1, P->s_main);
+        for (size_t q = 0; q < nc; ++q)
+          w[q] = Pn * 430.0 * (ch[cbox[q] + 1] - ch[cbox[q]]) + 3900.0;
+      }
+      cut_weighted(w, R, 0, cb);
     }
 }
 
-__device__ __forceinline__ int cone_owner(uint32_t q, uint32_t nc, int R) {
-  const uint32_t base = nc / R, extra = nc % R;
-  const uint32_t cut = extra * (base + 1);
-  return q < cut ? (int)(q / (base + 1)) : (int)(extra + (q - cut) / base);
+// Owner of cone q at a level, from that level's R+1 cone boundaries.
+__device__ __forceinline__ int cone_owner(uint32_t q, const uint32_t* cb, int R) {
+  int r = 0;
+  while (r < R - 1 && q >= cb[r + 1]) ++r;
+  return r;
 }
 
 // dist.cpp:179-201: cones of level d holding (via cone_of_point) the owned
 // points as seen from their cousins; foreign ones are flagged.
 __global__ void k_need_interp(const __grid_constant__ LevelDev L, const uint32_t* __restrict__ ptbox,
                               const double* xs, const double* ys, const double* zs, uint32_t p0,
-                              uint32_t p1, int R, int rank, uint8_t* need, int* err) {
+                              uint32_t p1, const uint32_t* bounds, int R, int rank,
+                              uint8_t* need, int* err) {
   const uint32_t i = p0 + blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= p1) return;
   const uint32_t b = ptbox[i];
@@ -419,7 +500,7 @@ __global__ void k_need_interp(const __grid_constant__ LevelDev L, const uint32_t
       raise_err(err, kErrInterpCover);
       return;
     }
-    if (cone_owner(q, L.nc, R) != rank) need[q] = 1;
+    if (cone_owner(q, bounds, R) != rank) need[q] = 1;
   }
 }
 
@@ -427,7 +508,7 @@ __global__ void k_need_interp(const __grid_constant__ LevelDev L, const uint32_t
 // parent cones of level d-1.
 __global__ void k_need_prop(const __grid_constant__ LevelDev L, const __grid_constant__ LevelDev U,
                             const __grid_constant__ InterpConsts K, uint32_t q0, uint32_t q1,
-                            int R, int rank, uint8_t* need, int* err) {
+                            const uint32_t* bounds, int R, int rank, uint8_t* need, int* err) {
   const size_t t = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
   if (t >= (size_t)(q1 - q0) * K.P) return;
   const uint32_t q = q0 + (uint32_t)(t / K.P);
@@ -449,7 +530,7 @@ __global__ void k_need_prop(const __grid_constant__ LevelDev L, const __grid_con
       raise_err(err, kErrPropCover);
       return;
     }
-    if (cone_owner(cq, L.nc, R) != rank) need[cq] = 1;
+    if (cone_owner(cq, bounds, R) != rank) need[cq] = 1;
   }
 }
 
@@ -553,6 +634,10 @@ int ifgf_plan_set_option(ifgf_plan* P, int option, int value) {
       if (value < IFGF_PROP_NODE || value > IFGF_PROP_STREAM)
         throw Error(IFGF_EINVAL, "unknown propagation kernel");
       P->prop_kernel = value;
+    } else if (option == IFGF_OPT_PARTITION) {
+      if (value < IFGF_PARTITION_COUNT || value > IFGF_PARTITION_WORK)
+        throw Error(IFGF_EINVAL, "unknown partition mode");
+      P->partition_mode = value;
     } else if (option == IFGF_OPT_NEAR_KERNEL) {
       if (value < IFGF_NEAR_POINT || value > IFGF_NEAR_BOX)
         throw Error(IFGF_EINVAL, "unknown near-field kernel");
@@ -879,18 +964,22 @@ int ifgf_plan_exchange_set(ifgf_plan* P, int R, int rank, int d, int kind, uint3
     const Level& L = P->lv[d];
     uint8_t* need = P->alloc<uint8_t>(L.nc + 1);
     IFGF_CUDA(cudaMemsetAsync(need, 0, L.nc + 1, P->s_main));
+    // this level's cone boundaries on the device (ownership test)
+    uint32_t* d_cb = P->alloc<uint32_t>(R + 1);
+    IFGF_CUDA(cudaMemcpyAsync(d_cb, cb.data() + (size_t)(d - 3) * (R + 1), (R + 1) * 4,
+                              cudaMemcpyHostToDevice, P->s_main));
     if (kind == 0) {
       const uint32_t p0 = pb[rank], p1 = pb[rank + 1];
       if (p1 > p0)
         k_need_interp<<<(p1 - p0 + 127) / 128, 128, 0, P->s_main>>>(
-            L.dev(), L.ptbox, P->xs, P->ys, P->zs, p0, p1, R, rank, need, P->err);
+            L.dev(), L.ptbox, P->xs, P->ys, P->zs, p0, p1, d_cb, R, rank, need, P->err);
     } else {
       const uint32_t* own = cb.data() + (size_t)(d - 4) * (R + 1);
       const uint32_t q0 = own[rank], q1 = own[rank + 1];
       const size_t work = (size_t)(q1 - q0) * P->K.P;
       if (work)
         k_need_prop<<<(unsigned)((work + 127) / 128), 128, 0, P->s_main>>>(
-            L.dev(), P->lv[d - 1].dev(), P->K, q0, q1, R, rank, need, P->err);
+            L.dev(), P->lv[d - 1].dev(), P->K, q0, q1, d_cb, R, rank, need, P->err);
     }
     IFGF_CUDA(cudaGetLastError());
     check_device_error(P);

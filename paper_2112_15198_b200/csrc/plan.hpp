@@ -181,6 +181,7 @@ struct ifgf_plan {
   bool serial = false;  // IFGF_OPT_SERIAL
   int prop_kernel = IFGF_PROP_ROWS;  // IFGF_OPT_PROP_KERNEL
   int near_kernel = IFGF_NEAR_BOX;   // IFGF_OPT_NEAR_KERNEL
+  int partition_mode = IFGF_PARTITION_COUNT;  // IFGF_OPT_PARTITION
   size_t setup_launches = 0;
 
   template <class T>

@@ -236,7 +236,7 @@ class DistributedPlan:
     exchange sets and learns its send sets with one all-to-all per level and
     kind (build_exchange_plan_rank)."""
 
-    def __init__(self, x1, x2, x3, cfg, params=None, group=None):
+    def __init__(self, x1, x2, x3, cfg, params=None, group=None, partition: int = 0):
         import torch
         import torch.distributed as dist
 
@@ -250,6 +250,7 @@ class DistributedPlan:
         p = params or EngineParams()
         p.device = torch.cuda.current_device()
         self.plan = Plan(x1, x2, x3, cfg, p)
+        self.plan.set_partition(partition)
         self.layout = rank_layout(self.plan, self.world)
         self.ex = build_exchange_plan_rank(
             self.layout, self.plan.depth, self.rank,
@@ -286,15 +287,20 @@ class DistributedPlan:
         self.plan.close()
 
 
-def simulate(plans, a_re, a_im):
+def simulate(plans, a_re, a_im, partition: int = 0, rank_seconds=None):
     """R ranks in one process (one plan each, all on the same GPU), blocks
     moved plan to plan through pack/unpack -- the reference's in-process rank
     simulation (dist.cpp) on real kernels.  Ranks advance phase by phase, so
     no kernel ever waits on another rank's kernel.  Returns the full result
-    in the caller's order and the number of blocks moved."""
+    in the caller's order and the number of blocks moved.  `partition`:
+    Plan.PARTITION_COUNT (the reference's layout) or Plan.PARTITION_WORK.
+    `rank_seconds` (a list): filled with each rank's compute time (its passes,
+    synchronised one by one -- exchanges excluded), the load-balance measure."""
     import torch
 
     R = len(plans)
+    for p in plans:
+        p.set_partition(partition)
     layout = rank_layout(plans[0], R)
     ex = build_exchange_plan(layout, plans[0].depth,
                              lambda r, d, kind: plans[0].exchange_set(R, r, d, kind))
@@ -320,24 +326,38 @@ def simulate(plans, a_re, a_im):
                 torch.cuda.synchronize()
                 moved[0] += len(a)
 
+    secs = [0.0] * R
+
+    def run(r, fn, *args):
+        if rank_seconds is None:
+            return fn(*args)
+        import time
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        fn(*args)
+        torch.cuda.synchronize()
+        secs[r] += time.perf_counter() - t0
+
     D = plans[0].depth
     for r in range(R):
         pb, pe = layout.points(r)
         plans[r].set_density(a_re, a_im)
         plans[r].zero_result()
-        plans[r].singular_pass(pb, pe)
-        plans[r].level_d_pass(*layout.cones(D, r))
+        run(r, plans[r].singular_pass, pb, pe)
+        run(r, plans[r].level_d_pass, *layout.cones(D, r))
     if D > 3:
         exchange_all(D, PROP)
     for d in range(D, 2, -1):
         exchange_all(d, INTERP)
         if d > 3:
             for r in range(R):
-                plans[r].propagation_pass(d, *layout.cones(d - 1, r))
+                run(r, plans[r].propagation_pass, d, *layout.cones(d - 1, r))
             if d > 4:
                 exchange_all(d - 1, PROP)
         for r in range(R):
-            plans[r].interpolation_pass(d, *layout.points(r))
+            run(r, plans[r].interpolation_pass, d, *layout.points(r))
+    if rank_seconds is not None:
+        rank_seconds[:] = secs
     n = plans[0].n
     s_re, s_im = np.zeros(n), np.zeros(n)
     for r in range(R):

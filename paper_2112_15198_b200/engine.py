@@ -292,8 +292,9 @@ class Plan:
 
     def set_option(self, option: int, value: int):
         """IFGF_OPT_* (include/ifgf_b200.h): 1 serial streams, 2 propagation
-        kernel (PROP_NODE, PROP_TILES, PROP_DMMA, PROP_ROWS default, PROP_FLY),
-        3 near-field kernel (NEAR_POINT, NEAR_BOX default)."""
+        kernel (PROP_NODE, PROP_TILES, PROP_DMMA, PROP_ROWS default, PROP_FLY,
+        PROP_STREAM), 3 near-field kernel (NEAR_POINT, NEAR_BOX default),
+        4 rank layout (PARTITION_COUNT default, PARTITION_WORK)."""
         check(lib.ifgf_plan_set_option(self._h, option, value))
 
     def set_prop_kernel(self, kind: int):
@@ -301,6 +302,14 @@ class Plan:
 
     def set_near_kernel(self, kind: int):
         self.set_option(3, kind)
+
+    PARTITION_COUNT, PARTITION_WORK = 0, 1
+
+    def set_partition(self, mode: int):
+        """Rank layout of partition()/exchange_set(): PARTITION_COUNT (the
+        reference's, dist.cpp:90-128) or PARTITION_WORK (balanced by
+        evaluation work)."""
+        self.set_option(4, mode)
 
     def _info(self) -> _lib.CPlanInfo:
         info = _lib.CPlanInfo()

@@ -51,7 +51,35 @@ def test_simulated_ranks_bitwise_equal_single_gpu(gpu, case, R):
         assert moved == 0
 
 
-def _dplan_worker(rank, world, port, args, out):
+@pytest.mark.parametrize("R", [2, 4, 8])
+def test_work_partition_layout_and_bitwise(gpu, R):
+    """IFGF_PARTITION_WORK (contiguous intervals balanced by evaluation work,
+    the paper's proposed extension) on a non-uniform spheroid: a valid layout
+    (monotone, covering, whole boxes, point cuts on box boundaries) that
+    differs from the reference's count-balanced one, and the distributed
+    result is still bitwise the single-GPU apply."""
+    from paper_2112_15198_b200.dist import simulate
+    pc = gpu.generate(40000, 1, 0.25, 0, 43)  # oblate spheroid (1,1,0.25)
+    cfg = gpu.KernelConfig(gpu.KernelKind.Helmholtz, 2 * math.pi * 6.0)
+    single = gpu.Plan.from_cloud(pc, cfg)
+    s_re, s_im, _ = single.apply(pc.a_re, pc.a_im)
+    bb0, pb0, cb0 = single.partition(R)
+    single.set_partition(gpu.Plan.PARTITION_WORK)
+    bb, pb, cb = single.partition(R)
+    info = single.info
+    assert bb[0] == 0 and bb[-1] == info.boxes[single.depth] and np.all(np.diff(bb) >= 1)
+    assert pb[0] == 0 and pb[-1] == len(pc.x1) and np.all(np.diff(pb.astype(np.int64)) > 0)
+    for d in range(3, single.depth + 1):
+        row = cb[d - 3]
+        assert row[0] == 0 and row[-1] == info.cones[d] and np.all(np.diff(row.astype(np.int64)) >= 0)
+    assert not (np.array_equal(bb, bb0) and np.array_equal(cb, cb0))
+    plans = [gpu.Plan.from_cloud(pc, cfg) for _ in range(R)]
+    i_re, i_im, moved, ex = simulate(plans, pc.a_re, pc.a_im, partition=gpu.Plan.PARTITION_WORK)
+    assert np.array_equal(i_re, s_re) and np.array_equal(i_im, s_im)
+    assert moved == ex.volume_blocks()
+
+
+def _dplan_worker(rank, world, port, args, out, partition=0):
     import os
 
     import torch
@@ -66,7 +94,7 @@ def _dplan_worker(rank, world, port, args, out):
     n, shape, c, dens, seed, kappa = args
     pc = ifgf.generate(n, shape, c, dens, seed)
     cfg = ifgf.KernelConfig(ifgf.KernelKind.Helmholtz, kappa)
-    dp = DistributedPlan(pc.x1, pc.x2, pc.x3, cfg)
+    dp = DistributedPlan(pc.x1, pc.x2, pc.x3, cfg, partition=partition)
     i_re, i_im = dp.apply(pc.a_re, pc.a_im)
     vol = dp.ex.volume_blocks()
     dp.close()
@@ -74,7 +102,8 @@ def _dplan_worker(rank, world, port, args, out):
     dist.destroy_process_group()
 
 
-def test_distributed_plan_two_ranks_one_gpu(gpu):
+@pytest.mark.parametrize("partition", [0, 1])
+def test_distributed_plan_two_ranks_one_gpu(gpu, partition):
     """The whole DistributedPlan path (rank layout, per-rank exchange sets and
     the all-to-all that pairs them, per-level block exchange, result gather)
     on real kernels: two processes share the GPU, blocks travel through gloo
@@ -96,7 +125,8 @@ def test_distributed_plan_two_ranks_one_gpu(gpu):
     s.close()
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
-    ps = [ctx.Process(target=_dplan_worker, args=(r, 2, port, args, q)) for r in range(2)]
+    ps = [ctx.Process(target=_dplan_worker, args=(r, 2, port, args, q, partition))
+          for r in range(2)]
     for p in ps:
         p.start()
     res = [q.get(timeout=300) for _ in ps]
