@@ -126,3 +126,26 @@ def test_argument_errors_mirror_reference(ifgf):
     bad = ifgf.EngineParams(orders=ifgf.InterpOrders(13, 5, 5))
     with pytest.raises(ifgf.InvalidArgument):  # engine.cpp:76-77 unsupported orders
         ifgf.Plan.from_cloud(pc, cfg, bad)
+
+
+def test_reference_acceptance_runner_binds_the_gpu_library(ifgf):
+    """oracle/_ref/ifgf_acceptance_b200 is the reference's acceptance.cpp
+    linked through integration/ref_apply_b200.cpp: its ifgf::apply must be
+    the shim's (calls into libifgf_b200.so), and without a device that call
+    fails loudly with the library's message instead of running the
+    reference's CPU engine."""
+    import subprocess
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    exe = os.path.join(root, "oracle", "_ref", "ifgf_acceptance_b200")
+    if not os.path.exists(exe):
+        pytest.skip("acceptance runner not built (needs /root/reference)")
+    libs = subprocess.run(["ldd", exe], capture_output=True, text=True).stdout
+    assert "libifgf_b200.so" in libs
+    syms = subprocess.run(["nm", exe], capture_output=True, text=True).stdout
+    apply_sym = "_ZN4ifgf5applyERNS_10PointCloudERKNS_12KernelConfigERKNS_12EngineParamsE"
+    kinds = {ln.split()[-2] for ln in syms.splitlines() if ln.endswith(" " + apply_sym)}
+    assert kinds == {"T"}, kinds  # one strong definition: the shim
+    if ifgf.device_ok():
+        pytest.skip("a device is visible (tests/test_gpu_acceptance.py runs it)")
+    p = subprocess.run([exe, "1"], capture_output=True, text=True, timeout=120)
+    assert p.returncode != 0 and "libifgf_b200 has no CPU path" in p.stderr, p.stderr[-500:]
