@@ -242,6 +242,16 @@ int ifgf_measure_fp64_peak(int device, double* tflops, double* ms);
 int ifgf_generate(size_t n, int shape, double c, int dens, uint64_t seed, double* x1,
                   double* x2, double* x3, double* a_re, double* a_im);
 
+/* generate_surface (geometry.cpp:57-93, geometry.hpp): 6 n_per_dim^2 points on
+ * the cube-face surface of radius a; shape 0 sphere, 1 oblate (z x 0.1),
+ * 2 prolate (z x 10) (Shape, geometry.hpp); densities U[0,1) from
+ * mt19937_64(seed).  Arrays hold 6 n_per_dim^2 entries. */
+int ifgf_generate_surface(int shape, double a, int n_per_dim, uint64_t seed, double* x1,
+                          double* x2, double* x3, double* a_re, double* a_im);
+/* bench::checksum_hex (bench.cpp:26-41): FNV-1a 64 of re then im, 16 hex
+ * digits + NUL into out[17]. */
+void ifgf_checksum_hex(const double* re, const double* im, size_t n, char* out);
+
 #ifdef __cplusplus
 }
 #endif

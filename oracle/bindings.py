@@ -352,6 +352,7 @@ class RefOracle(_Checker):
     kind = "reference"
 
     def __init__(self, path=REF_SO, simd="avx2"):
+        self.path = path
         if not os.path.exists(path):
             raise FileNotFoundError(f"{path} missing: run `make -C oracle ref`")
         os.environ.setdefault("IFGF_SIMD", simd)
@@ -366,6 +367,10 @@ class RefOracle(_Checker):
         L.ref_run_distributed.argtypes = [C.c_size_t] + [_dp] * 5 + [
             C.c_int, C.c_double, C.c_void_p, C.c_double, C.c_int, _dp, _dp, _u64p,
             C.POINTER(C.c_int)]
+        L.ref_generate_surface.argtypes = [C.c_int, C.c_double, C.c_int, C.c_uint64] + [_dp] * 5
+        L.ref_checksum_hex.argtypes = [_dp, _dp, C.c_size_t, C.c_char_p]
+        L.ref_checksum_hex.restype = None
+        L.ref_write_points_binary.argtypes = [C.c_char_p, C.c_size_t] + [_dp] * 5
         L.ref_direct_eval.argtypes = [C.c_size_t] + [_dp] * 5 + [C.c_int, C.c_double, C.c_int,
                                                                   _dp, _dp]
         L.ref_sample_indices.argtypes = [C.c_size_t, C.c_size_t, C.c_uint64, _u32p]
@@ -430,6 +435,37 @@ class RefOracle(_Checker):
         out = np.zeros(m, np.uint32)
         self._check(self.lib.ref_sample_indices(n, m, seed, out))
         return out
+
+    # harness: geometry.cpp:57-93, 147-226; bench.cpp:26-41
+    def generate_surface(self, shape, a, npd, seed):
+        m = 6 * npd * npd
+        arrs = [np.zeros(m) for _ in range(5)]
+        self._check(self.lib.ref_generate_surface(shape, C.c_double(a), npd, C.c_uint64(seed),
+                                                  *arrs))
+        return arrs
+
+    def checksum_hex(self, re, im):
+        out = C.create_string_buffer(17)
+        self.lib.ref_checksum_hex(_c(re), _c(im), C.c_size_t(len(re)), out)
+        return out.value.decode()
+
+    def write_points_binary(self, path, x1, x2, x3, ar, ai):
+        self._check(self.lib.ref_write_points_binary(str(path).encode(), C.c_size_t(len(x1)),
+                                                     _c(x1), _c(x2), _c(x3), _c(ar), _c(ai)))
+
+    def read_points(self, path):
+        """The reference's read_points, run out of process (oracle/_ref/
+        ref_read_points): its iostream CSV parsing crashes inside this
+        process.  Returns the five arrays, or raises RuntimeError(what)."""
+        import subprocess
+        exe = os.path.join(os.path.dirname(self.path), "ref_read_points")
+        out = subprocess.run([exe, str(path)], capture_output=True, text=True).stdout
+        if out.startswith("error: "):
+            raise RuntimeError(out[7:].strip())
+        lines = out.splitlines()
+        n = int(lines[0])
+        a = np.array([[float(v) for v in ln.split()] for ln in lines[1:1 + n]]).reshape(n, 5)
+        return [a[:, k].copy() for k in range(5)]
 
     def error_at_indices(self, x1, x2, x3, ar, ai, ir, ii, kind, k, idx, threads=0):
         e = C.c_double()

@@ -9,6 +9,7 @@
 //   apply / direct_eval / sample_indices / error_at_indices  (engine.hpp:112-128)
 //   Problem::build and the four passes                        (engine.hpp:46-110)
 //   dist::partition / dist::run_distributed                   (dist.hpp:23, 90)
+//   generate_surface, the point-file formats, checksum_hex    (geometry.hpp, bench.hpp)
 // and maps the reference's exception classes onto the return codes of
 // include/ifgf_b200.h (0 ok, 1 invalid_argument, 2 domain_error,
 // 3 logic_error, 4 runtime_error).
@@ -21,8 +22,10 @@
 #include <string>
 #include <vector>
 
+#include "ifgf/bench.hpp"
 #include "ifgf/dist.hpp"
 #include "ifgf/engine.hpp"
+#include "ifgf/geometry.hpp"
 #include "ifgf/simd_kernels.hpp"
 
 using namespace ifgf;
@@ -351,6 +354,39 @@ int ref_problem_partition(void* h, int n_ranks, std::uint32_t* box_begin,
     for (std::size_t l = 0; l < L.cone_begin.size(); ++l)
       std::memcpy(cone_begin + l * (n_ranks + 1), L.cone_begin[l].data(),
                   (n_ranks + 1) * sizeof(std::uint32_t));
+  });
+}
+
+// harness (geometry.cpp:57-93, 147-226; bench.cpp:26-41)
+int ref_generate_surface(int shape, double a, int npd, std::uint64_t seed, double* x1, double* x2,
+                         double* x3, double* a_re, double* a_im) {
+  return guarded([&] {
+    const PointCloud pc = generate_surface(static_cast<Shape>(shape), a, npd, seed);
+    std::memcpy(x1, pc.x1.data(), pc.size() * 8);
+    std::memcpy(x2, pc.x2.data(), pc.size() * 8);
+    std::memcpy(x3, pc.x3.data(), pc.size() * 8);
+    std::memcpy(a_re, pc.a_re.data(), pc.size() * 8);
+    std::memcpy(a_im, pc.a_im.data(), pc.size() * 8);
+  });
+}
+
+void ref_checksum_hex(const double* re, const double* im, std::size_t n, char* out) {
+  const std::string h = bench::checksum_hex(std::vector<double>(re, re + n),
+                                            std::vector<double>(im, im + n));
+  std::memcpy(out, h.c_str(), 17);
+}
+
+int ref_write_points_binary(const char* path, std::size_t n, const double* x1, const double* x2,
+                            const double* x3, const double* a_re, const double* a_im) {
+  return guarded([&] {
+    PointCloud pc;
+    pc.resize(n);
+    std::memcpy(pc.x1.data(), x1, n * 8);
+    std::memcpy(pc.x2.data(), x2, n * 8);
+    std::memcpy(pc.x3.data(), x3, n * 8);
+    std::memcpy(pc.a_re.data(), a_re, n * 8);
+    std::memcpy(pc.a_im.data(), a_im, n * 8);
+    write_points_binary(path, pc);
   });
 }
 

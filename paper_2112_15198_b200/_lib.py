@@ -96,6 +96,9 @@ SIGNATURES = {
                                          C.POINTER(C.c_double)]),
     "ifgf_generate": (C.c_int, [_sz, C.c_int, C.c_double, C.c_int, C.c_uint64, _vp, _vp, _vp,
                                 _vp, _vp]),
+    "ifgf_generate_surface": (C.c_int, [C.c_int, C.c_double, C.c_int, C.c_uint64, _vp, _vp,
+                                        _vp, _vp, _vp]),
+    "ifgf_checksum_hex": (None, [_vp, _vp, _sz, C.c_char_p]),
 }
 
 

@@ -82,3 +82,60 @@ extern "C" int ifgf_generate(size_t n, int shape, double c, int dens, uint64_t s
   }
   return IFGF_OK;
 }
+
+// generate_surface (geometry.cpp:57-93): the reference's cube-face surfaces,
+// n_per_dim^2 cell centres per face projected to the radius-a sphere, z scaled
+// by the shape (axis_scale, geometry.cpp:40-47); densities U[0,1) re then im
+// per point from mt19937_64(seed) (geometry.cpp:87-91).  Same operation order
+// as the reference (no contraction: this file is compiled without -ffp-contract).
+extern "C" int ifgf_generate_surface(int shape, double a, int n_per_dim, uint64_t seed,
+                                     double* x1, double* x2, double* x3, double* a_re,
+                                     double* a_im) {
+  if (!(a > 0.0) || n_per_dim < 2 || shape < 0 || shape > 2) return IFGF_EINVAL;
+  const int n = n_per_dim;
+  const double zs = shape == 0 ? 1.0 : (shape == 1 ? 0.1 : 10.0);
+  size_t m = 0;
+  for (int face = 0; face < 6; ++face) {
+    const int axis = face / 2;
+    const double sign = (face % 2 == 0) ? 1.0 : -1.0;
+    for (int i = 0; i < n; ++i) {
+      const double u = -1.0 + (2.0 * i + 1.0) / n;
+      for (int j = 0; j < n; ++j) {
+        const double v = -1.0 + (2.0 * j + 1.0) / n;
+        double p[3];
+        p[axis] = sign;
+        p[(axis + 1) % 3] = u;
+        p[(axis + 2) % 3] = v;
+        const double inv = 1.0 / std::sqrt(p[0] * p[0] + p[1] * p[1] + p[2] * p[2]);
+        x1[m] = a * p[0] * inv;
+        x2[m] = a * p[1] * inv;
+        x3[m] = zs * a * p[2] * inv;
+        ++m;
+      }
+    }
+  }
+  std::mt19937_64 g(seed);
+  for (size_t i = 0; i < m; ++i) {
+    a_re[i] = static_cast<double>(g() >> 11) * 0x1.0p-53;
+    a_im[i] = static_cast<double>(g() >> 11) * 0x1.0p-53;
+  }
+  return IFGF_OK;
+}
+
+// bench::checksum_hex (bench.cpp:26-41): 64-bit FNV-1a over the bytes of re
+// then im; out receives 16 hex digits and a NUL.
+extern "C" void ifgf_checksum_hex(const double* re, const double* im, size_t n, char* out) {
+  uint64_t h = 1469598103934665603ull;
+  const auto mix = [&h](const double* v, size_t count) {
+    const auto* p = reinterpret_cast<const unsigned char*>(v);
+    for (size_t i = 0; i < count * sizeof(double); ++i) {
+      h ^= p[i];
+      h *= 1099511628211ull;
+    }
+  };
+  mix(re, n);
+  mix(im, n);
+  static const char* hex = "0123456789abcdef";
+  for (int i = 0; i < 16; ++i) out[i] = hex[(h >> (60 - 4 * i)) & 15u];
+  out[16] = '\0';
+}

@@ -54,6 +54,10 @@ constexpr int kRowThreads = IFGF_ROWS_THREADS;
 #ifndef IFGF_ROWS_PF
 #define IFGF_ROWS_PF 1
 #endif
+// L1 prefetch of the round's blocks and row data after phase A
+#ifndef IFGF_ROWS_PFA
+#define IFGF_ROWS_PFA 1
+#endif
 constexpr int kRowMaxCpw = 16;  // parent cones per warp
 
 struct TilesDev {
@@ -826,6 +830,21 @@ __global__ void __launch_bounds__(kRowThreads, IFGF_ROWS_MINB)
           const uint2 rw = T.rw[(size_t)tl * P + loc];
           mt = make_uint2(find_cone(L, s_cb0[w][c] + kc, rw.x),
                           ((uint32_t)c << 24) | (rw.y & 0xff0000u) | loc);
+#if IFGF_ROWS_PFA
+          // the whole round's data into L1 before phase B: each child-cone
+          // group's block once (its first row), each 16-row run of row data
+          if ((rw.y >> 24) & 1u && mt.x != kNone) {
+            const char* pf = (const char*)(child + (size_t)mt.x * BL::Pst);
+#pragma unroll
+            for (int l = 0; l < (BL::Pst * 16 + 127) / 128; ++l)
+              asm volatile("prefetch.global.L1 [%0];" ::"l"(pf + 128 * l));
+          }
+          if ((loc & 15u) == 0) {
+            const char* rd = (const char*)(T.rdat + row_field(tl, P, 5 * R, (int)loc, 0));
+#pragma unroll
+            for (int f = 0; f < 5 * R; ++f) asm volatile("prefetch.global.L1 [%0];" ::"l"(rd + 256 * f));
+          }
+#endif
         } else {
           mt = make_uint2(kFlagTask, ((uint32_t)c << 24) | (loc - s_nrow[w][c]));
         }
