@@ -113,6 +113,11 @@ void ifgf_plan_destroy(ifgf_plan* plan);
  *                       of rows sharing the child cone stream past; orders
  *                       whose planes do not fit in registers run ROWS,
  *                       levels without the precomputed geometry run FLY.
+ *   IFGF_PROP_PIPE  (6) warp-specialised: a producer warp TMA-stages each
+ *                       unit's tile rows and child blocks in a ring of
+ *                       shared-memory stages, consumer warps evaluate from
+ *                       shared memory only; levels without the
+ *                       precomputed geometry run FLY.
  *   Where the precomputed geometry is not built (too few parent cones per
  *   gamma, P > 255) TILES and DMMA run IFGF_PROP_NODE.
  *   All agree to rounding; DESIGN.md records their measured times.
@@ -142,7 +147,8 @@ enum {
   IFGF_PROP_DMMA = 2,
   IFGF_PROP_ROWS = 3,
   IFGF_PROP_FLY = 4,
-  IFGF_PROP_STREAM = 5
+  IFGF_PROP_STREAM = 5,
+  IFGF_PROP_PIPE = 6
 };
 int ifgf_plan_set_option(ifgf_plan* plan, int option, int value);
 

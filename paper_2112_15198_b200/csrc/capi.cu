@@ -631,7 +631,7 @@ int ifgf_plan_set_option(ifgf_plan* P, int option, int value) {
     if (option == IFGF_OPT_SERIAL) {
       P->serial = value != 0;
     } else if (option == IFGF_OPT_PROP_KERNEL) {
-      if (value < IFGF_PROP_NODE || value > IFGF_PROP_STREAM)
+      if (value < IFGF_PROP_NODE || value > IFGF_PROP_PIPE)
         throw Error(IFGF_EINVAL, "unknown propagation kernel");
       P->prop_kernel = value;
     } else if (option == IFGF_OPT_PARTITION) {

@@ -945,6 +945,489 @@ __global__ void __launch_bounds__(kRowThreads, IFGF_ROWS_MINB)
   }
 }
 
+// K3 pipelined (IFGF_PROP_PIPE): warp-specialised CTA, one per SM.  Work
+// unit = <= kPpCh consecutive parent cones of one parent box (same
+// children); a stage = (unit, child), held in a ring of kPpStages
+// shared-memory buffers.
+//   producer warp: per stage, TMA bulk copies (cp.async.bulk + mbarrier
+//     transaction counts) of everything the stage reads that does not
+//     depend on the child blocks: each cone's tile rows (first 32-row chunk
+//     of local coordinates and transfer factors, the row list, the node map,
+//     row and flagged counts) and the child box's cone bitmap.  It never
+//     waits on what it copies, so it runs stages ahead.
+//   consumer warps, software-pipelined one stage apart:
+//     A(i+1): the rows' child cones from the staged bitmap, one shared slot
+//       per distinct cone (atomicCAS table), TMA copies of those blocks;
+//     B(i):   every row evaluated from shared memory only (eval_block_multi
+//       over LDS; ~47 of 64 DFMA/clk/SM measured for 3-node rows), the
+//       contributions added to the unit's node values, then the stage is
+//       released; after a unit's last child its cones are fitted.
+// The block copies of stage i+1 thus land while stage i is evaluated.  Named
+// barriers order the consumer phases; every node gets one contribution per
+// child, in child order: the sums of k_propagate_rows, bitwise.  Rows past
+// the first 32 of a tile, cones beyond the slot capacity and bitmaps wider
+// than kPpBitWords fall back to global memory; flagged nodes take the exact
+// per-box path.
+#ifndef IFGF_PP_CONSUMERS
+#define IFGF_PP_CONSUMERS 8
+#endif
+#ifndef IFGF_PP_STAGES
+#define IFGF_PP_STAGES 3
+#endif
+constexpr int kPpConsumers = IFGF_PP_CONSUMERS;
+constexpr int kPpThreads = (kPpConsumers + 1) * 32;
+constexpr int kPpStages = IFGF_PP_STAGES;
+#ifndef IFGF_PP_CH
+#define IFGF_PP_CH 8
+#endif
+constexpr int kPpCh = IFGF_PP_CH;  // parent cones per unit (<= 8: unit records)
+static_assert(kPpCh <= 8, "unit records hold 8 cones");
+constexpr int kPpBitWords = 72;   // staged bitmap words per child box
+constexpr int kPpTab = 2048;      // child cones covered by the slot table
+constexpr uint32_t kPpEmpty = 0xffffffffu, kPpPending = 0xfffffffeu;
+constexpr uint32_t kPpGlobal = 0xffu;
+
+__device__ __forceinline__ void pp_mbar_init(uint64_t* m, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"((uint32_t)__cvta_generic_to_shared(m)),
+               "r"(count));
+}
+__device__ __forceinline__ void pp_arrive(uint64_t* m) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"((uint32_t)__cvta_generic_to_shared(m))
+               : "memory");
+}
+__device__ __forceinline__ void pp_wait(uint64_t* m, uint32_t parity) {
+  const uint32_t a = (uint32_t)__cvta_generic_to_shared(m);
+  asm volatile(
+      "{\n .reg .pred p;\n"
+      "PPW: mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      " @!p bra PPW;\n}" ::"r"(a),
+      "r"(parity)
+      : "memory");
+}
+// expected bytes are added before each copy is issued, so the transaction
+// count never goes negative; the phase completes at the producer's final
+// arrive once every copy has landed
+__device__ __forceinline__ void pp_bulk(void* dst, const void* src, uint32_t bytes, uint64_t* m) {
+  asm volatile("mbarrier.expect_tx.relaxed.cta.shared::cta.b64 [%0], %1;" ::"r"(
+                   (uint32_t)__cvta_generic_to_shared(m)),
+               "r"(bytes)
+               : "memory");
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          (uint32_t)__cvta_generic_to_shared(dst)),
+      "l"(src), "r"(bytes), "r"((uint32_t)__cvta_generic_to_shared(m))
+      : "memory");
+}
+__device__ __forceinline__ void pp_consumer_sync() {
+  asm volatile("bar.sync 1, %0;" ::"n"(kPpConsumers * 32) : "memory");
+}
+
+// Units of <= ch consecutive cones of one parent box, the box's cones split
+// evenly: unit_start[u] .. unit_start[u + 1].
+__global__ void k_pp_units_count(const __grid_constant__ LevelDev U, uint32_t ch, uint32_t* cnt) {
+  const uint32_t b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b > U.nb) return;
+  cnt[b] = b == U.nb ? 0u : (U.box_cone[b + 1] - U.box_cone[b] + ch - 1) / ch;
+}
+__global__ void k_pp_units_fill(const __grid_constant__ LevelDev U, uint32_t ch, const uint32_t* off,
+                                uint32_t* ustart, uint32_t* nunits) {
+  const uint32_t b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= U.nb) {
+    if (b == U.nb) {
+      ustart[off[b]] = U.nc;
+      *nunits = off[b];
+    }
+    return;
+  }
+  const uint32_t q0 = U.box_cone[b], n = U.box_cone[b + 1] - q0;
+  const uint32_t parts = (n + ch - 1) / ch;
+  for (uint32_t j = 0; j < parts; ++j)
+    ustart[off[b] + j] = q0 + (uint32_t)(((uint64_t)j * n) / parts);
+}
+
+// Per-unit record for the producer (32 words, one coalesced load per unit):
+// [0] q0, [1] ncon, [2] first child, [3] children, [4] child octants (3 bits
+// each), [5 .. 5+nch] the children's first cone ordinals (box_cone), [14 ..
+// 14+ncon) the cones' gamma indices.
+constexpr int kPpRec = 32;
+__global__ void k_pp_units_info(const __grid_constant__ LevelDev U, const __grid_constant__ LevelDev L,
+                                const uint32_t* __restrict__ gidx, const uint32_t* __restrict__ ustart,
+                                const uint32_t* __restrict__ nunits, uint32_t* rec) {
+  const uint32_t u = blockIdx.x * blockDim.x + threadIdx.x;
+  if (u >= *nunits) return;
+  uint32_t* o = rec + (size_t)u * kPpRec;
+  const uint32_t q0 = ustart[u], ncon = ustart[u + 1] - q0;
+  const uint32_t pb = U.cone_box[q0];
+  const uint32_t cb0 = U.child_begin[pb], nch = U.child_begin[pb + 1] - cb0;
+  uint32_t octs = 0;
+  for (uint32_t k = 0; k < nch; ++k) octs |= (uint32_t)(L.code[cb0 + k] & 7) << (3 * k);
+  o[0] = q0;
+  o[1] = ncon;
+  o[2] = cb0;
+  o[3] = nch;
+  o[4] = octs;
+  for (uint32_t k = 0; k <= nch; ++k) o[5 + k] = L.box_cone[cb0 + k];
+  for (uint32_t c = 0; c < ncon; ++c) o[14 + c] = gidx[q0 + c];
+}
+
+template <int PS, int PT, int PP, int R>
+struct PipeShape {
+  static constexpr int P = PS * PT * PP;
+  static constexpr int Pst = BlockLayout<PS, PT, PP>::Pst;
+  static constexpr int NF = 5 * R;              // row fields
+  static constexpr int RowBytes = NF * 32 * 8;  // one 32-row chunk
+  static constexpr int RwBytes = 32 * 8 + 16;   // 32 row entries + alignment slack
+  static constexpr int NodeBytes = 32 * 4 + 16;
+  static constexpr int CntBytes = 32;           // rw_cnt and fl_cnt words, 16 B each
+  static constexpr int BitBytes = kPpBitWords * 8 + 16, RankBytes = kPpBitWords * 4 + 16;
+  static constexpr int NB = P <= 80 ? 16 : 4;   // block slots per stage
+  static constexpr int MaxTask = kPpCh * P;
+  static constexpr int off_row = 0;
+  static constexpr int off_rw = off_row + kPpCh * RowBytes;
+  static constexpr int off_node = off_rw + kPpCh * RwBytes;
+  static constexpr int off_cnt = off_node + kPpCh * NodeBytes;
+  static constexpr int off_bits = off_cnt + kPpCh * CntBytes;
+  static constexpr int off_rank = off_bits + BitBytes;
+  static constexpr int off_blk = (off_rank + RankBytes + 15) / 16 * 16;
+  static constexpr int off_task = off_blk + NB * Pst * 16;
+  static constexpr int off_cq = off_task + MaxTask * 4;
+  static constexpr int stage_bytes = ((off_cq + MaxTask * 4) + 127) / 128 * 128;
+  static constexpr size_t smem = (size_t)kPpStages * stage_bytes  // stages
+                                 + (size_t)kPpCh * P * 16          // sv
+                                 + (size_t)kPpConsumers * P * 16   // fit scratch
+                                 + (size_t)kPpTab * 4;             // slot table
+};
+
+struct PipeHdr {
+  uint32_t q0, ncon, cb, cbase, ncb, last, nwd, sbm;
+  uint64_t w0;
+  uint32_t tile[kPpCh], rwoff[kPpCh], nodeoff[kPpCh], rcoff[kPpCh], fcoff[kPpCh];
+  uint32_t bitoff, rankoff;
+  // consumers
+  uint32_t pre[kPpCh + 1], fpre[kPpCh + 1], nslot;
+};
+
+// 16-byte-aligned window [lo, lo + size) covering [p, p + bytes)
+__device__ __forceinline__ const void* pp_window(const void* p, uint32_t bytes, uint32_t& off,
+                                                 uint32_t& size) {
+  const uintptr_t a = (uintptr_t)p, lo = a & ~(uintptr_t)15;
+  off = (uint32_t)(a - lo);
+  size = (off + bytes + 15) & ~15u;
+  return (const void*)lo;
+}
+
+template <int PS, int PT, int PP, bool LAP, int R>
+__global__ void __launch_bounds__(kPpThreads, 1)
+    k_propagate_pipe(const __grid_constant__ LevelDev U, const __grid_constant__ LevelDev L,
+                     const __grid_constant__ InterpConsts K, const TilesDev T, double kappa,
+                     const uint32_t* __restrict__ ustart, const uint32_t* __restrict__ nunits,
+                     const uint32_t* __restrict__ urec, const double2* __restrict__ child,
+                     double2* parent, int* err) {
+  using BL = BlockLayout<PS, PT, PP>;
+  using SH = PipeShape<PS, PT, PP, R>;
+  constexpr int P = SH::P;
+  constexpr int NCT = kPpConsumers * 32;
+  constexpr uint32_t kBlkBytes = BL::Pst * 16;
+  extern __shared__ __align__(128) unsigned char pp_smem[];
+  double2* sv = reinterpret_cast<double2*>(pp_smem + (size_t)kPpStages * SH::stage_bytes);
+  double2* stf = sv + kPpCh * P;
+  uint32_t* tab = reinterpret_cast<uint32_t*>(stf + kPpConsumers * P);
+  __shared__ PipeHdr hdr[kPpStages];
+  __shared__ __align__(8) uint64_t full[kPpStages], blk[kPpStages], empty[kPpStages];
+  __shared__ double sM[PP * PP + PT * PT + PS * PS];
+  stage_fit_matrices<PS, PT, PP>(K, sM);
+  for (int i = threadIdx.x; i < kPpTab; i += blockDim.x) tab[i] = kPpEmpty;
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < kPpStages; ++i) {
+      pp_mbar_init(&full[i], 1);
+      pp_mbar_init(&blk[i], 1);
+      pp_mbar_init(&empty[i], 1);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const uint32_t nu = *nunits;
+  if (w == kPpConsumers) {
+    // ------------------------------------------------------------ producer
+    // unit records loaded one unit ahead; per stage no global loads, only
+    // the copies
+    uint32_t it = 0;
+    uint32_t rnext = blockIdx.x < nu ? urec[(size_t)blockIdx.x * kPpRec + lane] : 0u;
+    for (uint32_t u = blockIdx.x; u < nu; u += gridDim.x) {
+      const uint32_t rec = rnext;
+      if (u + gridDim.x < nu) rnext = urec[(size_t)(u + gridDim.x) * kPpRec + lane];
+      const uint32_t q0 = __shfl_sync(0xffffffffu, rec, 0), ncon = __shfl_sync(0xffffffffu, rec, 1);
+      const uint32_t cb0 = __shfl_sync(0xffffffffu, rec, 2), nch = __shfl_sync(0xffffffffu, rec, 3);
+      const uint32_t octs = __shfl_sync(0xffffffffu, rec, 4);
+      const uint32_t gid = __shfl_sync(0xffffffffu, rec, 14 + (lane & 7));
+      for (uint32_t kc = 0; kc < nch; ++kc, ++it) {
+        const int st = (int)(it % kPpStages);
+        const uint32_t round = it / kPpStages;
+        const uint32_t cbase = __shfl_sync(0xffffffffu, rec, 5 + kc);
+        const uint32_t cend = __shfl_sync(0xffffffffu, rec, 6 + kc);
+        if (round > 0) pp_wait(&empty[st], (round - 1) & 1u);
+        unsigned char* sb = pp_smem + (size_t)st * SH::stage_bytes;
+        PipeHdr& H = hdr[st];
+        const uint32_t cb = cb0 + kc;
+        const uint32_t oct = (octs >> (3 * kc)) & 7u;
+        if ((uint32_t)lane < ncon) {
+          const uint32_t tile = gid * 8 + oct;
+          H.tile[lane] = tile;
+          uint32_t off, size;
+          pp_bulk(sb + SH::off_row + lane * SH::RowBytes, T.rdat + row_field(tile, P, SH::NF, 0, 0),
+                  SH::RowBytes, &full[st]);
+          const void* src = pp_window(T.rw + (size_t)tile * P, 32 * 8, off, size);
+          pp_bulk(sb + SH::off_rw + lane * SH::RwBytes, src, size, &full[st]);
+          H.rwoff[lane] = off;
+          src = pp_window(T.rnode + (size_t)tile * P, 32 * 4, off, size);
+          pp_bulk(sb + SH::off_node + lane * SH::NodeBytes, src, size, &full[st]);
+          H.nodeoff[lane] = off;
+          src = pp_window(T.rw_cnt + tile, 4, off, size);
+          pp_bulk(sb + SH::off_cnt + lane * SH::CntBytes, src, 16, &full[st]);
+          H.rcoff[lane] = off;
+          src = pp_window(T.fl_cnt + tile, 4, off, size);
+          pp_bulk(sb + SH::off_cnt + lane * SH::CntBytes + 16, src, 16, &full[st]);
+          H.fcoff[lane] = off;
+        }
+        if (lane == 0) {
+          const uint64_t i0 = (uint64_t)cb * L.G, i1 = i0 + L.G;
+          const uint64_t w0 = i0 >> 6, nwd = ((i1 - 1) >> 6) - w0 + 1;
+          H.q0 = q0;
+          H.ncon = ncon;
+          H.cb = cb;
+          H.cbase = cbase;
+          H.ncb = cend - cbase;
+          H.last = kc + 1 == nch;
+          H.w0 = w0;
+          H.nwd = (uint32_t)nwd;
+          H.sbm = nwd <= (uint64_t)kPpBitWords;
+          if (H.sbm) {
+            uint32_t off, size;
+            const void* src = pp_window(L.bits + w0, (uint32_t)nwd * 8, off, size);
+            pp_bulk(sb + SH::off_bits, src, size, &full[st]);
+            H.bitoff = off;
+            src = pp_window(L.rank + w0, (uint32_t)nwd * 4, off, size);
+            pp_bulk(sb + SH::off_rank, src, size, &full[st]);
+            H.rankoff = off;
+          }
+        }
+        __syncwarp();
+        if (lane == 0) pp_arrive(&full[st]);
+      }
+    }
+    return;
+  }
+  // ------------------------------------------------------------ consumers
+  const int ct = threadIdx.x;  // 0 .. NCT - 1
+  // stage sequence of this CTA: (unit, child) in order; A runs one stage ahead
+  // A(i): child cones and slots of stage i, block copies issued
+  auto phaseA = [&](uint32_t i) {
+    const int st = (int)(i % kPpStages);
+    pp_wait(&full[st], (i / kPpStages) & 1u);
+    unsigned char* sb = pp_smem + (size_t)st * SH::stage_bytes;
+    PipeHdr& H = hdr[st];
+    if (w == 0) {
+      uint32_t nrow = 0, nfl = 0;
+      if ((uint32_t)lane < H.ncon) {
+        const unsigned char* cw = sb + SH::off_cnt + lane * SH::CntBytes;
+        nrow = *reinterpret_cast<const uint32_t*>(cw + H.rcoff[lane]);
+        nfl = *reinterpret_cast<const uint32_t*>(cw + 16 + H.fcoff[lane]);
+      }
+      uint32_t incl = nrow, fincl = nfl;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t v = __shfl_up_sync(0xffffffffu, incl, o);
+        const uint32_t f = __shfl_up_sync(0xffffffffu, fincl, o);
+        if (lane >= o) {
+          incl += v;
+          fincl += f;
+        }
+      }
+      if (lane < kPpCh) {
+        H.pre[lane + 1] = incl;
+        H.fpre[lane + 1] = fincl;
+      }
+      if (lane == 0) {
+        H.pre[0] = H.fpre[0] = 0;
+        H.nslot = 0;
+      }
+    }
+    pp_consumer_sync();
+    const uint32_t ncon = H.ncon, ntask = H.pre[ncon], cb = H.cb, cbase = H.cbase;
+    const bool use_tab = H.ncb <= (uint32_t)kPpTab;
+    uint32_t* task = reinterpret_cast<uint32_t*>(sb + SH::off_task);
+    uint32_t* tcq = reinterpret_cast<uint32_t*>(sb + SH::off_cq);
+    for (uint32_t t = ct; t < ntask; t += NCT) {
+      uint32_t c = 0;
+      while (c + 1 < ncon && H.pre[c + 1] <= t) ++c;
+      const uint32_t r = t - H.pre[c];
+      const uint2 rw = r < 32 ? *reinterpret_cast<const uint2*>(sb + SH::off_rw + c * SH::RwBytes +
+                                                                 H.rwoff[c] + 8 * r)
+                              : T.rw[(size_t)H.tile[c] * P + r];
+      uint32_t cq;
+      if (H.sbm) {
+        const uint64_t idx = (uint64_t)cb * L.G + rw.x;
+        const uint32_t wi = (uint32_t)((idx >> 6) - H.w0);
+        const uint64_t wd = *reinterpret_cast<const uint64_t*>(sb + SH::off_bits + H.bitoff + 8 * wi);
+        const uint32_t rk = *reinterpret_cast<const uint32_t*>(sb + SH::off_rank + H.rankoff + 4 * wi);
+        const uint64_t bit = 1ull << (idx & 63);
+        cq = (wd & bit) ? rk + (uint32_t)__popcll(wd & (bit - 1)) : kNone;
+      } else {
+        cq = find_cone(L, cb, rw.x);
+      }
+      task[t] = (c << 24) | (((rw.y >> 16) & 0xffu) << 8) | r;
+      tcq[t] = cq;
+      if (cq != kNone && use_tab) {
+        uint32_t* e = tab + (cq - cbase);
+        if (atomicCAS(e, kPpEmpty, kPpPending) == kPpEmpty) {
+          const uint32_t sl = atomicAdd(&H.nslot, 1u);
+          if (sl < (uint32_t)SH::NB)
+            pp_bulk(sb + SH::off_blk + sl * kBlkBytes, child + (size_t)cq * BL::Pst, kBlkBytes,
+                    &blk[st]);
+          *e = sl;
+        }
+      }
+    }
+    pp_consumer_sync();  // slots final, every copy of the stage issued
+    if (ct == 0) pp_arrive(&blk[st]);
+    for (uint32_t t = ct; t < ntask; t += NCT) {
+      const uint32_t cq = tcq[t];
+      uint32_t sl = kPpGlobal;
+      if (cq != kNone && use_tab) sl = min(tab[cq - cbase], kPpGlobal);
+      task[t] |= (sl < (uint32_t)SH::NB ? sl : kPpGlobal) << 16;
+    }
+    pp_consumer_sync();  // slots read: the table entries can be cleared
+    if (use_tab)
+      for (uint32_t t = ct; t < ntask; t += NCT)
+        if (tcq[t] != kNone) tab[tcq[t] - cbase] = kPpEmpty;
+  };
+  // B(i): evaluate stage i, release it; returns whether it ended a unit
+  auto phaseB = [&](uint32_t i) -> bool {
+    const int st = (int)(i % kPpStages);
+    pp_wait(&blk[st], (i / kPpStages) & 1u);
+    const unsigned char* sb = pp_smem + (size_t)st * SH::stage_bytes;
+    const PipeHdr& H = hdr[st];
+    const uint32_t* task = reinterpret_cast<const uint32_t*>(sb + SH::off_task);
+    const uint32_t* tcq = reinterpret_cast<const uint32_t*>(sb + SH::off_cq);
+    const uint32_t ncon = H.ncon, cb = H.cb, q0 = H.q0, ntask = H.pre[ncon];
+    for (uint32_t t = ct; t < ntask; t += NCT) {
+      const uint32_t cq = tcq[t];
+      if (cq == kNone) {
+        raise_err(err, kErrPropCover);
+        continue;
+      }
+      const uint32_t pk = task[t];
+      const int c = (int)(pk >> 24), r = (int)(pk & 0xffu), cnt = (int)((pk >> 8) & 0xffu);
+      const uint32_t slot = (pk >> 16) & 0xffu;
+      const uint32_t tl = H.tile[c];
+      double rv[SH::NF];
+      if (r < 32) {
+        const double* rd = reinterpret_cast<const double*>(sb + SH::off_row + c * SH::RowBytes) + r;
+#pragma unroll
+        for (int f = 0; f < SH::NF; ++f) rv[f] = rd[32 * f];
+      } else {
+        const double* rd = T.rdat + row_field(tl, P, SH::NF, r, 0);
+#pragma unroll
+        for (int f = 0; f < SH::NF; ++f) rv[f] = __ldg(rd + 32 * f);
+      }
+      double ts[R], tt[R], tp[R];
+#pragma unroll
+      for (int j = 0; j < R; ++j) {
+        const bool on = j < cnt;
+        ts[j] = on ? rv[0 * R + j] : 0.0;
+        tt[j] = on ? rv[1 * R + j] : 0.0;
+        tp[j] = on ? rv[2 * R + j] : 0.0;
+      }
+      double vr[R], vi[R];
+      if (slot != kPpGlobal)
+        eval_block_multi<PS, PT, PP, R, true>(
+            reinterpret_cast<const double2*>(sb + SH::off_blk + slot * kBlkBytes), ts, tt, tp, vr, vi);
+      else
+        eval_block_multi<PS, PT, PP, R>(child + (size_t)cq * BL::Pst, ts, tt, tp, vr, vi);
+      const uint32_t nodes =
+          r < 32 ? *reinterpret_cast<const uint32_t*>(sb + SH::off_node + c * SH::NodeBytes +
+                                                      H.nodeoff[c] + 4 * r)
+                 : __ldg(T.rnode + (size_t)tl * P + r);
+      double2* acc = sv + c * P;
+#pragma unroll
+      for (int j = 0; j < R; ++j) {
+        if (j < cnt) {
+          const double tr = rv[3 * R + j], ti = rv[4 * R + j];
+          const int m = (int)((nodes >> (8 * j)) & 0xffu);
+          double2 v = acc[m];
+          v.x = fma(vr[j], tr, fma(-vi[j], ti, v.x));
+          v.y = fma(vr[j], ti, fma(vi[j], tr, v.y));
+          acc[m] = v;
+        }
+      }
+    }
+    // flagged nodes: the exact per-box path
+    const uint32_t nflag = H.fpre[ncon];
+    for (uint32_t f = ct; f < nflag; f += NCT) {
+      uint32_t c = 0;
+      while (c + 1 < ncon && H.fpre[c + 1] <= f) ++c;
+      const uint32_t tl = H.tile[c];
+      const uint32_t q = q0 + c;
+      const uint32_t pb = U.cone_box[q];
+      const int m = T.fl_node[(size_t)tl * P + (f - H.fpre[c])];
+      const int jp = m % PP, jt = (m / PP) % PT, js = m / (PP * PT);
+      const SegMid sg = segment_mid(U, U.cone_gamma[q]);
+      const double pcx = U.cx[pb], pcy = U.cy[pb], pcz = U.cz[pb];
+      double x, y, z;
+      node_position(sg, U.rad, pcx, pcy, pcz, K.ns[js], K.nt[jt], K.np[jp], x, y, z);
+      const double ux = x - pcx, uy = y - pcy, uz = z - pcz;
+      const double rp = sqrt(fma(uz, uz, fma(uy, uy, ux * ux)));
+      Loc lo;
+      const int er = locate_fast(L, L.cx[cb], L.cy[cb], L.cz[cb], x, y, z, lo);
+      if (er) {
+        raise_err(err, er);
+        continue;
+      }
+      const uint32_t cq = find_cone(L, cb, lo.gamma);
+      if (cq == kNone) {
+        raise_err(err, kErrPropCover);
+        continue;
+      }
+      double vr, vi;
+      eval_block<PS, PT, PP>(child + (size_t)cq * BL::Pst, lo.ts, lo.tt, lo.tp, vr, vi);
+      const double ratio = rp * lo.rinv;
+      double sn = 0.0, cn = 1.0;
+      if (!LAP) sincos_fast(kappa * (lo.r - rp), sn, cn);
+      const double tr = ratio * cn, ti = ratio * sn;
+      double2* acc = sv + c * P;
+      double2 v = acc[m];
+      v.x = fma(vr, tr, fma(-vi, ti, v.x));
+      v.y = fma(vr, ti, fma(vi, tr, v.y));
+      acc[m] = v;
+    }
+    const bool last = H.last;
+    pp_consumer_sync();  // every row of stage i is in sv; the stage is free
+    if (ct == 0) pp_arrive(&empty[st]);
+    return last;
+  };
+  // number of stages of this CTA (units x children), for the lookahead
+  uint32_t nstage = 0;
+  for (uint32_t u = blockIdx.x; u < nu; u += gridDim.x) nstage += urec[(size_t)u * kPpRec + 3];
+  for (uint32_t i = ct; i < kPpCh * P; i += NCT) sv[i] = make_double2(0.0, 0.0);
+  if (nstage) phaseA(0);
+  uint32_t u = blockIdx.x;
+  for (uint32_t i = 0; i < nstage; ++i) {
+    if (i + 1 < nstage) phaseA(i + 1);
+    const uint32_t q0 = hdr[i % kPpStages].q0, ncon = hdr[i % kPpStages].ncon;
+    if (phaseB(i)) {
+      // fit the unit's cones: consumer warp w takes cones w, w + kPpConsumers, ...
+      double2* sf = stf + (size_t)w * P;
+      for (uint32_t c = w; c < ncon; c += kPpConsumers)
+        fit_cones_warp<PS, PT, PP>(sM, sv + c * P, sf, 1, parent + (size_t)(q0 + c) * BL::Pst, err);
+      pp_consumer_sync();
+      for (uint32_t k = ct; k < kPpCh * P; k += NCT) sv[k] = make_double2(0.0, 0.0);
+      pp_consumer_sync();
+      u += gridDim.x;
+    }
+  }
+}
+
 // K3 streaming (default where the orders allow it): the child block stays in
 // registers while the nodes that fall into it stream past.  A child cone of
 // a parent box collects ~25 nodes of each parent cone (the child's cone
@@ -1616,20 +2099,76 @@ bool launch_propagation_mma(ifgf_plan* P, int d, uint32_t qb, uint32_t qe, const
                             double2* parent, cudaStream_t s) {
   PropTiles& T = P->tiles[d];
   if (P->prop_kernel == IFGF_PROP_FLY ||
-      ((P->prop_kernel == IFGF_PROP_ROWS || P->prop_kernel == IFGF_PROP_STREAM) && !T.enabled))
+      ((P->prop_kernel == IFGF_PROP_ROWS || P->prop_kernel == IFGF_PROP_STREAM ||
+        P->prop_kernel == IFGF_PROP_PIPE) &&
+       !T.enabled))
     return launch_propagation_fly(P, d, qb, qe, child, parent, s);
   if (!T.enabled) return false;
   if (P->prop_kernel == IFGF_PROP_DMMA && !T.rt) build_dmma_extras(P, d, s);
   if (T.nchunks == 0 && P->prop_kernel == IFGF_PROP_DMMA) return false;
   const bool full = qb == 0 && qe == P->lv[d - 1].nc;
-  if (P->prop_kernel == IFGF_PROP_ROWS || P->prop_kernel == IFGF_PROP_STREAM) {
-    const bool stream = P->prop_kernel == IFGF_PROP_STREAM;
+  bool piped = false;
+  if (P->prop_kernel == IFGF_PROP_PIPE && full &&
+      dispatch_rows_orders(P->K.ps, P->K.pt, P->K.pp, [&](auto A, auto B, auto C) {
+        constexpr int PS = decltype(A)::value, PT = decltype(B)::value, PP = decltype(C)::value;
+        // orders whose stages do not fit in shared memory run the rows kernel
+        constexpr size_t kMaxSmem = 220 * 1024;
+        if constexpr (PipeShape<PS, PT, PP, 2>::smem > kMaxSmem ||
+                      PipeShape<PS, PT, PP, 3>::smem > kMaxSmem) {
+          return;
+        } else {
+        const Level& U = P->lv[d - 1];
+        const Level& L = P->lv[d];
+        if (!T.ustart) {  // units, built on first use (device only, no host sync)
+          uint32_t* cnt = P->alloc<uint32_t>(U.nb + 1);
+          uint32_t* off = P->alloc<uint32_t>(U.nb + 1);
+          T.ustart = P->alloc<uint32_t>((size_t)U.nc / kPpCh + U.nb + 2);
+          T.nunits = P->alloc<uint32_t>(1);
+          k_pp_units_count<<<nblk(U.nb + 1), 256, 0, s>>>(U.dev(), kPpCh, cnt);
+          size_t tb = 0;
+          cub::DeviceScan::ExclusiveSum(nullptr, tb, cnt, off, (int)(U.nb + 1), s);
+          void* tmp = P->alloc<unsigned char>(tb);
+          IFGF_CUDA(cub::DeviceScan::ExclusiveSum(tmp, tb, cnt, off, (int)(U.nb + 1), s));
+          k_pp_units_fill<<<nblk(U.nb + 1), 256, 0, s>>>(U.dev(), kPpCh, off, T.ustart, T.nunits);
+          const size_t umax = (size_t)U.nc / kPpCh + U.nb + 1;
+          T.urec = P->alloc<uint32_t>(umax * kPpRec);
+          k_pp_units_info<<<nblk(umax), 256, 0, s>>>(U.dev(), L.dev(), T.cone_gidx, T.ustart,
+                                                     T.nunits, T.urec);
+          IFGF_CUDA(cudaGetLastError());
+          P->launches += 3;
+        }
+        auto launch = [&](auto kern, size_t sm) {
+          IFGF_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+          kern<<<148, kPpThreads, sm, s>>>(U.dev(), L.dev(), P->K, tiles_dev(T), P->kappa, T.ustart,
+                                           T.nunits, T.urec, child, parent, P->err);
+          IFGF_CUDA(cudaGetLastError());
+        };
+        const bool lap = P->kappa == 0.0;
+        if (T.row_nodes == 2) {
+          const size_t sm = PipeShape<PS, PT, PP, 2>::smem;
+          lap ? launch(k_propagate_pipe<PS, PT, PP, true, 2>, sm)
+              : launch(k_propagate_pipe<PS, PT, PP, false, 2>, sm);
+        } else {
+          const size_t sm = PipeShape<PS, PT, PP, 3>::smem;
+          lap ? launch(k_propagate_pipe<PS, PT, PP, true, 3>, sm)
+              : launch(k_propagate_pipe<PS, PT, PP, false, 3>, sm);
+        }
+        ++P->launches;
+        piped = true;
+        }
+      }) &&
+      piped)
+    return true;
+  if (P->prop_kernel == IFGF_PROP_ROWS || P->prop_kernel == IFGF_PROP_STREAM ||
+      P->prop_kernel == IFGF_PROP_PIPE) {
     const Level& U = P->lv[d - 1];
     const Level& L = P->lv[d];
     const InterpConsts& K = P->K;
     return dispatch_rows_orders(K.ps, K.pt, K.pp, [&](auto A, auto B, auto C) {
       constexpr int PS = decltype(A)::value, PT = decltype(B)::value, PP = decltype(C)::value;
       constexpr int Pn = PS * PT * PP;
+      // orders whose planes do not fit in registers run the rows kernel
+      const bool stream = P->prop_kernel == IFGF_PROP_STREAM && StreamShape<PS, PT, PP>::ok;
       constexpr int NW = kRowThreads / 32;
       static const int cpw_env = [] {
         const char* v = std::getenv("IFGF_ROWS_CPW");

@@ -286,7 +286,7 @@ class Plan:
         """Run all apply kernels on one stream (exclusive per-pass timings)."""
         check(lib.ifgf_plan_set_option(self._h, 1, 1 if on else 0))
 
-    PROP_NODE, PROP_TILES, PROP_DMMA, PROP_ROWS, PROP_FLY, PROP_STREAM = 0, 1, 2, 3, 4, 5
+    PROP_NODE, PROP_TILES, PROP_DMMA, PROP_ROWS, PROP_FLY, PROP_STREAM, PROP_PIPE = 0, 1, 2, 3, 4, 5, 6
 
     NEAR_POINT, NEAR_BOX = 0, 1
 

@@ -149,9 +149,14 @@ def test_propagation_kernels_agree(built):
     fly) compute the same operator up to rounding."""
     case, pc, cfg, ep, op, plan, prob = built
     res = []
-    for kind in (plan.PROP_NODE, plan.PROP_TILES, plan.PROP_DMMA, plan.PROP_ROWS, plan.PROP_FLY):
+    kinds = (plan.PROP_NODE, plan.PROP_TILES, plan.PROP_DMMA, plan.PROP_ROWS, plan.PROP_FLY,
+             plan.PROP_STREAM, plan.PROP_PIPE)
+    for kind in kinds:
         plan.set_prop_kernel(kind)
         res.append(plan.apply(pc.a_re, pc.a_im)[:2])
     plan.set_prop_kernel(plan.PROP_ROWS)
     for r in res[1:]:
         assert rel_l2(r[0], r[1], res[0][0], res[0][1]) <= 1e-13
+    # the pipelined kernel sums exactly what the rows kernel sums
+    rows, pipe = res[kinds.index(plan.PROP_ROWS)], res[kinds.index(plan.PROP_PIPE)]
+    assert np.array_equal(rows[0], pipe[0]) and np.array_equal(rows[1], pipe[1])
