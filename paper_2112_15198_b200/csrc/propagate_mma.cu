@@ -968,20 +968,17 @@ __global__ void __launch_bounds__(kRowThreads, IFGF_ROWS_MINB)
 // the first 32 of a tile, cones beyond the slot capacity and bitmaps wider
 // than kPpBitWords fall back to global memory; flagged nodes take the exact
 // per-box path.
-#ifndef IFGF_PP_CONSUMERS
-#define IFGF_PP_CONSUMERS 8
+#ifndef IFGF_PP_CH
+#define IFGF_PP_CH 11
 #endif
 #ifndef IFGF_PP_STAGES
 #define IFGF_PP_STAGES 3
 #endif
-constexpr int kPpConsumers = IFGF_PP_CONSUMERS;
+constexpr int kPpCh = IFGF_PP_CH;          // parent cones per unit (<= 18: unit records)
+constexpr int kPpConsumers = IFGF_PP_CH;   // one consumer warp per unit cone
 constexpr int kPpThreads = (kPpConsumers + 1) * 32;
 constexpr int kPpStages = IFGF_PP_STAGES;
-#ifndef IFGF_PP_CH
-#define IFGF_PP_CH 8
-#endif
-constexpr int kPpCh = IFGF_PP_CH;  // parent cones per unit (<= 8: unit records)
-static_assert(kPpCh <= 8, "unit records hold 8 cones");
+static_assert(kPpCh <= 18, "unit records hold 18 cones");
 constexpr int kPpBitWords = 72;   // staged bitmap words per child box
 constexpr int kPpTab = 2048;      // child cones covered by the slot table
 constexpr uint32_t kPpEmpty = 0xffffffffu, kPpPending = 0xfffffffeu;
@@ -1018,9 +1015,6 @@ __device__ __forceinline__ void pp_bulk(void* dst, const void* src, uint32_t byt
       "l"(src), "r"(bytes), "r"((uint32_t)__cvta_generic_to_shared(m))
       : "memory");
 }
-__device__ __forceinline__ void pp_consumer_sync() {
-  asm volatile("bar.sync 1, %0;" ::"n"(kPpConsumers * 32) : "memory");
-}
 
 // Units of <= ch consecutive cones of one parent box, the box's cones split
 // evenly: unit_start[u] .. unit_start[u + 1].
@@ -1048,7 +1042,7 @@ __global__ void k_pp_units_fill(const __grid_constant__ LevelDev U, uint32_t ch,
 // Per-unit record for the producer (32 words, one coalesced load per unit):
 // [0] q0, [1] ncon, [2] first child, [3] children, [4] child octants (3 bits
 // each), [5 .. 5+nch] the children's first cone ordinals (box_cone), [14 ..
-// 14+ncon) the cones' gamma indices.
+// 14+ncon) the cones' gamma indices (ncon <= 18).
 constexpr int kPpRec = 32;
 __global__ void k_pp_units_info(const __grid_constant__ LevelDev U, const __grid_constant__ LevelDev L,
                                 const uint32_t* __restrict__ gidx, const uint32_t* __restrict__ ustart,
@@ -1080,7 +1074,7 @@ struct PipeShape {
   static constexpr int NodeBytes = 32 * 4 + 16;
   static constexpr int CntBytes = 32;           // rw_cnt and fl_cnt words, 16 B each
   static constexpr int BitBytes = kPpBitWords * 8 + 16, RankBytes = kPpBitWords * 4 + 16;
-  static constexpr int NB = P <= 80 ? 16 : 4;   // block slots per stage
+  static constexpr int NB = P <= 80 ? 12 : 4;   // block slots per stage
   static constexpr int MaxTask = kPpCh * P;
   static constexpr int off_row = 0;
   static constexpr int off_rw = off_row + kPpCh * RowBytes;
@@ -1090,12 +1084,12 @@ struct PipeShape {
   static constexpr int off_rank = off_bits + BitBytes;
   static constexpr int off_blk = (off_rank + RankBytes + 15) / 16 * 16;
   static constexpr int off_task = off_blk + NB * Pst * 16;
-  static constexpr int off_cq = off_task + MaxTask * 4;
+  static constexpr int off_cq = (off_task + MaxTask + 15) / 16 * 16;  // u8 slots, then u32 cones
   static constexpr int stage_bytes = ((off_cq + MaxTask * 4) + 127) / 128 * 128;
   static constexpr size_t smem = (size_t)kPpStages * stage_bytes  // stages
                                  + (size_t)kPpCh * P * 16          // sv
-                                 + (size_t)kPpConsumers * P * 16   // fit scratch
                                  + (size_t)kPpTab * 4;             // slot table
+  static constexpr bool fits = RowBytes >= P * 16;  // fit scratch in the cone's row chunk
 };
 
 struct PipeHdr {
@@ -1104,7 +1098,7 @@ struct PipeHdr {
   uint32_t tile[kPpCh], rwoff[kPpCh], nodeoff[kPpCh], rcoff[kPpCh], fcoff[kPpCh];
   uint32_t bitoff, rankoff;
   // consumers
-  uint32_t pre[kPpCh + 1], fpre[kPpCh + 1], nslot;
+  uint32_t nslot;
 };
 
 // 16-byte-aligned window [lo, lo + size) covering [p, p + bytes)
@@ -1126,12 +1120,10 @@ __global__ void __launch_bounds__(kPpThreads, 1)
   using BL = BlockLayout<PS, PT, PP>;
   using SH = PipeShape<PS, PT, PP, R>;
   constexpr int P = SH::P;
-  constexpr int NCT = kPpConsumers * 32;
   constexpr uint32_t kBlkBytes = BL::Pst * 16;
   extern __shared__ __align__(128) unsigned char pp_smem[];
   double2* sv = reinterpret_cast<double2*>(pp_smem + (size_t)kPpStages * SH::stage_bytes);
-  double2* stf = sv + kPpCh * P;
-  uint32_t* tab = reinterpret_cast<uint32_t*>(stf + kPpConsumers * P);
+  uint32_t* tab = reinterpret_cast<uint32_t*>(sv + kPpCh * P);
   __shared__ PipeHdr hdr[kPpStages];
   __shared__ __align__(8) uint64_t full[kPpStages], blk[kPpStages], empty[kPpStages];
   __shared__ double sM[PP * PP + PT * PT + PS * PS];
@@ -1140,8 +1132,8 @@ __global__ void __launch_bounds__(kPpThreads, 1)
   if (threadIdx.x == 0) {
     for (int i = 0; i < kPpStages; ++i) {
       pp_mbar_init(&full[i], 1);
-      pp_mbar_init(&blk[i], 1);
-      pp_mbar_init(&empty[i], 1);
+      pp_mbar_init(&blk[i], kPpConsumers);
+      pp_mbar_init(&empty[i], kPpConsumers);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -1160,7 +1152,7 @@ __global__ void __launch_bounds__(kPpThreads, 1)
       const uint32_t q0 = __shfl_sync(0xffffffffu, rec, 0), ncon = __shfl_sync(0xffffffffu, rec, 1);
       const uint32_t cb0 = __shfl_sync(0xffffffffu, rec, 2), nch = __shfl_sync(0xffffffffu, rec, 3);
       const uint32_t octs = __shfl_sync(0xffffffffu, rec, 4);
-      const uint32_t gid = __shfl_sync(0xffffffffu, rec, 14 + (lane & 7));
+      const uint32_t gid = __shfl_sync(0xffffffffu, rec, 14 + min(lane, kPpCh - 1));
       for (uint32_t kc = 0; kc < nch; ++kc, ++it) {
         const int st = (int)(it % kPpStages);
         const uint32_t round = it / kPpStages;
@@ -1196,6 +1188,7 @@ __global__ void __launch_bounds__(kPpThreads, 1)
           H.q0 = q0;
           H.ncon = ncon;
           H.cb = cb;
+          H.nslot = 0;
           H.cbase = cbase;
           H.ncb = cend - cbase;
           H.last = kc + 1 == nch;
@@ -1219,214 +1212,210 @@ __global__ void __launch_bounds__(kPpThreads, 1)
     return;
   }
   // ------------------------------------------------------------ consumers
-  const int ct = threadIdx.x;  // 0 .. NCT - 1
-  // stage sequence of this CTA: (unit, child) in order; A runs one stage ahead
-  // A(i): child cones and slots of stage i, block copies issued
+  // consumer warp w owns cone w of every unit: it alone writes sv[w], so the
+  // warps need no barrier among themselves -- they meet only at the stage
+  // mbarriers (blocks staged by all eight, stage released by all eight).
+  static_assert(kPpConsumers == kPpCh, "one consumer warp per unit cone");
+  const uint32_t c = (uint32_t)w;
+  double2* acc = sv + (size_t)c * P;
+  // A(i): this cone's rows of stage i -> child cones, one slot per distinct
+  // cone (tagged table entries: tag = stage sequence, no clearing), copies
   auto phaseA = [&](uint32_t i) {
     const int st = (int)(i % kPpStages);
     pp_wait(&full[st], (i / kPpStages) & 1u);
     unsigned char* sb = pp_smem + (size_t)st * SH::stage_bytes;
     PipeHdr& H = hdr[st];
-    if (w == 0) {
-      uint32_t nrow = 0, nfl = 0;
-      if ((uint32_t)lane < H.ncon) {
-        const unsigned char* cw = sb + SH::off_cnt + lane * SH::CntBytes;
-        nrow = *reinterpret_cast<const uint32_t*>(cw + H.rcoff[lane]);
-        nfl = *reinterpret_cast<const uint32_t*>(cw + 16 + H.fcoff[lane]);
-      }
-      uint32_t incl = nrow, fincl = nfl;
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const uint32_t v = __shfl_up_sync(0xffffffffu, incl, o);
-        const uint32_t f = __shfl_up_sync(0xffffffffu, fincl, o);
-        if (lane >= o) {
-          incl += v;
-          fincl += f;
+    if (c < H.ncon) {
+      const unsigned char* cw = sb + SH::off_cnt + c * SH::CntBytes;
+      const uint32_t nrow = *reinterpret_cast<const uint32_t*>(cw + H.rcoff[c]);
+      const uint32_t cb = H.cb, cbase = H.cbase;
+      const bool use_tab = H.ncb <= (uint32_t)kPpTab;
+      const uint32_t tag = (i & 0x7fffffu) << 9;
+      uint8_t* tslot = sb + SH::off_task + c * P;
+      uint32_t* tcq = reinterpret_cast<uint32_t*>(sb + SH::off_cq) + c * P;
+      for (uint32_t r0 = 0; r0 < nrow; r0 += 32) {
+        const uint32_t r = r0 + lane;
+        uint32_t cq = kNone;
+        if (r < nrow) {
+          const uint2 rw = r < 32 ? *reinterpret_cast<const uint2*>(sb + SH::off_rw + c * SH::RwBytes +
+                                                                     H.rwoff[c] + 8 * r)
+                                  : T.rw[(size_t)H.tile[c] * P + r];
+          if (H.sbm) {
+            const uint64_t idx = (uint64_t)cb * L.G + rw.x;
+            const uint32_t wi = (uint32_t)((idx >> 6) - H.w0);
+            const uint64_t wd = *reinterpret_cast<const uint64_t*>(sb + SH::off_bits + H.bitoff + 8 * wi);
+            const uint32_t rk = *reinterpret_cast<const uint32_t*>(sb + SH::off_rank + H.rankoff + 4 * wi);
+            const uint64_t bit = 1ull << (idx & 63);
+            cq = (wd & bit) ? rk + (uint32_t)__popcll(wd & (bit - 1)) : kNone;
+          } else {
+            cq = find_cone(L, cb, rw.x);
+          }
         }
-      }
-      if (lane < kPpCh) {
-        H.pre[lane + 1] = incl;
-        H.fpre[lane + 1] = fincl;
-      }
-      if (lane == 0) {
-        H.pre[0] = H.fpre[0] = 0;
-        H.nslot = 0;
-      }
-    }
-    pp_consumer_sync();
-    const uint32_t ncon = H.ncon, ntask = H.pre[ncon], cb = H.cb, cbase = H.cbase;
-    const bool use_tab = H.ncb <= (uint32_t)kPpTab;
-    uint32_t* task = reinterpret_cast<uint32_t*>(sb + SH::off_task);
-    uint32_t* tcq = reinterpret_cast<uint32_t*>(sb + SH::off_cq);
-    for (uint32_t t = ct; t < ntask; t += NCT) {
-      uint32_t c = 0;
-      while (c + 1 < ncon && H.pre[c + 1] <= t) ++c;
-      const uint32_t r = t - H.pre[c];
-      const uint2 rw = r < 32 ? *reinterpret_cast<const uint2*>(sb + SH::off_rw + c * SH::RwBytes +
-                                                                 H.rwoff[c] + 8 * r)
-                              : T.rw[(size_t)H.tile[c] * P + r];
-      uint32_t cq;
-      if (H.sbm) {
-        const uint64_t idx = (uint64_t)cb * L.G + rw.x;
-        const uint32_t wi = (uint32_t)((idx >> 6) - H.w0);
-        const uint64_t wd = *reinterpret_cast<const uint64_t*>(sb + SH::off_bits + H.bitoff + 8 * wi);
-        const uint32_t rk = *reinterpret_cast<const uint32_t*>(sb + SH::off_rank + H.rankoff + 4 * wi);
-        const uint64_t bit = 1ull << (idx & 63);
-        cq = (wd & bit) ? rk + (uint32_t)__popcll(wd & (bit - 1)) : kNone;
-      } else {
-        cq = find_cone(L, cb, rw.x);
-      }
-      task[t] = (c << 24) | (((rw.y >> 16) & 0xffu) << 8) | r;
-      tcq[t] = cq;
-      if (cq != kNone && use_tab) {
-        uint32_t* e = tab + (cq - cbase);
-        if (atomicCAS(e, kPpEmpty, kPpPending) == kPpEmpty) {
-          const uint32_t sl = atomicAdd(&H.nslot, 1u);
-          if (sl < (uint32_t)SH::NB)
-            pp_bulk(sb + SH::off_blk + sl * kBlkBytes, child + (size_t)cq * BL::Pst, kBlkBytes,
-                    &blk[st]);
-          *e = sl;
+        // one claim per distinct cone of the warp; the leader resolves it
+        const unsigned grp = __match_any_sync(0xffffffffu, cq);
+        const int leader = __ffs(grp) - 1;
+        uint32_t slot = kPpGlobal;
+        if (leader == lane && cq != kNone && use_tab) {
+          uint32_t* e = tab + (cq - cbase);
+          for (;;) {
+            const uint32_t old = *(volatile uint32_t*)e;
+            if ((old & ~0x1ffu) == tag) {  // this stage's entry
+              if (old & 0x100u) continue;   // claimed, slot not yet written
+              slot = old & 0xffu;
+              break;
+            }
+            if (atomicCAS(e, old, tag | 0x100u) == old) {
+              const uint32_t sl = atomicAdd(&H.nslot, 1u);
+              if (sl < (uint32_t)SH::NB) {
+                pp_bulk(sb + SH::off_blk + sl * kBlkBytes, child + (size_t)cq * BL::Pst, kBlkBytes,
+                        &blk[st]);
+                slot = sl;
+              }
+              __threadfence_block();
+              atomicExch(e, tag | slot);
+              break;
+            }
+          }
+        }
+        slot = __shfl_sync(0xffffffffu, slot, leader);
+        if (r < nrow) {
+          tslot[r] = (uint8_t)slot;
+          tcq[r] = cq;
         }
       }
     }
-    pp_consumer_sync();  // slots final, every copy of the stage issued
-    if (ct == 0) pp_arrive(&blk[st]);
-    for (uint32_t t = ct; t < ntask; t += NCT) {
-      const uint32_t cq = tcq[t];
-      uint32_t sl = kPpGlobal;
-      if (cq != kNone && use_tab) sl = min(tab[cq - cbase], kPpGlobal);
-      task[t] |= (sl < (uint32_t)SH::NB ? sl : kPpGlobal) << 16;
-    }
-    pp_consumer_sync();  // slots read: the table entries can be cleared
-    if (use_tab)
-      for (uint32_t t = ct; t < ntask; t += NCT)
-        if (tcq[t] != kNone) tab[tcq[t] - cbase] = kPpEmpty;
+    __syncwarp();
+    if (lane == 0) pp_arrive(&blk[st]);
   };
-  // B(i): evaluate stage i, release it; returns whether it ended a unit
+  // B(i): evaluate this cone's rows of stage i, release the stage; returns
+  // whether it ended a unit (the cone is then fitted)
   auto phaseB = [&](uint32_t i) -> bool {
     const int st = (int)(i % kPpStages);
     pp_wait(&blk[st], (i / kPpStages) & 1u);
     const unsigned char* sb = pp_smem + (size_t)st * SH::stage_bytes;
     const PipeHdr& H = hdr[st];
-    const uint32_t* task = reinterpret_cast<const uint32_t*>(sb + SH::off_task);
-    const uint32_t* tcq = reinterpret_cast<const uint32_t*>(sb + SH::off_cq);
-    const uint32_t ncon = H.ncon, cb = H.cb, q0 = H.q0, ntask = H.pre[ncon];
-    for (uint32_t t = ct; t < ntask; t += NCT) {
-      const uint32_t cq = tcq[t];
-      if (cq == kNone) {
-        raise_err(err, kErrPropCover);
-        continue;
-      }
-      const uint32_t pk = task[t];
-      const int c = (int)(pk >> 24), r = (int)(pk & 0xffu), cnt = (int)((pk >> 8) & 0xffu);
-      const uint32_t slot = (pk >> 16) & 0xffu;
+    const bool last = H.last;
+    const uint32_t q0 = H.q0, ncon = H.ncon, cb = H.cb;
+    if (c < ncon) {
+      const unsigned char* cw = sb + SH::off_cnt + c * SH::CntBytes;
+      const uint32_t nrow = *reinterpret_cast<const uint32_t*>(cw + H.rcoff[c]);
+      const uint32_t nfl = *reinterpret_cast<const uint32_t*>(cw + 16 + H.fcoff[c]);
       const uint32_t tl = H.tile[c];
-      double rv[SH::NF];
-      if (r < 32) {
-        const double* rd = reinterpret_cast<const double*>(sb + SH::off_row + c * SH::RowBytes) + r;
+      const uint8_t* tslot = sb + SH::off_task + c * P;
+      const uint32_t* tcq = reinterpret_cast<const uint32_t*>(sb + SH::off_cq) + c * P;
+      for (uint32_t r = lane; r < nrow; r += 32) {
+        const uint32_t cq = tcq[r];
+        if (cq == kNone) {
+          raise_err(err, kErrPropCover);
+          continue;
+        }
+        const uint32_t slot = tslot[r];
+        double rv[SH::NF];
+        uint32_t nodes;
+        if (r < 32) {
+          const double* rd = reinterpret_cast<const double*>(sb + SH::off_row + c * SH::RowBytes) + r;
 #pragma unroll
-        for (int f = 0; f < SH::NF; ++f) rv[f] = rd[32 * f];
-      } else {
-        const double* rd = T.rdat + row_field(tl, P, SH::NF, r, 0);
+          for (int f = 0; f < SH::NF; ++f) rv[f] = rd[32 * f];
+          nodes = *reinterpret_cast<const uint32_t*>(sb + SH::off_node + c * SH::NodeBytes +
+                                                     H.nodeoff[c] + 4 * r);
+        } else {
+          const double* rd = T.rdat + row_field(tl, P, SH::NF, (int)r, 0);
 #pragma unroll
-        for (int f = 0; f < SH::NF; ++f) rv[f] = __ldg(rd + 32 * f);
-      }
-      double ts[R], tt[R], tp[R];
+          for (int f = 0; f < SH::NF; ++f) rv[f] = __ldg(rd + 32 * f);
+          nodes = __ldg(T.rnode + (size_t)tl * P + r);
+        }
+        const uint2 rw = r < 32 ? *reinterpret_cast<const uint2*>(sb + SH::off_rw + c * SH::RwBytes +
+                                                                   H.rwoff[c] + 8 * r)
+                                : T.rw[(size_t)tl * P + r];
+        const int cnt = (int)((rw.y >> 16) & 0xffu);
+        double ts[R], tt[R], tp[R];
 #pragma unroll
-      for (int j = 0; j < R; ++j) {
-        const bool on = j < cnt;
-        ts[j] = on ? rv[0 * R + j] : 0.0;
-        tt[j] = on ? rv[1 * R + j] : 0.0;
-        tp[j] = on ? rv[2 * R + j] : 0.0;
-      }
-      double vr[R], vi[R];
-      if (slot != kPpGlobal)
-        eval_block_multi<PS, PT, PP, R, true>(
-            reinterpret_cast<const double2*>(sb + SH::off_blk + slot * kBlkBytes), ts, tt, tp, vr, vi);
-      else
-        eval_block_multi<PS, PT, PP, R>(child + (size_t)cq * BL::Pst, ts, tt, tp, vr, vi);
-      const uint32_t nodes =
-          r < 32 ? *reinterpret_cast<const uint32_t*>(sb + SH::off_node + c * SH::NodeBytes +
-                                                      H.nodeoff[c] + 4 * r)
-                 : __ldg(T.rnode + (size_t)tl * P + r);
-      double2* acc = sv + c * P;
+        for (int j = 0; j < R; ++j) {
+          const bool on = j < cnt;
+          ts[j] = on ? rv[0 * R + j] : 0.0;
+          tt[j] = on ? rv[1 * R + j] : 0.0;
+          tp[j] = on ? rv[2 * R + j] : 0.0;
+        }
+        double vr[R], vi[R];
+        if (slot != kPpGlobal)
+          eval_block_multi<PS, PT, PP, R, true>(
+              reinterpret_cast<const double2*>(sb + SH::off_blk + slot * kBlkBytes), ts, tt, tp, vr, vi);
+        else
+          eval_block_multi<PS, PT, PP, R>(child + (size_t)cq * BL::Pst, ts, tt, tp, vr, vi);
 #pragma unroll
-      for (int j = 0; j < R; ++j) {
-        if (j < cnt) {
-          const double tr = rv[3 * R + j], ti = rv[4 * R + j];
-          const int m = (int)((nodes >> (8 * j)) & 0xffu);
-          double2 v = acc[m];
-          v.x = fma(vr[j], tr, fma(-vi[j], ti, v.x));
-          v.y = fma(vr[j], ti, fma(vi[j], tr, v.y));
-          acc[m] = v;
+        for (int j = 0; j < R; ++j) {
+          if (j < cnt) {
+            const double tr = rv[3 * R + j], ti = rv[4 * R + j];
+            const int m = (int)((nodes >> (8 * j)) & 0xffu);
+            double2 v = acc[m];
+            v.x = fma(vr[j], tr, fma(-vi[j], ti, v.x));
+            v.y = fma(vr[j], ti, fma(vi[j], tr, v.y));
+            acc[m] = v;
+          }
         }
       }
-    }
-    // flagged nodes: the exact per-box path
-    const uint32_t nflag = H.fpre[ncon];
-    for (uint32_t f = ct; f < nflag; f += NCT) {
-      uint32_t c = 0;
-      while (c + 1 < ncon && H.fpre[c + 1] <= f) ++c;
-      const uint32_t tl = H.tile[c];
+      // flagged nodes of this cone: the exact per-box path
       const uint32_t q = q0 + c;
-      const uint32_t pb = U.cone_box[q];
-      const int m = T.fl_node[(size_t)tl * P + (f - H.fpre[c])];
-      const int jp = m % PP, jt = (m / PP) % PT, js = m / (PP * PT);
-      const SegMid sg = segment_mid(U, U.cone_gamma[q]);
-      const double pcx = U.cx[pb], pcy = U.cy[pb], pcz = U.cz[pb];
-      double x, y, z;
-      node_position(sg, U.rad, pcx, pcy, pcz, K.ns[js], K.nt[jt], K.np[jp], x, y, z);
-      const double ux = x - pcx, uy = y - pcy, uz = z - pcz;
-      const double rp = sqrt(fma(uz, uz, fma(uy, uy, ux * ux)));
-      Loc lo;
-      const int er = locate_fast(L, L.cx[cb], L.cy[cb], L.cz[cb], x, y, z, lo);
-      if (er) {
-        raise_err(err, er);
-        continue;
+      for (uint32_t f = lane; f < nfl; f += 32) {
+        const uint32_t pb = U.cone_box[q];
+        const int m = T.fl_node[(size_t)tl * P + f];
+        const int jp = m % PP, jt = (m / PP) % PT, js = m / (PP * PT);
+        const SegMid sg = segment_mid(U, U.cone_gamma[q]);
+        const double pcx = U.cx[pb], pcy = U.cy[pb], pcz = U.cz[pb];
+        double x, y, z;
+        node_position(sg, U.rad, pcx, pcy, pcz, K.ns[js], K.nt[jt], K.np[jp], x, y, z);
+        const double ux = x - pcx, uy = y - pcy, uz = z - pcz;
+        const double rp = sqrt(fma(uz, uz, fma(uy, uy, ux * ux)));
+        Loc lo;
+        const int er = locate_fast(L, L.cx[cb], L.cy[cb], L.cz[cb], x, y, z, lo);
+        if (er) {
+          raise_err(err, er);
+          continue;
+        }
+        const uint32_t cq = find_cone(L, cb, lo.gamma);
+        if (cq == kNone) {
+          raise_err(err, kErrPropCover);
+          continue;
+        }
+        double vr, vi;
+        eval_block<PS, PT, PP>(child + (size_t)cq * BL::Pst, lo.ts, lo.tt, lo.tp, vr, vi);
+        const double ratio = rp * lo.rinv;
+        double sn = 0.0, cn = 1.0;
+        if (!LAP) sincos_fast(kappa * (lo.r - rp), sn, cn);
+        const double tr = ratio * cn, ti = ratio * sn;
+        double2 v = acc[m];
+        v.x = fma(vr, tr, fma(-vi, ti, v.x));
+        v.y = fma(vr, ti, fma(vi, tr, v.y));
+        acc[m] = v;
       }
-      const uint32_t cq = find_cone(L, cb, lo.gamma);
-      if (cq == kNone) {
-        raise_err(err, kErrPropCover);
-        continue;
-      }
-      double vr, vi;
-      eval_block<PS, PT, PP>(child + (size_t)cq * BL::Pst, lo.ts, lo.tt, lo.tp, vr, vi);
-      const double ratio = rp * lo.rinv;
-      double sn = 0.0, cn = 1.0;
-      if (!LAP) sincos_fast(kappa * (lo.r - rp), sn, cn);
-      const double tr = ratio * cn, ti = ratio * sn;
-      double2* acc = sv + c * P;
-      double2 v = acc[m];
-      v.x = fma(vr, tr, fma(-vi, ti, v.x));
-      v.y = fma(vr, ti, fma(vi, tr, v.y));
-      acc[m] = v;
     }
-    const bool last = H.last;
-    pp_consumer_sync();  // every row of stage i is in sv; the stage is free
-    if (ct == 0) pp_arrive(&empty[st]);
+    __syncwarp();
+    if (last && c < ncon) {
+      // scratch: this cone's (consumed) row chunk of the stage; the generic
+      // writes are fenced against the producer's next bulk copies into it
+      double2* sf = reinterpret_cast<double2*>(const_cast<unsigned char*>(sb) + SH::off_row +
+                                               c * SH::RowBytes);
+      fit_cones_warp<PS, PT, PP>(sM, acc, sf, 1, parent + (size_t)(q0 + c) * BL::Pst, err);
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      __syncwarp();
+    }
+    if (lane == 0) pp_arrive(&empty[st]);
+    if (last)
+      for (int k = lane; k < P; k += 32) acc[k] = make_double2(0.0, 0.0);
+    __syncwarp();
     return last;
   };
-  // number of stages of this CTA (units x children), for the lookahead
   uint32_t nstage = 0;
   for (uint32_t u = blockIdx.x; u < nu; u += gridDim.x) nstage += urec[(size_t)u * kPpRec + 3];
-  for (uint32_t i = ct; i < kPpCh * P; i += NCT) sv[i] = make_double2(0.0, 0.0);
+  for (int k = lane; k < P; k += 32) acc[k] = make_double2(0.0, 0.0);
+  __syncwarp();
   if (nstage) phaseA(0);
-  uint32_t u = blockIdx.x;
   for (uint32_t i = 0; i < nstage; ++i) {
     if (i + 1 < nstage) phaseA(i + 1);
-    const uint32_t q0 = hdr[i % kPpStages].q0, ncon = hdr[i % kPpStages].ncon;
-    if (phaseB(i)) {
-      // fit the unit's cones: consumer warp w takes cones w, w + kPpConsumers, ...
-      double2* sf = stf + (size_t)w * P;
-      for (uint32_t c = w; c < ncon; c += kPpConsumers)
-        fit_cones_warp<PS, PT, PP>(sM, sv + c * P, sf, 1, parent + (size_t)(q0 + c) * BL::Pst, err);
-      pp_consumer_sync();
-      for (uint32_t k = ct; k < kPpCh * P; k += NCT) sv[k] = make_double2(0.0, 0.0);
-      pp_consumer_sync();
-      u += gridDim.x;
-    }
+    phaseB(i);
   }
 }
+
 
 // K3 streaming (default where the orders allow it): the child block stays in
 // registers while the nodes that fall into it stream past.  A child cone of
@@ -2114,7 +2103,8 @@ bool launch_propagation_mma(ifgf_plan* P, int d, uint32_t qb, uint32_t qe, const
         // orders whose stages do not fit in shared memory run the rows kernel
         constexpr size_t kMaxSmem = 220 * 1024;
         if constexpr (PipeShape<PS, PT, PP, 2>::smem > kMaxSmem ||
-                      PipeShape<PS, PT, PP, 3>::smem > kMaxSmem) {
+                      PipeShape<PS, PT, PP, 3>::smem > kMaxSmem ||
+                      !PipeShape<PS, PT, PP, 2>::fits || !PipeShape<PS, PT, PP, 3>::fits) {
           return;
         } else {
         const Level& U = P->lv[d - 1];
