@@ -304,19 +304,22 @@ def run_ours(args):
     dom = max(per_kernel, key=lambda k: per_kernel[k]["ms"])
     traffic = None
     summ = os.path.join(ROOT, "profiles", "ncu_summary.json")
-    kernel_prefix = {"near": "k_singular", "level_d": "k_level_d",
-                     "interpolation": "k_interp", "propagation": "k_propagate_rows"}[dom]
+    kernel_prefix = {"near": "k_near", "level_d": "k_level_d",
+                     "interpolation": "k_interp", "propagation": "k_propagate"}[dom]
     if os.path.exists(summ):
         try:
-            tb = json.load(open(summ)).get("traffic_bytes_per_launch", {})
-            hits = [v for k, v in tb.items() if k.startswith(kernel_prefix + "<")]
+            # mean DRAM bytes over every launch of the stage's kernels in one
+            # captured C2 apply (K3: the four tiled levels and the fly level)
+            ls = json.load(open(summ)).get("launches", [])
+            hits = [l["dram_read_bytes"] + l["dram_write_bytes"] for l in ls
+                    if l["kernel"].startswith(kernel_prefix)]
             traffic = statistics.mean(hits) if hits else None
         except Exception:
             traffic = None
     dk = per_kernel[dom]
     roofline = {"bound": "fp64", "kernel": dom, "achieved": dk["tflops"], "peak": fp64_peak,
-                "traffic_note": "DRAM bytes per launch of the dominant kernel from the committed "
-                                "ncu --set full capture (profiles/ncu_summary.json, C2)",
+                "traffic_note": "mean DRAM bytes per launch of the dominant stage's kernels over "
+                                "one C2 apply (ncu dram__bytes_read/write; profiles/ncu_summary.json)",
                 "unit": "TFLOP/s", "frac": dk["frac_fp64"], "traffic": traffic,
                 "peak_source": "measured in this run: best of DFMA chains and mma.sync m8n8k4 f64 "
                                "over all SMs (ifgf_measure_fp64_peak); MEASURED_PEAKS.json has no FP64 figure",
