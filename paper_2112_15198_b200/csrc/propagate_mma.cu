@@ -1431,7 +1431,7 @@ __global__ void __launch_bounds__(kPpThreads, 1)
 }
 
 
-// K3 streaming (default where the orders allow it): the child block stays in
+// K3 streaming (IFGF_PROP_STREAM, an option; measured slower than rows): the child block stays in
 // registers while the nodes that fall into it stream past.  A child cone of
 // a parent box collects ~25 nodes of each parent cone (the child's cone
 // grid is 2x coarser per axis), so a block loaded once serves a whole run
