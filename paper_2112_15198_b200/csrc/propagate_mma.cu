@@ -11,14 +11,11 @@
 //     exact-fallback margin; entries within the margin are flagged and
 //     recomputed per box with the reference's exact formulas),
 //   * the nodes grouped by gamma_c into row tiles of 8.
-// At apply time a CTA takes up to kChunk parent cones that share one gamma
-// (cones sorted by gamma) and, octant by octant in Morton order, computes
-//   V[node][cone] = sum_k B_k(t_node) * C_{child cone}[k]
-// with mma.sync.m8n8k4.f64: A = Chebyshev basis products of 8 nodes (built in
-// shared memory), B = gathered child coefficients of 4 cones (re/im columns),
-// so a coefficient is loaded once per warp instead of once per node.  The
-// accumulated node values are fitted exactly as before.  Same result as the
-// per-node evaluation up to rounding (the basis is evaluated at identical t).
+// With IFGF_PROP_DMMA a warp takes up to kChunk = 8 parent cones that share
+// one gamma (cones sorted by gamma) and, octant by octant in Morton order,
+// computes V[node][cone] = sum_k B_k(t_node) * C_{child cone}[k] with
+// mma.sync.m8n8k4.f64 (k_propagate_gemm).  Same result as the per-node
+// evaluation up to rounding (the basis is evaluated at identical t).
 #include <cub/cub.cuh>
 
 #include <algorithm>
@@ -30,14 +27,7 @@
 namespace ifgf_b200 {
 namespace {
 
-#ifndef IFGF_MMA_CHUNK
-#define IFGF_MMA_CHUNK 16
-#endif
-#ifndef IFGF_MMA_WARPS
-#define IFGF_MMA_WARPS 4
-#endif
-constexpr int kChunk = IFGF_MMA_CHUNK;    // parent cones per CTA (column tiles of 4)
-constexpr int kMmaWarps = IFGF_MMA_WARPS;  // warps per CTA
+constexpr int kChunk = 8;  // IFGF_PROP_DMMA: parent cones per warp (the B / D columns)
 constexpr uint32_t kNone = 0xffffffffu;
 constexpr uint32_t kFlag = 0x80000000u;
 constexpr uint32_t kFlagTask = 0xfffffffeu;  // task meta: flagged node (exact path)
@@ -341,7 +331,20 @@ __global__ void __launch_bounds__(256)
   }
 }
 
-__global__ void k_chunk_flags(const uint32_t* gsorted, uint32_t n, uint32_t* flag) {
+#ifndef IFGF_GEMM_BOXGROUP
+#define IFGF_GEMM_BOXGROUP 32
+#endif
+constexpr uint32_t kGemmBoxGroup = IFGF_GEMM_BOXGROUP;
+
+__global__ void k_gemm_keys(const __grid_constant__ LevelDev U, const uint32_t* __restrict__ gidx,
+                            uint32_t ngamma, uint64_t* key, uint32_t* qidx) {
+  const uint32_t q = blockIdx.x * blockDim.x + threadIdx.x;
+  if (q >= U.nc) return;
+  key[q] = (uint64_t)(U.cone_box[q] / kGemmBoxGroup) * ngamma + gidx[q];
+  qidx[q] = q;
+}
+
+__global__ void k_chunk_flags(const uint64_t* gsorted, uint32_t n, uint32_t* flag) {
   const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i > n) return;
   if (i == n) {
@@ -350,7 +353,7 @@ __global__ void k_chunk_flags(const uint32_t* gsorted, uint32_t n, uint32_t* fla
   }
   // chunk starts: every kChunk-th element of each run of equal gamma index
   uint32_t lo = 0, hi = i;
-  const uint32_t g = gsorted[i];
+  const uint64_t g = gsorted[i];
   while (lo < hi) {  // run start = lower_bound(g)
     const uint32_t mid = (lo + hi) >> 1;
     if (gsorted[mid] < g) lo = mid + 1;
@@ -414,193 +417,278 @@ __device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b)
                : "d"(a), "d"(b));
 }
 
-// GEMM K index = device block layout index (planes padded to PL, total
-// KD = PS*PL rounded up to 4); A is zero on the pad columns, B on pad rows.
+// K3 as FP64 tensor-core GEMMs (IFGF_PROP_DMMA).  For one tile (gamma,
+// octant) and one of its child-gamma groups, the evaluation of the child
+// interpolants at the group's nodes for 8 parent cones that share gamma is
+//   V[node][cone] = sum_k A[node][k] C_cone[k],
+//   A[node][k]   = T_ks(ts) T_kt(tt) T_kp(tp)   (box-independent),
+// C the child cone's complex coefficients, re and im as two
+// mma.sync.m8n8k4.f64 that share A and one 16-byte load of B.  A warp owns
+// 8 cones (the B / D columns); A fragments are formed in registers from each
+// lane's node basis, B fragments come straight from the child blocks, so
+// there is no shared-memory staging and no CTA barrier.  K order (GemmK):
+// part 1 steps (ks, kt, c), lane k of the quad -> kp = 4c + k; part 2 packs
+// the remaining kp >= 4 floor(PP/4) over (kp, ks, kt), four per step.  The
+// dense contraction does 2 (PS PT PP + pad) FMA per node and cone (160 at
+// (3,5,5), against 186 for the separable scalar evaluation).
 template <int PS, int PT, int PP>
-struct MmaShape {
-  static constexpr int P = PS * PT * PP, NR = PT * PP;
-  static constexpr int PL = BlockLayout<PS, PT, PP>::PL, Pst = BlockLayout<PS, PT, PP>::Pst;
-  static constexpr int KD = (Pst + 3) & ~3, NS = KD / 4, NB = PS + PT + PP;
-  static constexpr int AST = KD + 1;   // A row stride in doubles (odd: spreads banks)
-  static constexpr int BST = KD + 1;   // B column stride in double2
-  static constexpr int RTB = 4;        // row tiles staged per batch
-  static constexpr size_t acc_bytes = (size_t)kChunk * P * sizeof(double2);
-  static constexpr size_t b_bytes = (size_t)kChunk * BST * sizeof(double2);
-  static constexpr size_t a_bytes = (size_t)RTB * 8 * (AST + NB) * sizeof(double);
-  static constexpr size_t work = b_bytes + a_bytes;
-  static constexpr size_t smem = acc_bytes + (work > acc_bytes ? work : acc_bytes);
+struct GemmK {
+  static constexpr int NC = PP / 4;           // full kp chunks of 4
+  static constexpr int PPF = 4 * NC;
+  static constexpr int N1 = PS * PT * NC;      // part-1 steps
+  static constexpr int N2R = (PP - PPF) * PS * PT;
+  static constexpr int N2 = (N2R + 3) / 4;     // part-2 steps
+  static constexpr int NS = N1 + N2;           // K steps of 4
+  static constexpr int P = PS * PT * PP;
+  // warps per CTA: node values of 8 cones + one cone of fit scratch per warp
+  static constexpr int NW = (200 * 1024) / (9 * P * 16) >= 4 ? 4
+                          : ((200 * 1024) / (9 * P * 16) < 1 ? 1 : (200 * 1024) / (9 * P * 16));
+  static constexpr size_t smem = (size_t)NW * 9 * P * sizeof(double2);
 };
 
-__device__ __forceinline__ void cp_async16(void* smem_dst, const void* gmem_src) {
-  const unsigned dst = (unsigned)__cvta_generic_to_shared(smem_dst);
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(gmem_src));
-}
-__device__ __forceinline__ void cp_async_wait_all() {
-  asm volatile("cp.async.wait_all;" ::: "memory");
+// Coefficient (device block offset, or -1 for a pad entry) of K step st,
+// quad lane k (GemmK order).
+template <int PS, int PT, int PP>
+__host__ __device__ __forceinline__ int gemm_koff(int st, int k, int& ks, int& kt, int& kp) {
+  using G = GemmK<PS, PT, PP>;
+  constexpr int PL = BlockLayout<PS, PT, PP>::PL;
+  if (st < G::N1) {
+    const int c = st % G::NC, pair = st / G::NC;
+    ks = pair / PT;
+    kt = pair % PT;
+    kp = 4 * c + k;
+  } else {
+    const int p = 4 * (st - G::N1) + k;
+    if (p >= G::N2R) return -1;
+    const int e = p / (PS * PT), pr = p % (PS * PT);
+    ks = pr / PT;
+    kt = pr % PT;
+    kp = G::PPF + e;
+  }
+  return ks * PL + kt * PP + kp;
 }
 
+#ifndef IFGF_GEMM_RB
+#define IFGF_GEMM_RB 2
+#endif
+constexpr int kGemmRB = IFGF_GEMM_RB;  // row tiles per batch (one B load feeds 2 RB MMAs)
+constexpr int kGemmMaxRt = 16;      // row tiles per tile resolved ahead (more: resolved in the loop)
+constexpr int kGemmMaxGroups = 16;  // child-gamma groups per tile resolved ahead
+
 template <int PS, int PT, int PP, bool LAP>
-__global__ void __launch_bounds__(kMmaWarps * 32)
-    k_propagate_mma(const __grid_constant__ LevelDev U, const __grid_constant__ LevelDev L,
-                    const __grid_constant__ InterpConsts K, const TilesDev T, double kappa,
-                    const double2* __restrict__ child, double2* parent, int* err) {
-  using S = MmaShape<PS, PT, PP>;
-  constexpr int P = S::P, NR = S::NR, PL = S::PL, NS = S::NS, NB = S::NB, AST = S::AST;
-  constexpr int BST = S::BST, RTB = S::RTB;
+__global__ void __launch_bounds__(GemmK<PS, PT, PP>::NW * 32)
+    k_propagate_gemm(const __grid_constant__ LevelDev U, const __grid_constant__ LevelDev L,
+                     const __grid_constant__ InterpConsts K, const TilesDev T, double kappa,
+                     uint32_t nchunks, const double2* __restrict__ child, double2* parent,
+                     int* err) {
+  using BL = BlockLayout<PS, PT, PP>;
+  using G = GemmK<PS, PT, PP>;
+  constexpr int P = G::P, PL = BL::PL, NW = G::NW;
   extern __shared__ double2 smem[];
-  double2* acc = smem;                                        // kChunk x P node values
-  double2* Bs = acc + kChunk * P;                             // kChunk x BST child blocks
-  double* Ash = reinterpret_cast<double*>(Bs + kChunk * BST); // RTB*8 x AST
-  double* bas = Ash + RTB * 8 * AST;                          // RTB*8 x NB
-  double2* scr = acc + kChunk * P;                            // fit scratch (aliases Bs..)
-  __shared__ uint32_t qs[kChunk];
-  __shared__ uint32_t cbox[kChunk][8];
-  __shared__ int vl[kChunk];  // packed cones having a child in this octant
-  __shared__ int nv_s;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const uint32_t c0 = T.chunk_start[blockIdx.x], c1 = T.chunk_start[blockIdx.x + 1];
+  __shared__ double sM[PP * PP + PT * PT + PS * PS];
+  __shared__ uint32_t s_q[NW][8];
+  __shared__ uint32_t s_cb[NW][8][8];
+  __shared__ uint4 s_rt[NW][8][kGemmMaxRt];             // row tiles of each octant's tile
+  __shared__ uint32_t s_cq[NW][8][kGemmMaxGroups][8];   // child cone per (octant, group, cone)
+  __shared__ uint32_t s_off[NW][9];
+  stage_fit_matrices<PS, PT, PP>(K, sM);
+  __syncthreads();
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const uint32_t ch = blockIdx.x * NW + w;
+  if (ch >= nchunks) return;
+  const uint32_t c0 = T.chunk_start[ch], c1 = T.chunk_start[ch + 1];
   const int nq = (int)(c1 - c0);
-  for (int c = threadIdx.x; c < kChunk; c += blockDim.x) {
-    const uint32_t q = c < nq ? T.qsorted[c0 + c] : kNone;
-    qs[c] = q;
-    for (int o = 0; o < 8; ++o) cbox[c][o] = kNone;
+  double2* acc = smem + (size_t)w * 9 * P;
+  double2* scr = acc + 8 * P;
+  for (int i = lane; i < 8 * P; i += 32) acc[i] = make_double2(0.0, 0.0);
+  const uint32_t q0 = T.qsorted[c0];
+  const uint32_t gi = T.cone_gidx[q0];
+  if (lane < 8) {
+    const uint32_t q = lane < nq ? T.qsorted[c0 + lane] : kNone;
+    s_q[w][lane] = q;
+    uint32_t cbo[8];
+#pragma unroll
+    for (int o = 0; o < 8; ++o) cbo[o] = kNone;
     if (q != kNone) {
       const uint32_t pb = U.cone_box[q];
-      for (uint32_t cb = U.child_begin[pb]; cb < U.child_begin[pb + 1]; ++cb)
-        cbox[c][L.code[cb] & 7] = cb;
+      for (uint32_t cb = U.child_begin[pb]; cb < U.child_begin[pb + 1]; ++cb) {
+        const int o = (int)(L.code[cb] & 7);
+#pragma unroll
+        for (int oo = 0; oo < 8; ++oo)
+          if (oo == o) cbo[oo] = cb;
+      }
     }
+#pragma unroll
+    for (int o = 0; o < 8; ++o) s_cb[w][lane][o] = cbo[o];
   }
-  for (int i = threadIdx.x; i < kChunk * P; i += blockDim.x) acc[i] = make_double2(0.0, 0.0);
-  __syncthreads();
-  const uint32_t gi = T.cone_gidx[qs[0]];
-  const int arow = lane >> 2, acol = lane & 3;
-  for (int o = 0; o < 8; ++o) {
-    if (threadIdx.x == 0) {
-      int n = 0;
-      for (int c = 0; c < nq; ++c)
-        if (cbox[c][o] != kNone) vl[n++] = c;
-      nv_s = n;
-    }
-    __syncthreads();
-    const int nv = nv_s;
-    if (nv == 0) continue;
-    const int nct = (nv + 3) / 4;
-    const uint32_t tile = gi * 8 + o;
-    const uint32_t r0 = T.rt_off[tile], r1 = T.rt_off[tile + 1];
-    for (uint32_t ga = r0; ga < r1;) {
-      // group [ga, gb): row tiles sharing one child gamma
-      const uint4 RG = T.rt[ga];
-      const uint32_t gb = ga + max(RG.w, 1u);
-      const uint32_t gc = RG.x;
-      // stage B: the group's child block of every packed cone (zero for pads)
-      for (int i = threadIdx.x; i < nct * 4 * (S::KD / 2); i += blockDim.x) {
-        const int j = i / (S::KD / 2), h = i % (S::KD / 2);  // 2 complex (32 B) per step
-        double2* dst = Bs + j * BST + 2 * h;
-        const double2* src = nullptr;
-        if (j < nv && 2 * h < S::Pst) {
-          const uint32_t cq = find_cone(L, cbox[vl[j]][o], gc);
-          if (cq == kNone) raise_err(err, kErrPropCover);
-          else src = child + (size_t)cq * S::Pst + 2 * h;
-        }
-        if (src) {
-          cp_async16(dst, src);
-          cp_async16(dst + 1, src + 1);
+  if (lane < 9) s_off[w][lane] = T.rt_off[gi * 8 + lane];
+  __syncwarp();
+  // phase A1: the row tiles of all eight tiles (independent loads)
+#pragma unroll
+  for (int i = 0; i < 8 * kGemmMaxRt / 32; ++i) {
+    const int t = lane + 32 * i, o = t / kGemmMaxRt, rel = t % kGemmMaxRt;
+    if (s_off[w][o] + rel < s_off[w][o + 1]) s_rt[w][o][rel] = T.rt[s_off[w][o] + rel];
+  }
+  __syncwarp();
+  // phase A2: every (octant, cone) walks its tile's groups: child cone
+  // ordinals into s_cq, the blocks prefetched into L2
+#pragma unroll
+  for (int i = 0; i < 2; ++i) {
+    const int t = lane + 32 * i, o = t >> 3, c = t & 7;
+    const uint32_t cb = s_cb[w][c][o];
+    const int n = (int)min(s_off[w][o + 1] - s_off[w][o], (uint32_t)kGemmMaxRt);
+    int gidx = 0;
+    for (int rel = 0; rel < n && gidx < kGemmMaxGroups; ++gidx) {
+      const uint4 R = s_rt[w][o][rel];
+      uint32_t cq = kNone;
+      if (cb != kNone) {
+        cq = find_cone(L, cb, R.x);
+        if (cq != kNone) {
+          const char* pf = (const char*)(child + (size_t)cq * BL::Pst);
+#pragma unroll
+          for (int l = 0; l < (BL::Pst * 16 + 127) / 128; ++l)
+            asm volatile("prefetch.global.L2 [%0];" ::"l"(pf + 128 * l));
         } else {
-          dst[0] = make_double2(0.0, 0.0);
-          dst[1] = make_double2(0.0, 0.0);
+          raise_err(err, kErrPropCover);
         }
       }
-      for (uint32_t rb = ga; rb < gb; rb += RTB) {
-        const uint32_t re = min(gb, rb + RTB);
-        const int nrow = (int)(re - rb) * 8;
-        // bases of the staged rows
-        for (int i = threadIdx.x; i < nrow; i += blockDim.x) {
-          const int m = rt_node(T.rt[rb + i / 8], i % 8);
-          double* b = bas + i * NB;
-          if (m != 0xff) {
-            const double* tv = T.e_t + ((size_t)tile * P + m) * 3;
-            cheb_basis<PS>(tv[0], b);
-            cheb_basis<PT>(tv[1], b + PS);
-            cheb_basis<PP>(tv[2], b + PS + PT);
-          } else {
-            for (int j = 0; j < NB; ++j) b[j] = 0.0;
-          }
+      s_cq[w][o][gidx][c] = cq;
+      rel += (int)max(R.w, 1u);
+    }
+  }
+  __syncwarp();
+  const int kq = lane & 3, nn = lane >> 2;  // A/D row (node slot) = nn; B row k = kq, column = nn
+  for (int o = 0; o < 8; ++o) {
+    const uint32_t cbn = s_cb[w][nn][o];  // child box of this lane's B column cone
+    if (!__any_sync(0xffffffffu, cbn != kNone)) continue;
+    const uint32_t tile = gi * 8 + (uint32_t)o;
+    const uint32_t r0 = s_off[w][o], r1 = s_off[w][o + 1];
+    int gidx = 0;
+    for (uint32_t ga = r0; ga < r1; ++gidx) {
+      // group [ga, gb): row tiles sharing one child gamma
+      const uint32_t rel = ga - r0;
+      const uint4 RG = rel < kGemmMaxRt ? s_rt[w][o][rel] : T.rt[ga];
+      const uint32_t gb = ga + max(RG.w, 1u);
+      const double2* bb = child;  // unresolved column: any finite block (ignored)
+      if (cbn != kNone) {
+        uint32_t cq;
+        if (rel < kGemmMaxRt && gidx < kGemmMaxGroups) {
+          cq = s_cq[w][o][gidx][nn];
+        } else {
+          cq = find_cone(L, cbn, RG.x);
+          if (cq == kNone) raise_err(err, kErrPropCover);
         }
-        __syncthreads();
-        // A rows: thread per (row, ks plane), compile-time (kt, kp) offsets
-        for (int i = threadIdx.x; i < nrow * PS; i += blockDim.x) {
-          const int row = i / PS, ks = i % PS;
-          const double* b = bas + row * NB;
-          double* Ar = Ash + row * AST + ks * PL;
-          const double ts = b[ks];
+        if (cq != kNone) bb = child + (size_t)cq * BL::Pst;
+      }
+      for (uint32_t rb = ga; rb < gb; rb += kGemmRB) {
+        const int nrb = (int)min(gb - rb, (uint32_t)kGemmRB);
+        double Ts[kGemmRB][PS], Tt[kGemmRB][PT], Tp[kGemmRB][PP], TpL[kGemmRB][G::NC + 1];
+        int m[kGemmRB];
+        double dr[kGemmRB][2], di[kGemmRB][2];
 #pragma unroll
-          for (int kt = 0; kt < PT; ++kt) {
-            const double w = ts * b[PS + kt];
-#pragma unroll
-            for (int kp = 0; kp < PP; ++kp) Ar[kt * PP + kp] = w * b[PS + PT + kp];
+        for (int j = 0; j < kGemmRB; ++j) {
+          const uint32_t rj = rb + j - r0;
+          m[j] = j < nrb ? rt_node(rj < kGemmMaxRt ? s_rt[w][o][rj] : T.rt[rb + j], nn) : 0xff;
+          double ts = 0.0, tt = 0.0, tp = 0.0;
+          if (m[j] != 0xff) {
+            const double* tv = T.e_t + ((size_t)tile * P + m[j]) * 3;
+            ts = tv[0];
+            tt = tv[1];
+            tp = tv[2];
           }
+          cheb_basis<PS>(ts, Ts[j]);
+          cheb_basis<PT>(tt, Tt[j]);
+          cheb_basis<PP>(tp, Tp[j]);
 #pragma unroll
-          for (int k = NR; k < PL; ++k) Ar[k] = 0.0;
-          if (ks == PS - 1)
-            for (int k = PS * PL; k < S::KD; ++k) Ash[row * AST + k] = 0.0;
+          for (int k2 = 0; k2 < PS; ++k2)
+            if (m[j] == 0xff) Ts[j][k2] = 0.0;  // empty node slot: zero row of A
+#pragma unroll
+          for (int c = 0; c < G::NC; ++c) {
+            double v = Tp[j][4 * c];
+#pragma unroll
+            for (int kk = 1; kk < 4; ++kk)
+              if (kq == kk) v = Tp[j][4 * c + kk];
+            TpL[j][c] = v;
+          }
+          dr[j][0] = dr[j][1] = di[j][0] = di[j][1] = 0.0;
         }
-        cp_async_wait_all();
-        __syncthreads();
-        // MMA: warp per row tile; A fragments in registers, 4 column tiles at a time
-        for (int rt = warp; rt < (int)(re - rb); rt += kMmaWarps) {
-          double af[NS];
-          const double* ar = Ash + (rt * 8 + arow) * AST + acol;
+        // part 1: (ks, kt, c), lane kp = 4c + kq; A formed in registers
 #pragma unroll
-          for (int st = 0; st < NS; ++st) af[st] = ar[4 * st];
-          const int m = rt_node(T.rt[rb + rt], arow);
-          for (int cg = 0; cg < nct; cg += 4) {
-            double d[4][2];
+        for (int ks = 0; ks < PS; ++ks)
 #pragma unroll
-            for (int u = 0; u < 4; ++u) d[u][0] = d[u][1] = 0.0;
-            // B fragment: column lane>>2 -> cone (ct*4 + col/2), part col&1; row k = 4st+acol
-            const int col = lane >> 2;
-            const double* bcol = reinterpret_cast<const double*>(Bs) + (col & 1) + 2 * acol;
+          for (int kt = 0; kt < PT; ++kt)
 #pragma unroll
-            for (int st = 0; st < NS; ++st) {
+            for (int c = 0; c < G::NC; ++c) {
+              const double2 b = __ldg(bb + ks * PL + kt * PP + 4 * c + kq);
 #pragma unroll
-              for (int u = 0; u < 4; ++u) {
-                const int j = (cg + u) * 4 + (col >> 1);
-                const double bv = (cg + u < nct) ? bcol[2 * (j * BST + 4 * st)] : 0.0;
-                dmma(d[u][0], d[u][1], af[st], bv);
-              }
-            }
-#pragma unroll
-            for (int u = 0; u < 4; ++u) {
-              const int j = (cg + u) * 4 + acol;  // packed cone of this lane's D column pair
-              if (cg + u < nct && j < nv && m != 0xff) {
-                const int c = vl[j];
-                const double2 Tf = T.e_T[(size_t)tile * P + m];
-                double2 v = acc[c * P + m];
-                if (LAP) {
-                  v.x = fma(d[u][0], Tf.x, v.x);
-                  v.y = fma(d[u][1], Tf.x, v.y);
-                } else {
-                  v.x = fma(d[u][0], Tf.x, fma(-d[u][1], Tf.y, v.x));
-                  v.y = fma(d[u][0], Tf.y, fma(d[u][1], Tf.x, v.y));
+              for (int j = 0; j < kGemmRB; ++j)
+                if (j < nrb) {
+                  const double a = Ts[j][ks] * Tt[j][kt] * TpL[j][c];
+                  dmma(dr[j][0], dr[j][1], a, b.x);
+                  dmma(di[j][0], di[j][1], a, b.y);
                 }
-                acc[c * P + m] = v;
+            }
+        // part 2: entries p = 4g + kq over (kp >= PPF, ks, kt); pad entries
+        // (A = 0) read coefficient 0 (finite, contributes exactly 0)
+#pragma unroll
+        for (int st = G::N1; st < G::NS; ++st) {
+          int ks, kt, kp, off = 0;
+#pragma unroll
+          for (int kk = 0; kk < 4; ++kk) {
+            const int o2 = gemm_koff<PS, PT, PP>(st, kk, ks, kt, kp);
+            if (kq == kk && o2 >= 0) off = o2;
+          }
+          const double2 b = __ldg(bb + off);
+#pragma unroll
+          for (int j = 0; j < kGemmRB; ++j)
+            if (j < nrb) {
+              double a = 0.0;
+#pragma unroll
+              for (int kk = 0; kk < 4; ++kk) {
+                if (gemm_koff<PS, PT, PP>(st, kk, ks, kt, kp) >= 0) {
+                  const double v = Ts[j][ks] * Tt[j][kt] * Tp[j][kp];
+                  if (kq == kk) a = v;
+                }
+              }
+              dmma(dr[j][0], dr[j][1], a, b.x);
+              dmma(di[j][0], di[j][1], a, b.y);
+            }
+        }
+        // epilogue: D row nn = node m[j], columns 2 kq + h = cones
+#pragma unroll
+        for (int j = 0; j < kGemmRB; ++j) {
+          if (j < nrb && m[j] != 0xff) {
+            const double2 Tf = __ldg(&T.e_T[(size_t)tile * P + m[j]]);
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+              const int cn = 2 * kq + h;
+              if (s_cb[w][cn][o] != kNone) {
+                double2 v = acc[cn * P + m[j]];
+                if (LAP) {
+                  v.x = fma(dr[j][h], Tf.x, v.x);
+                  v.y = fma(di[j][h], Tf.x, v.y);
+                } else {
+                  v.x = fma(dr[j][h], Tf.x, fma(-di[j][h], Tf.y, v.x));
+                  v.y = fma(dr[j][h], Tf.y, fma(di[j][h], Tf.x, v.y));
+                }
+                acc[cn * P + m[j]] = v;
               }
             }
           }
         }
-        __syncthreads();
       }
       ga = gb;
     }
-    // flagged nodes: per-box exact locate + evaluation (rare)
+    // flagged nodes: per-box exact locate + evaluation (rare); lanes over
+    // (flagged node, cone)
     const size_t f0 = (size_t)tile * P;
     const uint32_t nfl = T.fl_cnt[tile];
-    for (uint32_t i = threadIdx.x; i < nfl * (uint32_t)nq; i += blockDim.x) {
-      const int c = (int)(i % nq);
-      const int m = T.fl_node[f0 + i / nq];
-      const uint32_t cb = cbox[c][o];
+    for (uint32_t i = lane; i < nfl * 8u; i += 32) {
+      const int c = (int)(i & 7u);
+      const uint32_t cb = s_cb[w][c][o];
       if (cb == kNone) continue;
-      const uint32_t q = qs[c], pb = U.cone_box[q];
+      const int m = T.fl_node[f0 + (i >> 3)];
+      const uint32_t q = s_q[w][c], pb = U.cone_box[q];
       const int jp = m % PP, jt = (m / PP) % PT, js = m / (PP * PT);
       const SegMid sg = segment_mid(U, U.cone_gamma[q]);
       const double pcx = U.cx[pb], pcy = U.cy[pb], pcz = U.cz[pb];
@@ -620,7 +708,7 @@ __global__ void __launch_bounds__(kMmaWarps * 32)
         continue;
       }
       double vr, vi;
-      eval_block<PS, PT, PP>(child + (size_t)cq * S::Pst, lo.ts, lo.tt, lo.tp, vr, vi);
+      eval_block<PS, PT, PP>(child + (size_t)cq * BL::Pst, lo.ts, lo.tt, lo.tp, vr, vi);
       const double ratio = rp * lo.rinv;
       double sn = 0.0, cn = 1.0;
       if (!LAP) sincos_fast(kappa * (lo.r - rp), sn, cn);
@@ -630,9 +718,12 @@ __global__ void __launch_bounds__(kMmaWarps * 32)
       v.y = fma(vr, ti, fma(vi, tr, v.y));
       acc[c * P + m] = v;
     }
-    __syncthreads();
+    __syncwarp();
   }
-  fit_cones_scatter<PS, PT, PP>(K, acc, scr, nq, parent, qs, err);
+  for (int c = 0; c < nq; ++c) {  // one cone at a time: one cone of scratch per warp
+    fit_cones_warp<PS, PT, PP>(sM, acc + c * P, scr, 1, parent, err, &s_q[w][c]);
+    __syncwarp();
+  }
 }
 
 // K3 per node with the tile geometry: thread = (parent cone, lane j); for
@@ -2063,21 +2154,24 @@ void build_dmma_extras(ifgf_plan* P, int d, cudaStream_t s) {
   T.rt = P->alloc<uint4>(nrt + 1);
   k_tile_rows<<<nblk(ntiles, 64), 64, 0, s>>>(ntiles, K.P, T.e_gc, nullptr, nullptr, T.rt_off,
                                               T.rt, nullptr, nullptr, nullptr);
-  // parent cones sorted by gamma index (stable) -> chunks of <= kChunk
+  // parent cones sorted (stably) by (group of kGemmBoxGroup consecutive parent
+  // boxes, gamma index) -> chunks of <= kChunk cones sharing gamma.  Box
+  // groups keep the child blocks that neighbouring gammas share in L2 (gamma
+  // order alone re-reads them from DRAM: 10 GB per C2 launch).
   uint32_t* qidx = P->alloc<uint32_t>(U.nc);
-  uint32_t* gsorted = P->alloc<uint32_t>(U.nc);
+  uint64_t* key = P->alloc<uint64_t>(U.nc);
+  uint64_t* gsorted = P->alloc<uint64_t>(U.nc);
   T.qsorted = P->alloc<uint32_t>(U.nc);
   {
-    std::vector<uint32_t> iota(U.nc);
-    for (uint32_t i = 0; i < U.nc; ++i) iota[i] = i;
-    IFGF_CUDA(cudaMemcpyAsync(qidx, iota.data(), U.nc * 4, cudaMemcpyHostToDevice, s));
+    k_gemm_keys<<<nblk(U.nc), 256, 0, s>>>(U.dev(), T.cone_gidx, T.ngamma, key, qidx);
     size_t tb = 0;
     int bits = 1;
-    while ((1u << bits) < T.ngamma && bits < 32) ++bits;
-    cub::DeviceRadixSort::SortPairs(nullptr, tb, T.cone_gidx, gsorted, qidx, T.qsorted,
-                                    (int)U.nc, 0, bits, s);
-    IFGF_CUDA(cub::DeviceRadixSort::SortPairs(tmp(tb), tb, T.cone_gidx, gsorted, qidx,
-                                              T.qsorted, (int)U.nc, 0, bits, s));
+    const uint64_t kmax = ((uint64_t)U.nb / kGemmBoxGroup + 1) * T.ngamma;
+    while ((1ull << bits) < kmax && bits < 64) ++bits;
+    cub::DeviceRadixSort::SortPairs(nullptr, tb, key, gsorted, qidx, T.qsorted, (int)U.nc, 0,
+                                    bits, s);
+    IFGF_CUDA(cub::DeviceRadixSort::SortPairs(tmp(tb), tb, key, gsorted, qidx, T.qsorted,
+                                              (int)U.nc, 0, bits, s));
     IFGF_CUDA(cudaStreamSynchronize(s));
   }
   uint32_t* flag = P->alloc<uint32_t>(U.nc + 1);
@@ -2267,21 +2361,16 @@ bool launch_propagation_mma(ifgf_plan* P, int d, uint32_t qb, uint32_t qe, const
   const InterpConsts& K = P->K;
   return dispatch_mma_orders(K.ps, K.pt, K.pp, [&](auto A, auto B, auto C) {
     constexpr int PS = decltype(A)::value, PT = decltype(B)::value, PP = decltype(C)::value;
-    const size_t sm = MmaShape<PS, PT, PP>::smem;
-    static bool attr_set = false;
-    if (!attr_set) {
-      cudaFuncSetAttribute(k_propagate_mma<PS, PT, PP, true>,
-                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-      cudaFuncSetAttribute(k_propagate_mma<PS, PT, PP, false>,
-                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-      attr_set = true;
-    }
-    if (P->kappa == 0.0)
-      k_propagate_mma<PS, PT, PP, true><<<T.nchunks, kMmaWarps * 32, sm, s>>>(
-          U.dev(), L.dev(), K, tiles_dev(T), P->kappa, child, parent, P->err);
-    else
-      k_propagate_mma<PS, PT, PP, false><<<T.nchunks, kMmaWarps * 32, sm, s>>>(
-          U.dev(), L.dev(), K, tiles_dev(T), P->kappa, child, parent, P->err);
+    using G = GemmK<PS, PT, PP>;
+    const size_t sm = G::smem;
+    auto launch = [&](auto kern) {
+      IFGF_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+      kern<<<(T.nchunks + G::NW - 1) / G::NW, G::NW * 32, sm, s>>>(U.dev(), L.dev(), K, tiles_dev(T),
+                                                                  P->kappa, T.nchunks, child, parent, P->err);
+      IFGF_CUDA(cudaGetLastError());
+    };
+    P->kappa == 0.0 ? launch(k_propagate_gemm<PS, PT, PP, true>)
+                    : launch(k_propagate_gemm<PS, PT, PP, false>);
     ++P->launches;
   });
 }
