@@ -472,6 +472,10 @@ __host__ __device__ __forceinline__ int gemm_koff(int st, int k, int& ks, int& k
 #define IFGF_GEMM_RB 2
 #endif
 constexpr int kGemmRB = IFGF_GEMM_RB;  // row tiles per batch (one B load feeds 2 RB MMAs)
+#ifndef IFGF_GEMM_KS
+#define IFGF_GEMM_KS 1
+#endif
+constexpr int kGemmKS = IFGF_GEMM_KS;  // accumulator sets (MMA chains split over K)
 constexpr int kGemmMaxRt = 16;      // row tiles per tile resolved ahead (more: resolved in the loop)
 constexpr int kGemmMaxGroups = 16;  // child-gamma groups per tile resolved ahead
 
@@ -584,7 +588,8 @@ __global__ void __launch_bounds__(GemmK<PS, PT, PP>::NW * 32)
         const int nrb = (int)min(gb - rb, (uint32_t)kGemmRB);
         double Ts[kGemmRB][PS], Tt[kGemmRB][PT], Tp[kGemmRB][PP], TpL[kGemmRB][G::NC + 1];
         int m[kGemmRB];
-        double dr[kGemmRB][2], di[kGemmRB][2];
+        // kGemmKS accumulator sets over alternating K steps: independent MMA chains
+        double dr[kGemmKS][kGemmRB][2], di[kGemmKS][kGemmRB][2];
 #pragma unroll
         for (int j = 0; j < kGemmRB; ++j) {
           const uint32_t rj = rb + j - r0;
@@ -610,7 +615,8 @@ __global__ void __launch_bounds__(GemmK<PS, PT, PP>::NW * 32)
               if (kq == kk) v = Tp[j][4 * c + kk];
             TpL[j][c] = v;
           }
-          dr[j][0] = dr[j][1] = di[j][0] = di[j][1] = 0.0;
+#pragma unroll
+          for (int u = 0; u < kGemmKS; ++u) dr[u][j][0] = dr[u][j][1] = di[u][j][0] = di[u][j][1] = 0.0;
         }
         // part 1: (ks, kt, c), lane kp = 4c + kq; A formed in registers
 #pragma unroll
@@ -624,8 +630,9 @@ __global__ void __launch_bounds__(GemmK<PS, PT, PP>::NW * 32)
               for (int j = 0; j < kGemmRB; ++j)
                 if (j < nrb) {
                   const double a = Ts[j][ks] * Tt[j][kt] * TpL[j][c];
-                  dmma(dr[j][0], dr[j][1], a, b.x);
-                  dmma(di[j][0], di[j][1], a, b.y);
+                  const int u = ((ks * PT + kt) * G::NC + c) % kGemmKS;
+                  dmma(dr[u][j][0], dr[u][j][1], a, b.x);
+                  dmma(di[u][j][0], di[u][j][1], a, b.y);
                 }
             }
         // part 2: entries p = 4g + kq over (kp >= PPF, ks, kt); pad entries
@@ -650,10 +657,20 @@ __global__ void __launch_bounds__(GemmK<PS, PT, PP>::NW * 32)
                   if (kq == kk) a = v;
                 }
               }
-              dmma(dr[j][0], dr[j][1], a, b.x);
-              dmma(di[j][0], di[j][1], a, b.y);
+              const int u = st % kGemmKS;
+              dmma(dr[u][j][0], dr[u][j][1], a, b.x);
+              dmma(di[u][j][0], di[u][j][1], a, b.y);
             }
         }
+#pragma unroll
+        for (int u = 1; u < kGemmKS; ++u)
+#pragma unroll
+          for (int j = 0; j < kGemmRB; ++j)
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+              dr[0][j][h] += dr[u][j][h];
+              di[0][j][h] += di[u][j][h];
+            }
         // epilogue: D row nn = node m[j], columns 2 kq + h = cones
 #pragma unroll
         for (int j = 0; j < kGemmRB; ++j) {
@@ -665,11 +682,11 @@ __global__ void __launch_bounds__(GemmK<PS, PT, PP>::NW * 32)
               if (s_cb[w][cn][o] != kNone) {
                 double2 v = acc[cn * P + m[j]];
                 if (LAP) {
-                  v.x = fma(dr[j][h], Tf.x, v.x);
-                  v.y = fma(di[j][h], Tf.x, v.y);
+                  v.x = fma(dr[0][j][h], Tf.x, v.x);
+                  v.y = fma(di[0][j][h], Tf.x, v.y);
                 } else {
-                  v.x = fma(dr[j][h], Tf.x, fma(-di[j][h], Tf.y, v.x));
-                  v.y = fma(dr[j][h], Tf.y, fma(di[j][h], Tf.x, v.y));
+                  v.x = fma(dr[0][j][h], Tf.x, fma(-di[0][j][h], Tf.y, v.x));
+                  v.y = fma(dr[0][j][h], Tf.y, fma(di[0][j][h], Tf.x, v.y));
                 }
                 acc[cn * P + m[j]] = v;
               }
@@ -2039,7 +2056,11 @@ void build_prop_tiles(ifgf_plan* P, int d, void* (*scratch)(void*, size_t), void
     const double bytes = (double)ng * 8.0 * K.P *
                          (rows_bytes + 3 * sizeof(double) + sizeof(double2) +
                           2 * sizeof(uint32_t) + sizeof(uint2) + sizeof(uint16_t) + 1);
-    if (bytes > std::min(8.0 * (1ull << 30), 0.25 * (double)fr)) return;
+    static const double max_gb = [] {
+      const char* v = std::getenv("IFGF_TILE_MAX_GB");
+      return v ? std::atof(v) : 8.0;
+    }();
+    if (bytes > std::min(max_gb * (1ull << 30), 0.25 * (double)fr)) return;
   }
   T.ngamma = ng;
   T.cone_gidx = P->alloc<uint32_t>(U.nc);
