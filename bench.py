@@ -55,6 +55,10 @@ class ClockSampler:
               "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
               "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
 
+    # seconds between NVML polls; each poll takes the driver's lock, which the
+    # device setup's allocations and syncs then wait on
+    INTERVAL = float(os.environ.get("IFGF_CLOCK_INTERVAL", "0.1"))
+
     def __init__(self, index):
         self.index, self.rows, self._stop = index, [], threading.Event()
         self._t = threading.Thread(target=self._run, daemon=True)
@@ -74,7 +78,7 @@ class ClockSampler:
                 rs = N.nvmlDeviceGetCurrentClocksEventReasons(h)
                 self.rows.append([str(sm), str(mx), f"{pw:.1f}", hex(rs)]
                                  + ["Active" if rs & b else "Not Active" for b in bits])
-                self._stop.wait(0.02)
+                self._stop.wait(self.INTERVAL)
             return
         except Exception:
             self.rows = []
