@@ -15,6 +15,9 @@
  *   ifgf_error_at_indices    ifgf::error_at_indices              engine.hpp:123-124
  *   ifgf_choose_depth        ifgf::choose_depth                  engine.hpp:21
  *   ifgf_plan_partition      ifgf::dist::partition               dist.hpp:23
+ *   ifgf_run_distributed     ifgf::dist::run_distributed         dist.hpp:90
+ *   ifgf_dist_plan_*         the rank loop of run_distributed    dist.cpp:241-361
+ *                            as one process per GPU (MPI ranks, PAPER.md)
  *
  * Conventions: plain pointers and sizes, no CUDA or C++ types.  Functions
  * return 0 on success or an IFGF_E* code mirroring the reference's exception
@@ -36,7 +39,7 @@
 extern "C" {
 #endif
 
-#define IFGF_B200_ABI_VERSION 1
+#define IFGF_B200_ABI_VERSION 2
 
 enum {
   IFGF_OK = 0,
@@ -56,6 +59,8 @@ typedef struct ifgf_params {
   int base_s, base_theta, base_phi; /* 1, 2, 4 */
   int p_s, p_theta, p_phi;          /* 3, 5, 5 */
   int device;                       /* CUDA ordinal (replaces `threads`) */
+  int partition; /* rank layout of multi-GPU plans: IFGF_PARTITION_COUNT (0,
+                    the reference's) or IFGF_PARTITION_WORK (1); see below */
 } ifgf_params;
 
 #define IFGF_MAX_LEVELS 22
@@ -225,6 +230,57 @@ int ifgf_plan_partition(const ifgf_plan* plan, int n_ranks, uint32_t* box_begin,
  * dist.cpp:206-237), sorted.  Call with cones == NULL to get the count. */
 int ifgf_plan_exchange_set(ifgf_plan* plan, int n_ranks, int rank, int d, int kind,
                            uint32_t* cones, size_t* count);
+
+/* ---- multi-GPU: the reference's rank algorithm (dist.hpp, dist.cpp:241-361)
+ * with partitioned block storage and per-level exchanges of the boundary
+ * cone-segment interpolants.  Each rank builds the (replicated) structure and
+ * owns its Morton interval of points and, per level, an equal-count interval
+ * of cones (dist.cpp:78-130); it stores only its own blocks plus its halo.
+ *
+ * One process per GPU: rank 0 calls ifgf_comm_unique_id, the launcher
+ * broadcasts the IFGF_COMM_ID_BYTES bytes, every rank calls ifgf_comm_create
+ * (NCCL communicator over NVLink/NVSwitch, loaded on first use).  Then per
+ * matvec configuration ifgf_dist_plan_create_device (collective) and
+ * ifgf_dist_plan_apply_device (collective; full result in the caller's order
+ * on every rank).  ifgf_plan_destroy frees a rank plan. */
+#define IFGF_COMM_ID_BYTES 128
+typedef struct ifgf_comm ifgf_comm;
+int ifgf_comm_unique_id(void* id_out);
+int ifgf_comm_create(const void* id, int rank, int world, int device, ifgf_comm** out);
+void ifgf_comm_destroy(ifgf_comm* comm);
+int ifgf_dist_plan_create_device(ifgf_comm* comm, const double* d_x1, const double* d_x2,
+                                 const double* d_x3, size_t n, int kernel_kind,
+                                 double wavenumber, const ifgf_params* p, void* stream,
+                                 ifgf_plan** out);
+int ifgf_dist_plan_apply_device(ifgf_plan* plan, const double* d_a_re, const double* d_a_im,
+                                double* d_i_re, double* d_i_im, void* stream, ifgf_report* rep);
+
+/* Per-level view of a rank plan.  interp_needed / prop_needed: the foreign
+ * cones this rank reads for interpolation / propagation (dist.cpp:179-237,
+ * deduplicated per (rank, cone) like CommLevelStats); halo_cones: their union
+ * (what the exchange moves in); sent_cones: blocks this rank sends. */
+typedef struct ifgf_dist_level {
+  size_t owned_cones, halo_cones, interp_needed, prop_needed, sent_cones;
+} ifgf_dist_level;
+typedef struct ifgf_dist_info {
+  int rank, world, depth;
+  size_t point_begin, point_end;      /* owned sorted points */
+  ifgf_dist_level levels[IFGF_MAX_LEVELS]; /* index d - 3 */
+  size_t block_bytes;                 /* this rank's block storage (owned + halo) */
+  size_t device_bytes;                /* all of this rank plan's device memory */
+} ifgf_dist_info;
+int ifgf_dist_plan_info(const ifgf_plan* plan, ifgf_dist_info* info);
+
+/* dist::run_distributed (dist.hpp:90): n_ranks rank plans in THIS process on
+ * devices[r] (entries may repeat: several ranks on one GPU), advanced phase
+ * by phase, blocks moved rank to rank by device copies; host arrays in/out,
+ * output in the caller's order, bitwise equal to ifgf_apply.  info (may be
+ * NULL) receives n_ranks entries. */
+int ifgf_run_distributed(size_t n, const double* x1, const double* x2, const double* x3,
+                         const double* a_re, const double* a_im, int kernel_kind,
+                         double wavenumber, const ifgf_params* p, int n_ranks,
+                         const int* devices, double* i_re, double* i_im, ifgf_report* rep,
+                         ifgf_dist_info* info);
 
 /* ---- oracle side (engine.hpp:117-128), computed on the device ---- */
 /* o_* = exact sums at the m listed targets (all points if targets == NULL). */

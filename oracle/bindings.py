@@ -229,6 +229,7 @@ class COracle(_Checker):
         L.oc_error_at_indices.argtypes = [C.c_size_t] + [_dp] * 7 + [
             C.c_int, C.c_double, _u32p, C.c_size_t, C.POINTER(C.c_double)]
         L.oc_partition.argtypes = [C.c_void_p, C.c_int, _u32p, _u32p, _u32p]
+        L.oc_set_threads.argtypes = [C.c_int]
         L.oc_exchange_set.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_int, C.c_void_p,
                                       C.POINTER(C.c_size_t)]
 
@@ -264,14 +265,16 @@ class COracle(_Checker):
         n = len(x1)
         ir, ii = np.zeros(n), np.zeros(n)
         rep = _OcReport()
+        self.lib.oc_set_threads(max(1, p.threads))
         self._check(self.lib.oc_apply(n, _c(x1), _c(x2), _c(x3), _c(ar), _c(ai), kind, k,
                                       C.byref(_OcParams.of(p)), ir, ii, C.byref(rep)))
         return ir, ii, {"seconds": list(rep.seconds), "depth": rep.depth,
                         "peak_live_blocks": rep.peak_live_blocks}
 
-    def direct(self, x1, x2, x3, ar, ai, kind, k, targets=None):
+    def direct(self, x1, x2, x3, ar, ai, kind, k, targets=None, threads=1):
         n = len(x1)
         m = n if targets is None else len(targets)
+        self.lib.oc_set_threads(max(1, threads))
         o_re, o_im = np.zeros(m), np.zeros(m)
         tp = None if targets is None else _c(targets, np.uint32)
         self._check(self.lib.oc_direct_eval(
@@ -393,6 +396,10 @@ class RefOracle(_Checker):
         L.ref_problem_propagation.argtypes = [C.c_void_p, C.c_int, C.c_int, _dp, _dp, _dp, _dp]
         L.ref_problem_interpolation.argtypes = [C.c_void_p, C.c_int, C.c_int, _dp, _dp, _dp, _dp]
         L.ref_problem_partition.argtypes = [C.c_void_p, C.c_int, _u32p, _u32p, _u32p]
+        L.ref_bench_open.restype = C.c_void_p
+        L.ref_bench_open.argtypes = [C.c_void_p]
+        L.ref_bench_close.argtypes = [C.c_void_p]
+        L.ref_bench_slice.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_int, _dp]
 
     def variant(self):
         return self.lib.ref_simd_variant().decode()
@@ -489,6 +496,11 @@ class _RefProblem(_Problem):
         self._chk = chk
         self._threads = p.threads
 
+    def bench(self):
+        """Handle for bench.py's reference leg: the stock passes of apply()
+        on this Problem in S slices (oracle/ref_shim.cpp ref_bench_slice)."""
+        return _RefBench(self)
+
     def singular(self):
         ir, ii = np.zeros(self.n), np.zeros(self.n)
         self._chk._check(self._lib.ref_problem_singular(self._h, 0, self.n, self._threads, ir, ii))
@@ -519,6 +531,28 @@ class _RefProblem(_Problem):
         cb = np.zeros((D - 2) * (R + 1), np.uint32)
         self._chk._check(self._lib.ref_problem_partition(self._h, R, bb, pb, cb))
         return bb, pb, cb.reshape(D - 2, R + 1)
+
+
+class _RefBench:
+    def __init__(self, prob):
+        self._prob = prob  # keeps the Problem alive
+        self._lib = prob._lib
+        h = self._lib.ref_bench_open(prob._h)
+        if not h:
+            raise CheckerError(-1, prob._chk.last_error())
+        self._h = C.c_void_p(h)
+
+    def slice(self, threads, k, S):
+        """Slice k of S of every pass; returns {singular, level_d, interpolation,
+        propagation} seconds."""
+        secs = np.zeros(4)
+        self._prob._chk._check(self._lib.ref_bench_slice(self._h, threads, k, S, secs))
+        return dict(zip(("singular", "level_d", "interpolation", "propagation"), secs.tolist()))
+
+    def __del__(self):
+        if getattr(self, "_h", None):
+            self._lib.ref_bench_close(self._h)
+            self._h = None
 
 
 def rel_l2(got_re, got_im, want_re, want_im):

@@ -12,6 +12,7 @@
 #include "ifgf_oracle.h"
 
 #include <math.h>
+#include <pthread.h>
 #include <stdio.h>
 #include <stdlib.h>
 #include <string.h>
@@ -43,6 +44,72 @@ void oc_default_params(oc_params* p) {
   p->p_s = 3;
   p->p_theta = 5;
   p->p_phi = 5;
+}
+
+/* ------------------------------------------------------------ threading
+ * oc_set_threads(T): the passes, the relevant-cone marking and the direct
+ * sums split their ranges over T pthreads.  Every output slot (a target, a
+ * cone, a box's cone list) is still computed by one thread in the serial
+ * order, so results are bitwise independent of T. */
+static int g_threads = 1;
+void oc_set_threads(int t) { g_threads = t < 1 ? 1 : t; }
+int oc_get_threads(void) { return g_threads; }
+
+typedef int (*range_fn)(void* ctx, size_t b, size_t e);
+typedef struct {
+  range_fn fn;
+  void* ctx;
+  size_t n, chunk, next;
+  int rc;
+  char err[256];
+  pthread_mutex_t mu;
+} par_job;
+
+static void* par_worker(void* arg) {
+  par_job* J = (par_job*)arg;
+  for (;;) {
+    if (__atomic_load_n(&J->rc, __ATOMIC_RELAXED)) break;
+    const size_t b = __atomic_fetch_add(&J->next, J->chunk, __ATOMIC_RELAXED);
+    if (b >= J->n) break;
+    const size_t e = J->n - b > J->chunk ? b + J->chunk : J->n;
+    const int rc = J->fn(J->ctx, b, e);
+    if (rc) {
+      pthread_mutex_lock(&J->mu);
+      if (!J->rc) {
+        J->rc = rc;
+        memcpy(J->err, g_err, sizeof J->err);
+      }
+      pthread_mutex_unlock(&J->mu);
+      break;
+    }
+  }
+  return NULL;
+}
+
+/* fn over [0, n) in chunks; returns the first error code (message in g_err) */
+static int par_for(size_t n, size_t chunk, range_fn fn, void* ctx) {
+  if (!n) return OC_OK;
+  if (chunk < 1) chunk = 1;
+  int T = g_threads;
+  if ((size_t)T > (n + chunk - 1) / chunk) T = (int)((n + chunk - 1) / chunk);
+  if (T <= 1) return fn(ctx, 0, n);
+  par_job J;
+  memset(&J, 0, sizeof J);
+  J.fn = fn;
+  J.ctx = ctx;
+  J.n = n;
+  J.chunk = chunk;
+  pthread_mutex_init(&J.mu, NULL);
+  pthread_t* th = (pthread_t*)malloc((size_t)(T - 1) * sizeof(pthread_t));
+  int started = 0;
+  for (int t = 0; t < T - 1; ++t)
+    if (pthread_create(&th[started], NULL, par_worker, &J) == 0) ++started;
+  par_worker(&J);
+  for (int t = 0; t < started; ++t) pthread_join(th[t], NULL);
+  free(th);
+  pthread_mutex_destroy(&J.mu);
+  if (J.rc) memcpy(g_err, J.err, sizeof J.err);
+  return J.rc;
 }
 
 static double now_s(void) {
@@ -713,21 +780,32 @@ static int build_levels(oc_problem* P) {
 }
 
 /* cones.cpp:90-150: top-down d = 3..D, clause 1 (cousin points) and clause 2
- * (nodes of the parent box's relevant cones). */
-static int relevant_cones(oc_problem* P) {
-  const int D = P->depth;
+ * (nodes of the parent box's relevant cones).  Boxes are independent within a
+ * level: chunks of RC_CHUNK boxes run in parallel (oc_set_threads), each
+ * writing its boxes' sorted unique gammas into its own list, concatenated in
+ * box order afterwards. */
+#define RC_CHUNK 64
+typedef struct {
+  oc_problem* P;
+  int d;
+  vu64* out;      /* per chunk: the chunk's boxes' gammas, box order */
+  uint32_t* cnt;  /* per box: number of relevant cones */
+} rc_ctx;
+
+static int rc_chunks(void* vctx, size_t c0, size_t c1) {
+  rc_ctx* X = (rc_ctx*)vctx;
+  oc_problem* P = X->P;
+  const int d = X->d;
   const int np = P->p.p_s * P->p.p_theta * P->p.p_phi;
+  oc_level* L = &P->lv[d];
+  const oc_level* U = d > 3 ? &P->lv[d - 1] : NULL;
   double* nodes = (double*)malloc(3 * (size_t)np * sizeof(double));
   vu64 gam = {0, 0, 0};
   int rc = OC_OK;
-  for (int d = 3; d <= D && rc == OC_OK; ++d) {
-    oc_level* L = &P->lv[d];
-    L->g = level_geom(&P->p, D, d);
-    L->box_cone = (uint32_t*)calloc(L->nb + 1, sizeof(uint32_t));
-    vu32 cb = {0, 0, 0};
-    vu64 cg = {0, 0, 0};
-    const oc_level* U = d > 3 ? &P->lv[d - 1] : NULL;
-    for (size_t b = 0; b < L->nb && rc == OC_OK; ++b) {
+  for (size_t ch = c0; ch < c1 && rc == OC_OK; ++ch) {
+    vu64* cg = &X->out[ch];
+    const size_t b1 = (ch + 1) * RC_CHUNK < L->nb ? (ch + 1) * RC_CHUNK : L->nb;
+    for (size_t b = ch * RC_CHUNK; b < b1 && rc == OC_OK; ++b) {
       gam.n = 0;
       const double* c = &L->ctr[3 * b];
       for (uint32_t ci = L->cous_off[b]; ci < L->cous_off[b + 1] && rc == OC_OK; ++ci) {
@@ -751,19 +829,49 @@ static int relevant_cones(oc_problem* P) {
         }
       }
       qsort(gam.v, gam.n, sizeof(uint64_t), cmp_u64);
+      uint32_t k = 0;
       for (size_t i = 0; i < gam.n; ++i) {
         if (i > 0 && gam.v[i] == gam.v[i - 1]) continue;
-        vu32_push(&cb, (uint32_t)b);
-        vu64_push(&cg, gam.v[i]);
+        vu64_push(cg, gam.v[i]);
+        ++k;
       }
-      L->box_cone[b + 1] = (uint32_t)cg.n;
+      X->cnt[b] = k;
     }
-    L->nc = cg.n;
-    L->cone_box = cb.v;
-    L->cone_gamma = cg.v;
   }
   free(gam.v);
   free(nodes);
+  return rc;
+}
+
+static int relevant_cones(oc_problem* P) {
+  const int D = P->depth;
+  int rc = OC_OK;
+  for (int d = 3; d <= D && rc == OC_OK; ++d) {
+    oc_level* L = &P->lv[d];
+    L->g = level_geom(&P->p, D, d);
+    L->box_cone = (uint32_t*)calloc(L->nb + 1, sizeof(uint32_t));
+    const size_t nch = (L->nb + RC_CHUNK - 1) / RC_CHUNK;
+    rc_ctx X = {P, d, (vu64*)calloc(nch ? nch : 1, sizeof(vu64)),
+                (uint32_t*)calloc(L->nb ? L->nb : 1, sizeof(uint32_t))};
+    rc = par_for(nch, 1, rc_chunks, &X);
+    if (rc == OC_OK) {
+      for (size_t b = 0; b < L->nb; ++b) L->box_cone[b + 1] = L->box_cone[b] + X.cnt[b];
+      const size_t nc = L->box_cone[L->nb];
+      L->nc = nc;
+      L->cone_box = (uint32_t*)malloc((nc ? nc : 1) * sizeof(uint32_t));
+      L->cone_gamma = (uint64_t*)malloc((nc ? nc : 1) * sizeof(uint64_t));
+      size_t o = 0;
+      for (size_t ch = 0; ch < nch; ++ch) {
+        if (X.out[ch].n) memcpy(L->cone_gamma + o, X.out[ch].v, X.out[ch].n * sizeof(uint64_t));
+        o += X.out[ch].n;
+      }
+      for (size_t b = 0; b < L->nb; ++b)
+        for (uint32_t q = L->box_cone[b]; q < L->box_cone[b + 1]; ++q) L->cone_box[q] = (uint32_t)b;
+    }
+    for (size_t ch = 0; ch < nch; ++ch) free(X.out[ch].v);
+    free(X.out);
+    free(X.cnt);
+  }
   return rc;
 }
 
@@ -1054,6 +1162,32 @@ int oc_interpolation_pass(const oc_problem* P, int d, const double* bre, const d
   return OC_OK;
 }
 
+/* Range-parallel drivers of the passes (oc_set_threads); each target / cone
+ * is computed by exactly one thread with the serial arithmetic. */
+typedef struct {
+  const oc_problem* P;
+  int d;
+  const double *in_re, *in_im;
+  double *out_re, *out_im;
+} pass_ctx;
+static int par_singular(void* v, size_t b, size_t e) {
+  pass_ctx* X = (pass_ctx*)v;
+  return oc_singular_pass(X->P, b, e, X->out_re, X->out_im);
+}
+static int par_level_d(void* v, size_t b, size_t e) {
+  pass_ctx* X = (pass_ctx*)v;
+  return oc_level_d_pass(X->P, (uint32_t)b, (uint32_t)e, X->out_re, X->out_im);
+}
+static int par_interp(void* v, size_t b, size_t e) {
+  pass_ctx* X = (pass_ctx*)v;
+  return oc_interpolation_pass(X->P, X->d, X->in_re, X->in_im, b, e, X->out_re, X->out_im);
+}
+static int par_prop(void* v, size_t b, size_t e) {
+  pass_ctx* X = (pass_ctx*)v;
+  return oc_propagation_pass(X->P, X->d, X->in_re, X->in_im, (uint32_t)b, (uint32_t)e,
+                             X->out_re, X->out_im);
+}
+
 /* ------------------------------------------------------------------- apply */
 int oc_apply(size_t n, const double* x1, const double* x2, const double* x3,
              const double* a_re, const double* a_im, int kind, double wavenumber,
@@ -1072,18 +1206,27 @@ int oc_apply(size_t n, const double* x1, const double* x2, const double* x3,
   double* sr = (double*)calloc(n, sizeof(double));
   double* si = (double*)calloc(n, sizeof(double));
   t0 = now_s();
-  oc_singular_pass(P, 0, n, sr, si);
+  {
+    pass_ctx X = {P, 0, NULL, NULL, sr, si};
+    rc = par_for(n, 4096, par_singular, &X);
+  }
   r.seconds[1] = now_s() - t0;
   size_t ncur = P->lv[D].nc;
   double* cre = (double*)calloc(ncur * np + 1, sizeof(double));
   double* cim = (double*)calloc(ncur * np + 1, sizeof(double));
   r.peak_live_blocks = ncur;
   t0 = now_s();
-  rc = oc_level_d_pass(P, 0, (uint32_t)ncur, cre, cim);
+  if (!rc) {
+    pass_ctx X = {P, D, NULL, NULL, cre, cim};
+    rc = par_for(ncur, 32, par_level_d, &X);
+  }
   r.seconds[2] = now_s() - t0;
   for (int d = D; d >= 3 && !rc; --d) {
     t0 = now_s();
-    rc = oc_interpolation_pass(P, d, cre, cim, 0, n, sr, si);
+    {
+      pass_ctx X = {P, d, cre, cim, sr, si};
+      rc = par_for(n, 4096, par_interp, &X);
+    }
     r.seconds[3] += now_s() - t0;
     if (rc || d == 3) break;
     const size_t npar = P->lv[d - 1].nc;
@@ -1091,7 +1234,10 @@ int oc_apply(size_t n, const double* x1, const double* x2, const double* x3,
     double* pre = (double*)calloc(npar * np + 1, sizeof(double));
     double* pim = (double*)calloc(npar * np + 1, sizeof(double));
     t0 = now_s();
-    rc = oc_propagation_pass(P, d, cre, cim, 0, (uint32_t)npar, pre, pim);
+    {
+      pass_ctx X = {P, d, cre, cim, pre, pim};
+      rc = par_for(npar, 32, par_prop, &X);
+    }
     r.seconds[4] += now_s() - t0;
     free(cre);
     free(cim);
@@ -1115,18 +1261,30 @@ int oc_apply(size_t n, const double* x1, const double* x2, const double* x3,
   return rc;
 }
 
+typedef struct {
+  size_t n;
+  const double *x1, *x2, *x3, *ar, *ai;
+  double kappa;
+  const uint32_t* targets;
+  double *o_re, *o_im;
+} direct_ctx;
+static int par_direct(void* v, size_t b, size_t e) {
+  const direct_ctx* X = (const direct_ctx*)v;
+  for (size_t j = b; j < e; ++j) {
+    const size_t i = X->targets ? X->targets[j] : j;
+    green_sum(X->x1, X->x2, X->x3, X->ar, X->ai, 0, X->n, i, X->x1[i], X->x2[i], X->x3[i],
+              X->kappa, &X->o_re[j], &X->o_im[j]);
+  }
+  return OC_OK;
+}
+
 /* engine.cpp:327-339 restricted to a target list (all points when targets == NULL) */
 int oc_direct_eval(size_t n, const double* x1, const double* x2, const double* x3,
                    const double* a_re, const double* a_im, int kind, double wavenumber,
                    const uint32_t* targets, size_t m, double* o_re, double* o_im) {
   if (n < 2) return fail(OC_EINVAL, "direct_eval: need at least two points");
-  const double kappa = kind == 1 ? 0.0 : wavenumber;
-  const size_t cnt = targets ? m : n;
-  for (size_t j = 0; j < cnt; ++j) {
-    const size_t i = targets ? targets[j] : j;
-    green_sum(x1, x2, x3, a_re, a_im, 0, n, i, x1[i], x2[i], x3[i], kappa, &o_re[j], &o_im[j]);
-  }
-  return OC_OK;
+  direct_ctx X = {n, x1, x2, x3, a_re, a_im, kind == 1 ? 0.0 : wavenumber, targets, o_re, o_im};
+  return par_for(targets ? m : n, 4, par_direct, &X);
 }
 
 /* engine.cpp:341-352 */

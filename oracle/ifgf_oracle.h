@@ -6,7 +6,7 @@
  * It is pinned against the unmodified reference (oracle/_ref, built by
  * oracle/Makefile) and against tests/golden/ fixtures generated from it.
  *
- * Plain C11, single-threaded, no FMA contraction (-ffp-contract=off), libm
+ * Plain C11, no FMA contraction (-ffp-contract=off), libm
  * transcendentals.  Each function cites the reference file:line it restates
  * (paths relative to /root/reference/proj).
  */
@@ -33,6 +33,10 @@ typedef struct oc_params {
 
 void oc_default_params(oc_params* p);
 const char* oc_last_error(void);
+/* Threads used by oc_apply, oc_problem_build's cone marking and
+ * oc_direct_eval (default 1).  Results are bitwise independent of it. */
+void oc_set_threads(int threads);
+int oc_get_threads(void);
 
 /* ---- seeded synthetic inputs (shared spec with the product generator) ---- */
 uint64_t oc_mt64_first(uint64_t seed, int k); /* k-th output of mt19937_64(seed) */

@@ -14,6 +14,7 @@
 // include/ifgf_b200.h (0 ok, 1 invalid_argument, 2 domain_error,
 // 3 logic_error, 4 runtime_error).
 
+#include <chrono>
 #include <cstdint>
 #include <cstring>
 #include <exception>
@@ -387,6 +388,87 @@ int ref_write_points_binary(const char* path, std::size_t n, const double* x1, c
     std::memcpy(pc.a_re.data(), a_re, n * 8);
     std::memcpy(pc.a_im.data(), a_im, n * 8);
     write_points_binary(path, pc);
+  });
+}
+
+}  // extern "C"
+
+// ------------------------------------------------------------- bench leg --
+// bench.py --impl reference: the stock passes of apply() (engine.cpp:270-315)
+// on a Problem built once, each pass restricted to slice k of S equal
+// sub-ranges of its work items (points / cones), so S consecutive calls run
+// exactly one full matvec minus setup.  The block stores of every level are
+// allocated once (zero-filled) when the bench handle opens, outside timing;
+// the stock apply() allocates them per call, so the timed passes favour the
+// reference slightly.
+namespace {
+struct RefBench {
+  RefProblem* P = nullptr;
+  std::vector<BlockStore> st;  // index d
+  std::vector<double> ire, iim;
+};
+}  // namespace
+
+extern "C" {
+
+void* ref_bench_open(void* problem) {
+  RefBench* b = nullptr;
+  const int rc = guarded([&] {
+    auto B = std::make_unique<RefBench>();
+    B->P = static_cast<RefProblem*>(problem);
+    const Problem& pr = B->P->prob;
+    const int D = pr.depth, Pn = B->P->params.orders.total();
+    B->st.resize(D + 1);
+    for (int d = 3; d <= D; ++d) B->st[d].allocate(pr.cones.level(d).size(), Pn);
+    B->ire.assign(pr.cloud.size(), 0.0);
+    B->iim.assign(pr.cloud.size(), 0.0);
+    b = B.release();
+  });
+  return rc == 0 ? b : nullptr;
+}
+
+void ref_bench_close(void* b) { delete static_cast<RefBench*>(b); }
+
+// secs = {singular, level_d, interpolation, propagation}
+int ref_bench_slice(void* hb, int threads, int k, int S, double* secs) {
+  auto* B = static_cast<RefBench*>(hb);
+  return guarded([&] {
+    using clk = std::chrono::steady_clock;
+    auto since = [](clk::time_point t) {
+      return std::chrono::duration<double>(clk::now() - t).count();
+    };
+    const Problem& pr = B->P->prob;
+    const KernelConfig& cfg = B->P->cfg;
+    const int D = pr.depth;
+    auto part = [&](std::size_t n, std::size_t& b, std::size_t& e) {
+      b = n * static_cast<std::size_t>(k) / S;
+      e = n * static_cast<std::size_t>(k + 1) / S;
+    };
+    std::size_t b, e;
+    auto t0 = clk::now();
+    part(pr.cloud.size(), b, e);
+    singular_pass(pr, cfg, b, e, threads, B->ire, B->iim);
+    secs[0] = since(t0);
+    t0 = clk::now();
+    part(pr.cones.level(D).size(), b, e);
+    eval_level_d(pr, cfg, static_cast<std::uint32_t>(b), static_cast<std::uint32_t>(e), threads,
+                 B->st[D]);
+    secs[1] = since(t0);
+    secs[2] = secs[3] = 0.0;
+    for (int d = D; d >= 3; --d) {
+      const BlockTable table = BlockTable::all_of(B->st[d], pr.cones.level(d).size());
+      t0 = clk::now();
+      part(pr.cloud.size(), b, e);
+      interpolation_pass(pr, cfg, d, table, b, e, threads, B->ire, B->iim);
+      secs[2] += since(t0);
+      if (d > 3) {
+        t0 = clk::now();
+        part(pr.cones.level(d - 1).size(), b, e);
+        propagation_pass(pr, cfg, d, table, static_cast<std::uint32_t>(b),
+                         static_cast<std::uint32_t>(e), threads, B->st[d - 1]);
+        secs[3] += since(t0);
+      }
+    }
   });
 }
 

@@ -20,7 +20,8 @@ MAX_LEVELS = 22
 class CParams(C.Structure):
     _fields_ = [("depth", C.c_int), ("box_lambda", C.c_double), ("points_per_box", C.c_int),
                 ("base_s", C.c_int), ("base_theta", C.c_int), ("base_phi", C.c_int),
-                ("p_s", C.c_int), ("p_theta", C.c_int), ("p_phi", C.c_int), ("device", C.c_int)]
+                ("p_s", C.c_int), ("p_theta", C.c_int), ("p_phi", C.c_int), ("device", C.c_int),
+                ("partition", C.c_int)]
 
 
 class CReport(C.Structure):
@@ -43,6 +44,21 @@ class CPlanInfo(C.Structure):
                 ("setup_launches", C.c_size_t),
                 ("launches", C.c_size_t)]
 
+
+class CDistLevel(C.Structure):
+    _fields_ = [("owned_cones", C.c_size_t), ("halo_cones", C.c_size_t),
+                ("interp_needed", C.c_size_t), ("prop_needed", C.c_size_t),
+                ("sent_cones", C.c_size_t)]
+
+
+class CDistInfo(C.Structure):
+    _fields_ = [("rank", C.c_int), ("world", C.c_int), ("depth", C.c_int),
+                ("point_begin", C.c_size_t), ("point_end", C.c_size_t),
+                ("levels", CDistLevel * MAX_LEVELS), ("block_bytes", C.c_size_t),
+                ("device_bytes", C.c_size_t)]
+
+
+COMM_ID_BYTES = 128
 
 _dp = np.ctypeslib.ndpointer(dtype=np.float64, flags="C_CONTIGUOUS")
 _u32p = np.ctypeslib.ndpointer(dtype=np.uint32, flags="C_CONTIGUOUS")
@@ -87,6 +103,17 @@ SIGNATURES = {
     "ifgf_plan_partition": (C.c_int, [_vp, C.c_int, _vp, _vp, _vp]),
     "ifgf_plan_exchange_set": (C.c_int, [_vp, C.c_int, C.c_int, C.c_int, C.c_int, _vp,
                                          C.POINTER(C.c_size_t)]),
+    "ifgf_comm_unique_id": (C.c_int, [_vp]),
+    "ifgf_comm_create": (C.c_int, [_vp, C.c_int, C.c_int, C.c_int, _PP]),
+    "ifgf_comm_destroy": (None, [_vp]),
+    "ifgf_dist_plan_create_device": (C.c_int, [_vp, _vp, _vp, _vp, _sz, C.c_int, C.c_double,
+                                               C.POINTER(CParams), _vp, _PP]),
+    "ifgf_dist_plan_apply_device": (C.c_int, [_vp, _vp, _vp, _vp, _vp, _vp,
+                                              C.POINTER(CReport)]),
+    "ifgf_dist_plan_info": (C.c_int, [_vp, C.POINTER(CDistInfo)]),
+    "ifgf_run_distributed": (C.c_int, [_sz, _vp, _vp, _vp, _vp, _vp, C.c_int, C.c_double,
+                                       C.POINTER(CParams), C.c_int, _vp, _vp, _vp,
+                                       C.POINTER(CReport), _vp]),
     "ifgf_direct_eval": (C.c_int, [_sz, _vp, _vp, _vp, _vp, _vp, C.c_int, C.c_double, _vp, _sz,
                                    C.c_int, _vp, _vp]),
     "ifgf_sample_indices": (C.c_int, [_sz, _sz, C.c_uint64, _vp]),

@@ -147,30 +147,26 @@ def _evaluate(b: Built, ranks: int):
                 "n": rep.n, "depth": rep.depth, "h_level_d": rep.h_level_d,
                 "levels": [{"d": l.d, "boxes": l.boxes, "cones": l.cones} for l in rep.levels],
                 "peak_live_blocks": rep.peak_live_blocks}, None
-    t0 = time.perf_counter()
-    plans = [Plan.from_cloud(b.pc, b.cfg, b.params) for _ in range(ranks)]
-    t1 = time.perf_counter()
+    # the result from the C++ rank group (ifgf_run_distributed); the
+    # reference's CommStats from the device exchange sets of one plan
+    drep, _ = dist.run_distributed(b.pc, b.cfg, b.params, ranks)
+    plan = Plan.from_cloud(b.pc, b.cfg, b.params)
     try:
-        secs = [0.0] * ranks
-        i_re, i_im, _, ex = dist.simulate(plans, b.pc.a_re, b.pc.a_im, rank_seconds=secs)
-        t2 = time.perf_counter()
-        b.pc.i_re[:] = i_re
-        b.pc.i_im[:] = i_im
-        p0 = plans[0]
-        comm = CommStats(ex, p0, ranks)
-        D = p0.depth
-        rep = {"seconds": {"setup": (t1 - t0) / ranks, "singular": 0.0, "level_d_eval": 0.0,
-                           "interpolation": 0.0, "propagation": 0.0,
-                           "total": (t1 - t0) / ranks + (t2 - t1)},
-               "n": b.pc.size(), "depth": D, "h_level_d": p0.info.h[D],
-               "levels": [{"d": d, "boxes": p0.n_boxes(d), "cones": p0.n_cones(d)}
+        ex = dist.build_exchange_plan(dist.rank_layout(plan, ranks), plan.depth,
+                                      lambda r, d, kind: plan.exchange_set(ranks, r, d, kind))
+        comm = CommStats(ex, plan, ranks)
+        D = plan.depth
+        s = drep.seconds
+        rep = {"seconds": {"setup": s.setup, "singular": 0.0, "level_d_eval": 0.0,
+                           "interpolation": 0.0, "propagation": 0.0, "total": s.total},
+               "n": b.pc.size(), "depth": D, "h_level_d": plan.info.h[D],
+               "levels": [{"d": d, "boxes": plan.n_boxes(d), "cones": plan.n_cones(d)}
                           for d in range(3, D + 1)],
-               "peak_live_blocks": int(max(p0.n_cones(d) + (p0.n_cones(d - 1) if d > 3 else 0)
+               "peak_live_blocks": int(max(plan.n_cones(d) + (plan.n_cones(d - 1) if d > 3 else 0)
                                            for d in range(3, D + 1)))}
         return rep, comm
     finally:
-        for p in plans:
-            p.close()
+        plan.close()
 
 
 def report_json(o, b: Built, rep, comm, eps: float, m_used: int) -> dict:

@@ -51,6 +51,8 @@ int guarded(F&& f) {
 using clk = std::chrono::steady_clock;
 double since(clk::time_point t0) { return std::chrono::duration<double>(clk::now() - t0).count(); }
 
+void tune_pool(int device);
+
 void require_device(int device) {
   int count = 0;
   const cudaError_t e = cudaGetDeviceCount(&count);
@@ -69,16 +71,37 @@ void require_device(int device) {
                                    " is not sm_100 (this build targets sm_100a only)");
   }
   IFGF_CUDA(cudaSetDevice(device));
-  static bool pool_tuned = false;
-  if (!pool_tuned) {
-    cudaMemPool_t pool;
-    if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
-      uint64_t thr = UINT64_MAX;
-      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
-    }
-    pool_tuned = true;
-  }
+  tune_pool(device);
 }
+
+// Keep freed stream-ordered memory in each device's default pool (a release
+// threshold of 0 returns it to the driver at every sync point: 20-80 ms setup
+// spikes).  Once per device ordinal.
+void tune_pool(int device) {
+  static std::mutex mu;
+  static uint64_t tuned = 0;  // bit per device ordinal
+  if (device < 0 || device >= 64) return;
+  std::lock_guard<std::mutex> g(mu);
+  if (tuned >> device & 1) return;
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+    uint64_t thr = UINT64_MAX;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+  }
+  tuned |= 1ull << device;
+}
+
+// Restores the caller's current device when an entry point returns (the C
+// ABI switches to the plan's device internally).
+struct DeviceGuard {
+  int prev = -1;
+  DeviceGuard() {
+    if (cudaGetDevice(&prev) != cudaSuccess) prev = -1;
+  }
+  ~DeviceGuard() {
+    if (prev >= 0) cudaSetDevice(prev);
+  }
+};
 
 void validate_params(const ifgf_params* p) {
   if (!p) throw Error(IFGF_EINVAL, "null params");
@@ -152,6 +175,7 @@ void give_stream(int device, cudaStream_t s) {
 void plan_free(ifgf_plan* P) {
   if (!P) return;
   cudaSetDevice(P->device);
+  dist_free(P);
   if (P->s_aux) cudaStreamSynchronize(P->s_aux);
   // stream-ordered frees back into the pool (a cudaFree per allocation would
   // synchronise the device ~150 times)
@@ -182,6 +206,9 @@ ifgf_plan* new_plan(size_t n, int kind, double wavenumber, const ifgf_params* p)
   P->kappa = kind == IFGF_LAPLACE ? 0.0 : wavenumber;  // KernelConfig::kappa, kernel.hpp:20
   P->params = *p;
   P->K = make_consts(p);
+  if (p->partition != IFGF_PARTITION_COUNT && p->partition != IFGF_PARTITION_WORK)
+    throw Error(IFGF_EINVAL, "unknown partition mode");
+  P->partition_mode = p->partition;
   try {
     P->s_main = take_stream(P->device);
     P->s_aux = take_stream(P->device);
@@ -339,6 +366,13 @@ void apply_device(ifgf_plan* P, const double* a_re, const double* a_im, double* 
   }
 }
 
+// 2n doubles of host<->device staging for the pass-level API, allocated once
+// per plan (each call synchronises before returning, so calls can share it).
+double* staging(ifgf_plan* P) {
+  if (!P->staging) P->staging = P->alloc<double>(2 * P->n);
+  return P->staging;
+}
+
 double2* stage_blocks(ifgf_plan* P, int d) {
   if (d < 3 || d > P->depth) throw Error(IFGF_EINVAL, "level out of range");
   if (!P->stage_blocks[d]) {
@@ -356,6 +390,10 @@ std::vector<T> d2h(const T* d, size_t count, cudaStream_t s) {
   IFGF_CUDA(cudaStreamSynchronize(s));
   return h;
 }
+
+}  // namespace
+
+namespace ifgf_b200 {
 
 // dist.cpp:78-130 (partition), on host arrays of the level-D boxes.
 // Cut [0, n) into R contiguous intervals of about equal weight (w: per unit,
@@ -471,70 +509,8 @@ void partition_host(ifgf_plan* P, int R, uint32_t* box_begin, uint32_t* point_be
     }
 }
 
-// Owner of cone q at a level, from that level's R+1 cone boundaries.
-__device__ __forceinline__ int cone_owner(uint32_t q, const uint32_t* cb, int R) {
-  int r = 0;
-  while (r < R - 1 && q >= cb[r + 1]) ++r;
-  return r;
-}
 
-// dist.cpp:179-201: cones of level d holding (via cone_of_point) the owned
-// points as seen from their cousins; foreign ones are flagged.
-__global__ void k_need_interp(const __grid_constant__ LevelDev L, const uint32_t* __restrict__ ptbox,
-                              const double* xs, const double* ys, const double* zs, uint32_t p0,
-                              uint32_t p1, const uint32_t* bounds, int R, int rank,
-                              uint8_t* need, int* err) {
-  const uint32_t i = p0 + blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= p1) return;
-  const uint32_t b = ptbox[i];
-  for (uint32_t k = L.cous_off[b]; k < L.cous_off[b + 1]; ++k) {
-    const uint32_t cb = L.cous[k];
-    uint32_t g;
-    const int e = cone_of_point_fast(L, L.cx[cb], L.cy[cb], L.cz[cb], xs[i], ys[i], zs[i], g);
-    if (e) {
-      raise_err(err, e);
-      return;
-    }
-    const uint32_t q = find_cone(L, cb, g);
-    if (q == 0xffffffffu) {
-      raise_err(err, kErrInterpCover);
-      return;
-    }
-    if (cone_owner(q, bounds, R) != rank) need[q] = 1;
-  }
-}
-
-// dist.cpp:206-237: child cones of level d hit by the nodes of the owned
-// parent cones of level d-1.
-__global__ void k_need_prop(const __grid_constant__ LevelDev L, const __grid_constant__ LevelDev U,
-                            const __grid_constant__ InterpConsts K, uint32_t q0, uint32_t q1,
-                            const uint32_t* bounds, int R, int rank, uint8_t* need, int* err) {
-  const size_t t = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
-  if (t >= (size_t)(q1 - q0) * K.P) return;
-  const uint32_t q = q0 + (uint32_t)(t / K.P);
-  const int m = (int)(t % K.P);
-  const int jp = m % K.pp, jt = (m / K.pp) % K.pt, js = m / (K.pp * K.pt);
-  const uint32_t pb = U.cone_box[q];
-  const SegMid sg = segment_mid(U, U.cone_gamma[q]);
-  double x, y, z;
-  node_position(sg, U.rad, U.cx[pb], U.cy[pb], U.cz[pb], K.ns[js], K.nt[jt], K.np[jp], x, y, z);
-  for (uint32_t cb = U.child_begin[pb]; cb < U.child_begin[pb + 1]; ++cb) {
-    uint32_t g;
-    const int e = cone_of_point_fast(L, L.cx[cb], L.cy[cb], L.cz[cb], x, y, z, g);
-    if (e) {
-      raise_err(err, e);
-      return;
-    }
-    const uint32_t cq = find_cone(L, cb, g);
-    if (cq == 0xffffffffu) {
-      raise_err(err, kErrPropCover);
-      return;
-    }
-    if (cone_owner(cq, bounds, R) != rank) need[cq] = 1;
-  }
-}
-
-}  // namespace
+}  // namespace ifgf_b200
 
 extern "C" {
 
@@ -553,10 +529,20 @@ void ifgf_default_params(ifgf_params* p) {
   p->p_theta = 5;
   p->p_phi = 5;
   p->device = 0;
+  p->partition = IFGF_PARTITION_COUNT;
 }
 
 int ifgf_device_ok(void) {
-  return guarded([] { require_device(0); }) == IFGF_OK ? 1 : 0;
+  // the caller's current device (bench.py: torch.cuda.set_device(local_rank)),
+  // left current on return
+  DeviceGuard keep;
+  return guarded([] {
+           int dev = 0;
+           if (cudaGetDevice(&dev) != cudaSuccess) dev = 0;
+           require_device(dev);
+         }) == IFGF_OK
+             ? 1
+             : 0;
 }
 
 int ifgf_choose_depth(size_t n, double side, double kappa, const ifgf_params* p, int* out) {
@@ -580,6 +566,7 @@ int ifgf_choose_depth(size_t n, double side, double kappa, const ifgf_params* p,
 int ifgf_plan_create_device(const double* dx, const double* dy, const double* dz, size_t n,
                             int kind, double k, const ifgf_params* p, void* stream,
                             ifgf_plan** out) {
+  DeviceGuard keep;
   return guarded([&] {
     if (!out) throw Error(IFGF_EINVAL, "null output");
     *out = nullptr;
@@ -601,6 +588,7 @@ int ifgf_plan_create_device(const double* dx, const double* dy, const double* dz
 
 int ifgf_plan_create(const double* x1, const double* x2, const double* x3, size_t n, int kind,
                      double k, const ifgf_params* p, ifgf_plan** out) {
+  DeviceGuard keep;
   return guarded([&] {
     if (!out) throw Error(IFGF_EINVAL, "null output");
     *out = nullptr;
@@ -623,7 +611,10 @@ int ifgf_plan_create(const double* x1, const double* x2, const double* x3, size_
   });
 }
 
-void ifgf_plan_destroy(ifgf_plan* plan) { plan_free(plan); }
+void ifgf_plan_destroy(ifgf_plan* plan) {
+  DeviceGuard keep;
+  plan_free(plan);
+}
 
 int ifgf_plan_set_option(ifgf_plan* P, int option, int value) {
   return guarded([&] {
@@ -650,6 +641,7 @@ int ifgf_plan_set_option(ifgf_plan* P, int option, int value) {
 
 int ifgf_plan_apply_device(ifgf_plan* P, const double* a_re, const double* a_im, double* i_re,
                            double* i_im, void* stream, ifgf_report* rep) {
+  DeviceGuard keep;
   return guarded([&] {
     if (!P || !a_re || !i_re || !i_im) throw Error(IFGF_EINVAL, "null argument");
     if (P->n < 2) throw Error(IFGF_EINVAL, "apply: need at least two points");
@@ -659,6 +651,7 @@ int ifgf_plan_apply_device(ifgf_plan* P, const double* a_re, const double* a_im,
 
 int ifgf_plan_apply(ifgf_plan* P, const double* a_re, const double* a_im, double* i_re,
                     double* i_im, ifgf_report* rep) {
+  DeviceGuard keep;
   return guarded([&] {
     if (!P || !a_re || !i_re || !i_im) throw Error(IFGF_EINVAL, "null argument");
     if (P->n < 2) throw Error(IFGF_EINVAL, "apply: need at least two points");
@@ -804,7 +797,7 @@ int ifgf_plan_set_density(ifgf_plan* P, const double* a_re, const double* a_im) 
     if (!P || !a_re) throw Error(IFGF_EINVAL, "null argument");
     IFGF_CUDA(cudaSetDevice(P->device));
     const size_t n = P->n;
-    double* buf = P->alloc<double>(2 * n);
+    double* buf = staging(P);
     IFGF_CUDA(cudaMemcpyAsync(buf, a_re, n * 8, cudaMemcpyHostToDevice, P->s_main));
     if (a_im) IFGF_CUDA(cudaMemcpyAsync(buf + n, a_im, n * 8, cudaMemcpyHostToDevice, P->s_main));
     // gather without touching the result buffer
@@ -913,7 +906,7 @@ int ifgf_plan_read_result(ifgf_plan* P, int sorted, double* i_re, double* i_im) 
       IFGF_CUDA(cudaStreamSynchronize(P->s_main));
       return;
     }
-    double* buf = P->alloc<double>(2 * n);
+    double* buf = staging(P);
     launch_scatter_result(P, buf, buf + n, P->s_main);
     IFGF_CUDA(cudaMemcpyAsync(i_re, buf, n * 8, cudaMemcpyDeviceToHost, P->s_main));
     IFGF_CUDA(cudaMemcpyAsync(i_im, buf + n, n * 8, cudaMemcpyDeviceToHost, P->s_main));
@@ -923,24 +916,51 @@ int ifgf_plan_read_result(ifgf_plan* P, int sorted, double* i_re, double* i_im) 
 
 int ifgf_plan_block_stride(const ifgf_plan* P) { return P ? P->K.Pst : 0; }
 
+// Pack/unpack run on the caller's stream but touch the plan's level storage,
+// which the passes (and stage_blocks' first-use zero fill) use on s_main: the
+// caller's stream first waits for s_main, and s_main then waits for the copy,
+// so a pass issued after an unpack never reads blocks the unpack has not
+// written, and an unpack never overwrites blocks a pending pass still reads.
+void order_with_main(ifgf_plan* P, cudaStream_t s, bool before) {
+  cudaEvent_t e;
+  IFGF_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  if (before) {
+    IFGF_CUDA(cudaEventRecord(e, P->s_main));
+    IFGF_CUDA(cudaStreamWaitEvent(s, e, 0));
+  } else {
+    IFGF_CUDA(cudaEventRecord(e, s));
+    IFGF_CUDA(cudaStreamWaitEvent(P->s_main, e, 0));
+  }
+  cudaEventDestroy(e);
+}
+
 int ifgf_plan_pack_blocks(ifgf_plan* P, int d, const uint32_t* d_cones, size_t m, double* d_buf,
                           void* stream) {
+  DeviceGuard keep;
   return guarded([&] {
     if (!P) throw Error(IFGF_EINVAL, "null plan");
+    IFGF_CUDA(cudaSetDevice(P->device));
+    const cudaStream_t s = static_cast<cudaStream_t>(stream);
     double2* blk = stage_blocks(P, d);  // the pass-level API's level storage
-    launch_pack(P, blk, d_cones, m, d_buf, 0, nullptr, static_cast<cudaStream_t>(stream));
+    order_with_main(P, s, true);
+    launch_pack(P, blk, d_cones, m, P->lv[d].nc, d_buf, 0, nullptr, s);
     IFGF_CUDA(cudaGetLastError());
+    order_with_main(P, s, false);
   });
 }
 
 int ifgf_plan_unpack_blocks(ifgf_plan* P, int d, const uint32_t* d_cones, size_t m,
                             const double* d_buf, void* stream) {
+  DeviceGuard keep;
   return guarded([&] {
     if (!P) throw Error(IFGF_EINVAL, "null plan");
+    IFGF_CUDA(cudaSetDevice(P->device));
+    const cudaStream_t s = static_cast<cudaStream_t>(stream);
     double2* blk = stage_blocks(P, d);
-    launch_pack(P, nullptr, d_cones, m, const_cast<double*>(d_buf), 1, blk,
-                static_cast<cudaStream_t>(stream));
+    order_with_main(P, s, true);
+    launch_pack(P, nullptr, d_cones, m, P->lv[d].nc, const_cast<double*>(d_buf), 1, blk, s);
     IFGF_CUDA(cudaGetLastError());
+    order_with_main(P, s, false);
   });
 }
 
@@ -957,30 +977,33 @@ int ifgf_plan_exchange_set(ifgf_plan* P, int R, int rank, int d, int kind, uint3
   return guarded([&] {
     if (!P || !count) throw Error(IFGF_EINVAL, "null argument");
     if (rank < 0 || rank >= R) throw Error(IFGF_EINVAL, "rank out of range");
+    if (P->dist) throw Error(IFGF_EINVAL, "exchange_set: not on a rank plan of a group");
     if (d < 3 || d > P->depth || (kind == 1 && d < 4) || kind < 0 || kind > 1)
       throw Error(IFGF_EINVAL, "bad level or kind");
     std::vector<uint32_t> bb(R + 1), pb(R + 1), cb((size_t)(P->depth - 2) * (R + 1));
     partition_host(P, R, bb.data(), pb.data(), cb.data());
     const Level& L = P->lv[d];
-    uint8_t* need = P->alloc<uint8_t>(L.nc + 1);
+    // call-scoped scratch, returned to the pool when the call ends
+    struct Tmp {
+      void* p = nullptr;
+      cudaStream_t s;
+      ~Tmp() {
+        if (p) cudaFreeAsync(p, s);
+      }
+    } t_need{nullptr, P->s_main}, t_cb{nullptr, P->s_main};
+    IFGF_CUDA(cudaMallocAsync(&t_need.p, L.nc + 1, P->s_main));
+    IFGF_CUDA(cudaMallocAsync(&t_cb.p, (R + 1) * sizeof(uint32_t), P->s_main));
+    uint8_t* need = static_cast<uint8_t*>(t_need.p);
     IFGF_CUDA(cudaMemsetAsync(need, 0, L.nc + 1, P->s_main));
     // this level's cone boundaries on the device (ownership test)
-    uint32_t* d_cb = P->alloc<uint32_t>(R + 1);
+    uint32_t* d_cb = static_cast<uint32_t*>(t_cb.p);
     IFGF_CUDA(cudaMemcpyAsync(d_cb, cb.data() + (size_t)(d - 3) * (R + 1), (R + 1) * 4,
                               cudaMemcpyHostToDevice, P->s_main));
-    if (kind == 0) {
-      const uint32_t p0 = pb[rank], p1 = pb[rank + 1];
-      if (p1 > p0)
-        k_need_interp<<<(p1 - p0 + 127) / 128, 128, 0, P->s_main>>>(
-            L.dev(), L.ptbox, P->xs, P->ys, P->zs, p0, p1, d_cb, R, rank, need, P->err);
-    } else {
-      const uint32_t* own = cb.data() + (size_t)(d - 4) * (R + 1);
-      const uint32_t q0 = own[rank], q1 = own[rank + 1];
-      const size_t work = (size_t)(q1 - q0) * P->K.P;
-      if (work)
-        k_need_prop<<<(unsigned)((work + 127) / 128), 128, 0, P->s_main>>>(
-            L.dev(), P->lv[d - 1].dev(), P->K, q0, q1, d_cb, R, rank, need, P->err);
-    }
+    if (kind == 0)
+      launch_need(P, d, 0, d_cb, R, rank, pb[rank], pb[rank + 1], need, P->s_main);
+    else
+      launch_need(P, d, 1, d_cb, R, rank, cb[(size_t)(d - 4) * (R + 1) + rank],
+                  cb[(size_t)(d - 4) * (R + 1) + rank + 1], need, P->s_main);
     IFGF_CUDA(cudaGetLastError());
     check_device_error(P);
     const auto h = d2h(need, L.nc, P->s_main);
@@ -994,9 +1017,122 @@ int ifgf_plan_exchange_set(ifgf_plan* P, int R, int rank, int d, int kind, uint3
   });
 }
 
+
+// ---- multi-GPU (dist.cu) ----
+int ifgf_comm_unique_id(void* id_out) {
+  return guarded([&] {
+    if (!id_out) throw Error(IFGF_EINVAL, "null id buffer");
+    comm_unique_id(id_out);
+  });
+}
+
+int ifgf_comm_create(const void* id, int rank, int world, int device, ifgf_comm** out) {
+  DeviceGuard keep;
+  return guarded([&] {
+    if (!out) throw Error(IFGF_EINVAL, "null output");
+    *out = nullptr;
+    require_device(device);
+    *out = comm_create(id, rank, world, device);
+  });
+}
+
+void ifgf_comm_destroy(ifgf_comm* comm) {
+  DeviceGuard keep;
+  comm_destroy(comm);
+}
+
+int ifgf_dist_plan_create_device(ifgf_comm* comm, const double* dx, const double* dy,
+                                 const double* dz, size_t n, int kind, double k,
+                                 const ifgf_params* p, void* stream, ifgf_plan** out) {
+  DeviceGuard keep;
+  return guarded([&] {
+    if (!out || !comm) throw Error(IFGF_EINVAL, "null argument");
+    *out = nullptr;
+    if (!p) throw Error(IFGF_EINVAL, "null params");
+    ifgf_params q = *p;
+    q.device = comm->device;
+    ifgf_plan* P = new_plan(n, kind, k, &q);
+    try {
+      cudaEvent_t e;
+      IFGF_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+      IFGF_CUDA(cudaEventRecord(e, static_cast<cudaStream_t>(stream)));
+      IFGF_CUDA(cudaStreamWaitEvent(P->s_main, e, 0));
+      cudaEventDestroy(e);
+      const auto t0 = clk::now();
+      finish_create(P, dx, dy, dz);
+      dist_prepare(P, comm->world, comm->rank);
+      comm_attach(P, comm);
+      dist_connect(P);
+      P->setup_seconds = since(t0);
+    } catch (...) {
+      plan_free(P);
+      throw;
+    }
+    *out = P;
+  });
+}
+
+int ifgf_dist_plan_apply_device(ifgf_plan* P, const double* a_re, const double* a_im,
+                                double* i_re, double* i_im, void* stream, ifgf_report* rep) {
+  DeviceGuard keep;
+  return guarded([&] {
+    if (!P || !a_re || !i_re || !i_im) throw Error(IFGF_EINVAL, "null argument");
+    if (P->n < 2) throw Error(IFGF_EINVAL, "apply: need at least two points");
+    dist_apply_device(P, a_re, a_im, i_re, i_im, static_cast<cudaStream_t>(stream), rep);
+  });
+}
+
+int ifgf_dist_plan_info(const ifgf_plan* P, ifgf_dist_info* info) {
+  return guarded([&] {
+    if (!P || !info) throw Error(IFGF_EINVAL, "null argument");
+    dist_fill_info(P, info);
+  });
+}
+
+int ifgf_run_distributed(size_t n, const double* x1, const double* x2, const double* x3,
+                         const double* a_re, const double* a_im, int kind, double k,
+                         const ifgf_params* p, int R, const int* devices, double* i_re,
+                         double* i_im, ifgf_report* rep, ifgf_dist_info* info) {
+  DeviceGuard keep;
+  return guarded([&] {
+    // dist.cpp:241-243
+    if (n < 2) throw Error(IFGF_EINVAL, "run_distributed: need two points");
+    if (R < 1) throw Error(IFGF_EINVAL, "run_distributed: need at least one rank");
+    if (!x1 || !x2 || !x3 || !a_re || !i_re || !i_im || !p)
+      throw Error(IFGF_EINVAL, "null argument");
+    std::vector<ifgf_plan*> G;
+    struct Free {
+      std::vector<ifgf_plan*>& g;
+      ~Free() {
+        for (auto* P : g) plan_free(P);
+      }
+    } fr{G};
+    const auto t0 = clk::now();
+    for (int r = 0; r < R; ++r) {
+      ifgf_params q = *p;
+      q.device = devices ? devices[r] : p->device;
+      ifgf_plan* P = nullptr;
+      const int rc = ifgf_plan_create(x1, x2, x3, n, kind, k, &q, &P);
+      if (rc) throw Error(rc, g_err);
+      G.push_back(P);
+      dist_prepare(P, R, r);
+    }
+    dist_connect_local(G);
+    const double setup = since(t0);
+    run_local_group(G, a_re, a_im, i_re, i_im, rep);
+    if (rep) {
+      rep->setup = setup;
+      rep->total += setup;
+    }
+    if (info)
+      for (int r = 0; r < R; ++r) dist_fill_info(G[r], &info[r]);
+  });
+}
+
 int ifgf_direct_eval(size_t n, const double* x1, const double* x2, const double* x3,
                      const double* a_re, const double* a_im, int kind, double k,
                      const uint32_t* targets, size_t m, int device, double* o_re, double* o_im) {
+  DeviceGuard keep;
   return guarded([&] {
     if (n < 2) throw Error(IFGF_EINVAL, "direct_eval: need at least two points");
     require_device(device);

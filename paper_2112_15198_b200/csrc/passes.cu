@@ -543,11 +543,17 @@ __global__ void k_scatter_result(const uint32_t* __restrict__ perm, const double
 }
 
 __global__ void k_pack(const double2* __restrict__ blocks, const uint32_t* __restrict__ cones,
-                       size_t m, int Pst, double2* buf, int unpack, double2* blocks_out) {
+                       size_t m, int Pst, uint32_t nc, double2* buf, int unpack,
+                       double2* blocks_out, int* err) {
   const size_t t = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
   if (t >= m * Pst) return;
   const size_t j = t / Pst, k = t % Pst;
-  const size_t g = (size_t)cones[j] * Pst + k;
+  const uint32_t q = cones[j];
+  if (q >= nc) {  // caller-supplied ordinal out of range: invalid_argument
+    if (k == 0) raise_err(err, kErrBadCone);
+    return;
+  }
+  const size_t g = (size_t)q * Pst + k;
   if (unpack) blocks_out[g] = buf[t];
   else buf[t] = blocks[g];
 }
@@ -689,12 +695,12 @@ void launch_interpolation(ifgf_plan* P, int d, size_t b, size_t e, const double2
 }
 
 void launch_pack(ifgf_plan* P, const double2* blocks, const uint32_t* cones, size_t m,
-                 double* buf, int unpack, double2* blocks_out, cudaStream_t s) {
+                 uint32_t nc, double* buf, int unpack, double2* blocks_out, cudaStream_t s) {
   if (!m) return;
   const int Pn = P->K.Pst;
-  k_pack<<<blocks_for(m * Pn, 256), 256, 0, s>>>(blocks, cones, m, Pn,
+  k_pack<<<blocks_for(m * Pn, 256), 256, 0, s>>>(blocks, cones, m, Pn, nc,
                                                  reinterpret_cast<double2*>(buf), unpack,
-                                                 blocks_out);
+                                                 blocks_out, P->err);
   ++P->launches;
 }
 

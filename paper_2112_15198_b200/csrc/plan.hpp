@@ -12,7 +12,16 @@
 #include "../../include/ifgf_b200.h"
 #include "ifgf_common.cuh"
 
+// A multi-process rank group's handle (dist.cu): this process's rank and its
+// NCCL communicator (ncclComm_t, opaque here).
+struct ifgf_comm {
+  int rank = 0, world = 1, device = 0;
+  void* nccl = nullptr;
+};
+
 namespace ifgf_b200 {
+
+struct DistState;  // dist.cu: a rank's share of a multi-GPU plan
 
 // C++ exception carrying one of the IFGF_E* codes; caught at the C ABI.
 struct Error : std::runtime_error {
@@ -169,6 +178,7 @@ struct ifgf_plan {
   double *xs = nullptr, *ys = nullptr, *zs = nullptr;  // Morton-sorted coordinates
   double *ar = nullptr, *ai = nullptr;                 // sorted densities
   double *ir = nullptr, *ii = nullptr;                 // sorted results
+  double* staging = nullptr;  // 2n doubles: pass-level API host<->device staging, reused
   int* err = nullptr;
   const double2* phase = nullptr;  // sincos_tab table (kPhaseEntries), after the trig table
   uint32_t* work_ctr = nullptr;    // persistent-kernel work counters (kWorkCtrs)
@@ -188,6 +198,7 @@ struct ifgf_plan {
   int near_kernel = IFGF_NEAR_BOX;   // IFGF_OPT_NEAR_KERNEL
   int partition_mode = IFGF_PARTITION_COUNT;  // IFGF_OPT_PARTITION
   size_t setup_launches = 0;
+  ifgf_b200::DistState* dist = nullptr;  // rank plans of a multi-GPU group (dist.cu)
 
   template <class T>
   T* alloc(size_t count) {
@@ -215,13 +226,32 @@ void launch_propagation(ifgf_plan* P, int d, uint32_t qb, uint32_t qe, const dou
 void launch_interpolation(ifgf_plan* P, int d, size_t b, size_t e, const double2* blocks,
                           cudaStream_t s);
 void launch_pack(ifgf_plan* P, const double2* blocks, const uint32_t* cones, size_t m,
-                 double* buf, int unpack, double2* blocks_out, cudaStream_t s);
+                 uint32_t nc, double* buf, int unpack, double2* blocks_out, cudaStream_t s);
 bool orders_supported(int ps, int pt, int pp);
 // propagate_mma.cu
 void build_prop_tiles(ifgf_plan* P, int d, void* (*scratch)(void*, size_t), void* sctx);
 void launch_mark_nodes_tiles(ifgf_plan* P, int d, uint64_t* bits);
 bool launch_propagation_mma(ifgf_plan* P, int d, uint32_t qb, uint32_t qe, const double2* child,
                             double2* parent, cudaStream_t s);
+// capi.cu
+void partition_host(ifgf_plan* P, int R, uint32_t* box_begin, uint32_t* point_begin,
+                    uint32_t* cone_begin);
+// dist.cu
+void launch_need(ifgf_plan* P, int d, int kind, const uint32_t* d_bounds, int R, int rank,
+                 uint32_t lo, uint32_t hi, uint8_t* need, cudaStream_t s);
+void dist_prepare(ifgf_plan* P, int R, int rank);
+void dist_connect(ifgf_plan* P);
+void dist_connect_local(std::vector<ifgf_plan*>& G);
+void dist_apply_device(ifgf_plan* P, const double* a_re, const double* a_im, double* i_re,
+                       double* i_im, cudaStream_t caller, ifgf_report* rep);
+void run_local_group(std::vector<ifgf_plan*>& G, const double* a_re, const double* a_im,
+                     double* i_re, double* i_im, ifgf_report* rep);
+void dist_fill_info(const ifgf_plan* P, ifgf_dist_info* info);
+void dist_free(ifgf_plan* P);
+ifgf_comm* comm_create(const void* id, int rank, int world, int device);
+void comm_unique_id(void* out);
+void comm_destroy(ifgf_comm* C);
+void comm_attach(ifgf_plan* P, ifgf_comm* C);
 // direct.cu
 void direct_sums(const double* x, const double* y, const double* z, const double* ar,
                  const double* ai, size_t n, double kappa, const uint32_t* targets, size_t m,

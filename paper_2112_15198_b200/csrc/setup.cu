@@ -422,6 +422,8 @@ void check_device_error(ifgf_plan* P) {
       throw Error(IFGF_EDOMAIN, "point outside bounding cube");
     case kErrNonFinite:
       throw Error(IFGF_EINVAL, "cheb_fit: non-finite node value");
+    case kErrBadCone:
+      throw Error(IFGF_EINVAL, "block exchange: cone ordinal out of range");
     default:
       throw Error(IFGF_ERUNTIME, "unknown device error " + std::to_string(e));
   }

@@ -1,25 +1,21 @@
 """Multi-GPU IFGF matvec: the reference's rank algorithm (dist.cpp:241-361,
-the paper's "IFGF Method" in MPI form) with real exchanges.
+the paper's "IFGF Method" in MPI form) on the C++ engine of libifgf_b200.so
+(csrc/dist.cu, include/ifgf_b200.h "multi-GPU").
 
 * Layout (dist.cpp:78-130): points in contiguous Morton intervals of level-D
   boxes balanced by population; each level's cones in equal-count intervals
   of the (box, gamma) order -- boxes at fine levels, cone segments at coarse
-  levels.  Every rank builds the same plan (setup is cheap on the GPU), so
-  every rank can compute every other rank's needs locally.
-* Exchange sets (dist.cpp:179-237): per level d, the deduplicated foreign
-  cones a rank needs for interpolation (its points' cousin cones) and for
-  propagation (child cones hit by its parent cones' nodes), computed on the
-  device by ifgf_plan_exchange_set.
-* Transport: blocks are packed on the device (ifgf_plan_pack_blocks), moved
-  with torch.distributed batched P2P (NCCL over NVLink on B200; gloo in the
-  CPU tests) and unpacked into the receiving rank's level storage at their
-  global cone ordinal -- the analogue of Window::get (dist.cpp:154-173).
+  levels.  The structure is built on every rank; the interpolant blocks are
+  partitioned: a rank stores its owned cones plus its halo (the foreign cones
+  its points and parent cones read, dist.cpp:179-237).
+* Transport: per level, the owners pack the requested blocks on the device
+  and one NCCL group of send/recv moves them (one process per GPU,
+  Comm/DistPlan); in-process rank groups (run_distributed, the analogue of
+  dist::run_distributed) move them with device copies.
 
-Phase order follows dist.cpp:273-342: near field and level-D seeding on owned
-work, then per level: interpolation data in; propagation of owned parent
-cones (after the propagation data of that level arrived); interpolation of
-owned points.  Each kernel computes its work items independently, so the
-distributed result is bitwise equal to the single-GPU apply (tested).
+This module is the host-side mirror: ctypes wrappers over the C ABI, plus the
+rank layout and exchange lists as host data (Layout, build_exchange_plan)
+that the CLI's CommStats and the CPU tests use.
 """
 from __future__ import annotations
 
@@ -85,117 +81,6 @@ def build_exchange_plan(layout: Layout, depth: int, need) -> ExchangePlan:
     return ex
 
 
-def build_exchange_plan_rank(layout: Layout, depth: int, rank: int, need_self, group=None,
-                             device=None) -> ExchangePlan:
-    """This rank's rows of the exchange plan without computing anyone else's
-    needs: the rank computes its own foreign-cone sets (need_self(d, kind)),
-    tells every owner which of its cones it needs (one all-to-all of counts and
-    one of indices per level and kind) and learns what it must send.  Only
-    row `rank` of recv/send is filled."""
-    import torch
-    import torch.distributed as dist
-    R = layout.n_ranks
-    dev = device if device is not None else torch.device("cpu")
-    ex = ExchangePlan(depth, R)
-    empty = np.zeros(0, np.uint32)
-    for d in range(3, depth + 1):
-        for kind in (INTERP, PROP):
-            if kind == PROP and d < 4:
-                continue
-            cones = np.asarray(need_self(d, kind), dtype=np.uint32)
-            owner = layout.cone_owner(d, cones) if len(cones) else np.zeros(0, np.int64)
-            mine = [cones[owner == p] for p in range(R)]
-            if len(mine[rank]):
-                raise AssertionError("a rank never fetches its own cones")
-            cnt = torch.tensor([len(a) for a in mine], dtype=torch.int64, device=dev)
-            cnt_in = torch.empty_like(cnt)
-            dist.all_to_all_single(cnt_in, cnt, group=group)
-            sizes_out, sizes_in = cnt.tolist(), cnt_in.tolist()
-            flat = torch.as_tensor(np.concatenate(mine).astype(np.int64) if len(cones) else
-                                   np.zeros(0, np.int64), device=dev)
-            got = torch.empty(sum(sizes_in), dtype=torch.int64, device=dev)
-            dist.all_to_all_single(got, flat, sizes_in, sizes_out, group=group)
-            got = got.cpu().numpy().astype(np.uint32)
-            off = np.concatenate([[0], np.cumsum(sizes_in)])
-            recv = [[empty] * R for _ in range(R)]
-            send = [[empty] * R for _ in range(R)]
-            recv[rank] = mine
-            send[rank] = [got[off[p]:off[p + 1]] for p in range(R)]
-            ex.recv[(d, kind)] = recv
-            ex.send[(d, kind)] = send
-    return ex
-
-
-class TorchExchanger:
-    """Moves blocks between ranks with torch.distributed batched P2P.
-
-    `store` provides block_doubles (2 * Pst), pack(d, idx_tensor, buf) and
-    unpack(d, idx_tensor, buf) over tensors on `device`.  With a backend that
-    moves host tensors only (gloo) the packed buffers are staged through host
-    memory (`wire` = cpu); with NCCL they travel device to device."""
-
-    def __init__(self, store, ex: ExchangePlan, rank: int, device, group=None, wire=None):
-        import torch
-        self.torch = torch
-        self.store, self.ex, self.rank, self.device, self.group = store, ex, rank, device, group
-        self.wire = wire if wire is not None else device
-        self._idx = {}
-        for key in ex.recv:
-            for p in range(ex.n_ranks):
-                for role, lists in (("send", ex.send[key][rank]), ("recv", ex.recv[key][rank])):
-                    a = lists[p]
-                    if len(a):
-                        self._idx[(key, role, p)] = torch.as_tensor(a.astype(np.int32),
-                                                                    device=device)
-
-    def exchange(self, d, kind):
-        torch = self.torch
-        import torch.distributed as dist
-        key = (d, kind)
-        if key not in self.ex.recv:
-            return 0
-        bd = self.store.block_doubles
-        ops, recv_bufs = [], []
-        for p in range(self.ex.n_ranks):
-            if p == self.rank:
-                continue
-            si = self._idx.get((key, "send", p))
-            if si is not None:
-                buf = torch.empty(len(si) * bd, dtype=torch.float64, device=self.device)
-                self.store.pack(d, si, buf)
-                if self.wire != self.device:
-                    torch.cuda.synchronize()
-                    buf = buf.to(self.wire)
-                ops.append(dist.P2POp(dist.isend, buf, p, group=self.group))
-            ri = self._idx.get((key, "recv", p))
-            if ri is not None:
-                buf = torch.empty(len(ri) * bd, dtype=torch.float64, device=self.wire)
-                recv_bufs.append((ri, buf))
-                ops.append(dist.P2POp(dist.irecv, buf, p, group=self.group))
-        if ops:
-            for w in dist.batch_isend_irecv(ops):
-                w.wait()
-        moved = 0
-        for ri, buf in recv_bufs:
-            self.store.unpack(d, ri, buf.to(self.device))
-            moved += len(ri)
-        return moved
-
-
-class PlanStore:
-    """Block store over an ifgf Plan's level storage (device pointers)."""
-
-    def __init__(self, plan, stream=0):
-        from . import _lib
-        self.plan = plan
-        self.block_doubles = 2 * int(_lib.lib.ifgf_plan_block_stride(plan._h))
-        self.stream = stream
-
-    def pack(self, d, idx, buf):
-        self.plan.pack_blocks(d, idx.data_ptr(), idx.numel(), buf.data_ptr(), self.stream)
-
-    def unpack(self, d, idx, buf):
-        self.plan.unpack_blocks(d, idx.data_ptr(), idx.numel(), buf.data_ptr(), self.stream)
 
 
 def rank_layout(plan, n_ranks) -> Layout:
@@ -203,168 +88,148 @@ def rank_layout(plan, n_ranks) -> Layout:
     return Layout(n_ranks, bb, pb, cb)
 
 
-def run_rank_share(plan, layout: Layout, rank: int, a_re, a_im, exchange):
-    """This rank's part of the distributed apply, in the reference's phase
-    order (dist.cpp:273-342).  `exchange(d, kind)` moves the blocks of that
-    level/kind in (and out).  Returns (i_re, i_im) of the rank's sorted point
-    interval."""
-    D = plan.depth
-    pb, pe = layout.points(rank)
-    plan.set_density(a_re, a_im)
-    plan.zero_result()
-    plan.singular_pass(pb, pe)
-    qb, qe = layout.cones(D, rank)
-    plan.level_d_pass(qb, qe)
-    if D > 3:
-        exchange(D, PROP)
-    for d in range(D, 2, -1):
-        exchange(d, INTERP)
-        if d > 3:
-            qb, qe = layout.cones(d - 1, rank)
-            plan.propagation_pass(d, qb, qe)
-            if d > 4:
-                exchange(d - 1, PROP)
-        plan.interpolation_pass(d, pb, pe)
-    i_re, i_im = plan.read_result(sorted_order=True)
-    return i_re[pb:pe], i_im[pb:pe]
+# ---------------------------------------------------------------- C ABI mirror
+def _engine():
+    from . import _lib, engine
+    return _lib, engine
 
 
-class DistributedPlan:
-    """One plan per rank (this process's GPU); apply() returns the full
-    result in the caller's order on every rank.  Every rank builds the same
-    plan (setup is cheap on the GPU); each rank computes only its own
-    exchange sets and learns its send sets with one all-to-all per level and
-    kind (build_exchange_plan_rank)."""
+@dataclass
+class RankInfo:
+    """ifgf_dist_info: one rank's share of a multi-GPU plan."""
+    rank: int
+    world: int
+    point_begin: int
+    point_end: int
+    levels: list  # per d = 3..D: dict(owned_cones, halo_cones, interp_needed, prop_needed, sent_cones)
+    block_bytes: int
+    device_bytes: int
 
-    def __init__(self, x1, x2, x3, cfg, params=None, group=None, partition: int = 0):
-        import torch
-        import torch.distributed as dist
+    @classmethod
+    def from_c(cls, c, depth):
+        lv = [{f: int(getattr(c.levels[d - 3], f)) for f in
+               ("owned_cones", "halo_cones", "interp_needed", "prop_needed", "sent_cones")}
+              | {"d": d} for d in range(3, depth + 1)]
+        return cls(c.rank, c.world, int(c.point_begin), int(c.point_end), lv,
+                   int(c.block_bytes), int(c.device_bytes))
 
-        from .engine import EngineParams, Plan
-        self.torch, self.dist, self.group = torch, dist, group
-        self.rank = dist.get_rank(group)
-        self.world = dist.get_world_size(group)
-        self.device = torch.device("cuda", torch.cuda.current_device())
-        # NCCL moves device tensors; gloo (CPU tests, shared-GPU checks) host ones
-        self.wire = self.device if dist.get_backend(group) == "nccl" else torch.device("cpu")
-        p = params or EngineParams()
-        p.device = torch.cuda.current_device()
-        self.plan = Plan(x1, x2, x3, cfg, p)
-        self.plan.set_partition(partition)
-        self.layout = rank_layout(self.plan, self.world)
-        self.ex = build_exchange_plan_rank(
-            self.layout, self.plan.depth, self.rank,
-            lambda d, kind: self.plan.exchange_set(self.world, self.rank, d, kind),
-            group=group, device=self.wire)
-        self.store = PlanStore(self.plan)
-        self.xch = TorchExchanger(self.store, self.ex, self.rank, self.device, group,
-                                  wire=self.wire)
-        self.perm = self.plan.perm()
 
-    def apply(self, a_re, a_im=None):
-        torch = self.torch
-        a_im = np.zeros_like(a_re) if a_im is None else a_im
-        part = run_rank_share(self.plan, self.layout, self.rank, a_re, a_im, self.xch.exchange)
-        n = self.plan.n
-        m = int(np.max(np.diff(self.layout.point_begin)))
-        mine = torch.zeros((2, m), dtype=torch.float64, device=self.wire)
-        mine[0, :len(part[0])] = torch.as_tensor(part[0], device=self.wire)
-        mine[1, :len(part[1])] = torch.as_tensor(part[1], device=self.wire)
-        pieces = [torch.empty_like(mine) for _ in range(self.world)]
-        self.dist.all_gather(pieces, mine, group=self.group)
-        s_re, s_im = np.zeros(n), np.zeros(n)
-        for r in range(self.world):
-            b, e = self.layout.points(r)
-            pr = pieces[r].cpu().numpy()
-            s_re[b:e] = pr[0, :e - b]
-            s_im[b:e] = pr[1, :e - b]
-        i_re, i_im = np.zeros(n), np.zeros(n)
-        i_re[self.perm] = s_re
-        i_im[self.perm] = s_im
-        return i_re, i_im
+def run_distributed(pc, cfg, p=None, n_ranks: int = 2, devices=None):
+    """dist::run_distributed (dist.hpp:90) on the GPU: n_ranks rank plans in
+    this process (devices[r], default all on p.device), blocks exchanged
+    rank to rank.  Fills pc.i_re / pc.i_im (caller's order, bitwise equal to
+    apply()) and returns (ApplyReport, [RankInfo])."""
+    import ctypes as C
+    _lib, engine = _engine()
+    p = p or engine.EngineParams()
+    devs = None
+    if devices is not None:
+        devs = (C.c_int * n_ranks)(*[int(v) for v in devices])
+    rep = _lib.CReport()
+    infos = (_lib.CDistInfo * n_ranks)()
+    a_im = pc.a_im
+    engine.check(_lib.lib.ifgf_run_distributed(
+        pc.size(), _lib.ptr(pc.x1), _lib.ptr(pc.x2), _lib.ptr(pc.x3), _lib.ptr(pc.a_re),
+        _lib.ptr(a_im), int(cfg.kind), float(cfg.wavenumber), C.byref(p.c()), n_ranks, devs,
+        _lib.ptr(pc.i_re), _lib.ptr(pc.i_im), C.byref(rep), C.cast(infos, C.c_void_p)))
+    r = engine.ApplyReport.from_c(rep)
+    return r, [RankInfo.from_c(infos[k], r.depth) for k in range(n_ranks)]
+
+
+class Comm:
+    """A rank's handle of a multi-process group (ifgf_comm): one process per
+    GPU, NCCL over NVLink/NVSwitch.  Rank 0 makes the id (unique_id()), the
+    launcher broadcasts it (share_comm_id below), every rank constructs."""
+
+    def __init__(self, comm_id: bytes, rank: int, world: int, device: int):
+        import ctypes as C
+        _lib, engine = _engine()
+        self._lib = _lib
+        self.rank, self.world, self.device = rank, world, device
+        buf = C.create_string_buffer(bytes(comm_id), _lib.COMM_ID_BYTES)
+        h = C.c_void_p()
+        engine.check(_lib.lib.ifgf_comm_create(buf, rank, world, device, C.byref(h)))
+        self._h = h
+
+    @staticmethod
+    def unique_id() -> bytes:
+        import ctypes as C
+        _lib, engine = _engine()
+        buf = C.create_string_buffer(_lib.COMM_ID_BYTES)
+        engine.check(_lib.lib.ifgf_comm_unique_id(buf))
+        return buf.raw
 
     def close(self):
-        self.plan.close()
+        if getattr(self, "_h", None):
+            self._lib.lib.ifgf_comm_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        self.close()
 
 
-def simulate(plans, a_re, a_im, partition: int = 0, rank_seconds=None):
-    """R ranks in one process (one plan each, all on the same GPU), blocks
-    moved plan to plan through pack/unpack -- the reference's in-process rank
-    simulation (dist.cpp) on real kernels.  Ranks advance phase by phase, so
-    no kernel ever waits on another rank's kernel.  Returns the full result
-    in the caller's order and the number of blocks moved.  `partition`:
-    Plan.PARTITION_COUNT (the reference's layout) or Plan.PARTITION_WORK.
-    `rank_seconds` (a list): filled with each rank's compute time (its passes,
-    synchronised one by one -- exchanges excluded), the load-balance measure."""
+class DistPlan:
+    """One rank's plan of a multi-process group (collective create / apply)."""
+
+    def __init__(self, comm: Comm, x1_ptr: int, x2_ptr: int, x3_ptr: int, n: int, cfg, p=None,
+                 stream: int = 0):
+        import ctypes as C
+        _lib, engine = _engine()
+        self._lib, self._engine = _lib, engine
+        p = p or engine.EngineParams()
+        h = C.c_void_p()
+        engine.check(_lib.lib.ifgf_dist_plan_create_device(
+            comm._h, C.c_void_p(x1_ptr), C.c_void_p(x2_ptr), C.c_void_p(x3_ptr), n,
+            int(cfg.kind), float(cfg.wavenumber), C.byref(p.c()), C.c_void_p(stream),
+            C.byref(h)))
+        self._h = h
+        self.n = n
+        self.comm = comm
+
+    def apply_device(self, a_re_ptr: int, a_im_ptr, i_re_ptr: int, i_im_ptr: int,
+                     stream: int = 0):
+        import ctypes as C
+        rep = self._lib.CReport()
+        self._engine.check(self._lib.lib.ifgf_dist_plan_apply_device(
+            self._h, C.c_void_p(a_re_ptr), C.c_void_p(a_im_ptr) if a_im_ptr else None,
+            C.c_void_p(i_re_ptr), C.c_void_p(i_im_ptr), C.c_void_p(stream), C.byref(rep)))
+        return self._engine.ApplyReport.from_c(rep)
+
+    def info(self) -> RankInfo:
+        import ctypes as C
+        c = self._lib.CDistInfo()
+        self._engine.check(self._lib.lib.ifgf_dist_plan_info(self._h, C.byref(c)))
+        return RankInfo.from_c(c, c.depth)
+
+    def plan_info(self):
+        import ctypes as C
+        c = self._lib.CPlanInfo()
+        self._engine.check(self._lib.lib.ifgf_plan_get_info(self._h, C.byref(c)))
+        return c
+
+    def close(self):
+        if getattr(self, "_h", None):
+            self._lib.lib.ifgf_plan_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        self.close()
+
+
+def share_comm_id(make_id, group=None) -> bytes:
+    """The launcher side of Comm: rank 0 calls make_id() (Comm.unique_id),
+    every rank of the torch.distributed group receives the same bytes."""
+    import torch.distributed as dist
+    obj = [make_id() if dist.get_rank(group) == 0 else None]
+    dist.broadcast_object_list(obj, src=0, group=group)
+    return obj[0]
+
+
+def max_over_ranks(value: float, group=None, device=None) -> float:
+    """The slowest rank's time (bench timing rule: max over ranks)."""
     import torch
-
-    R = len(plans)
-    for p in plans:
-        p.set_partition(partition)
-    layout = rank_layout(plans[0], R)
-    ex = build_exchange_plan(layout, plans[0].depth,
-                             lambda r, d, kind: plans[0].exchange_set(R, r, d, kind))
-    stores = [PlanStore(p) for p in plans]
-    bd = stores[0].block_doubles
-    dev = torch.device("cuda", torch.cuda.current_device())
-    moved = [0]
-
-    def exchange_all(d, kind):
-        key = (d, kind)
-        if key not in ex.recv:
-            return
-        for r in range(R):
-            for p in range(R):
-                a = ex.recv[key][r][p]
-                if not len(a):
-                    continue
-                idx = torch.as_tensor(a.astype(np.int32), device=dev)
-                buf = torch.empty(len(a) * bd, dtype=torch.float64, device=dev)
-                stores[p].pack(d, idx, buf)
-                torch.cuda.synchronize()
-                stores[r].unpack(d, idx, buf)
-                torch.cuda.synchronize()
-                moved[0] += len(a)
-
-    secs = [0.0] * R
-
-    def run(r, fn, *args):
-        if rank_seconds is None:
-            return fn(*args)
-        import time
-        torch.cuda.synchronize()
-        t0 = time.perf_counter()
-        fn(*args)
-        torch.cuda.synchronize()
-        secs[r] += time.perf_counter() - t0
-
-    D = plans[0].depth
-    for r in range(R):
-        pb, pe = layout.points(r)
-        plans[r].set_density(a_re, a_im)
-        plans[r].zero_result()
-        run(r, plans[r].singular_pass, pb, pe)
-        run(r, plans[r].level_d_pass, *layout.cones(D, r))
-    if D > 3:
-        exchange_all(D, PROP)
-    for d in range(D, 2, -1):
-        exchange_all(d, INTERP)
-        if d > 3:
-            for r in range(R):
-                run(r, plans[r].propagation_pass, d, *layout.cones(d - 1, r))
-            if d > 4:
-                exchange_all(d - 1, PROP)
-        for r in range(R):
-            run(r, plans[r].interpolation_pass, d, *layout.points(r))
-    if rank_seconds is not None:
-        rank_seconds[:] = secs
-    n = plans[0].n
-    s_re, s_im = np.zeros(n), np.zeros(n)
-    for r in range(R):
-        b, e = layout.points(r)
-        g_re, g_im = plans[r].read_result(sorted_order=True)
-        s_re[b:e], s_im[b:e] = g_re[b:e], g_im[b:e]
-    perm = plans[0].perm()
-    i_re, i_im = np.zeros(n), np.zeros(n)
-    i_re[perm], i_im[perm] = s_re, s_im
-    return i_re, i_im, moved[0], ex
+    import torch.distributed as dist
+    t = torch.tensor([float(value)], dtype=torch.float64,
+                     device=device if device is not None else "cpu")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX, group=group)
+    return float(t.item())

@@ -103,12 +103,13 @@ class EngineParams:
     orders: InterpOrders = field(default_factory=InterpOrders)
     threads: int = 1  # accepted for API parity; the GPU ignores it
     device: int = 0
+    partition: int = 0  # rank layout of multi-GPU plans (Plan.PARTITION_COUNT / _WORK)
 
     def c(self) -> _lib.CParams:
         o = self.orders
         return _lib.CParams(self.depth, self.box_lambda, self.points_per_box, self.base_s,
                             self.base_theta, self.base_phi, o.p_s, o.p_theta, o.p_phi,
-                            self.device)
+                            self.device, self.partition)
 
 
 @dataclass

@@ -1,7 +1,8 @@
-"""Multi-rank host logic of paper_2112_15198_b200.dist on the CPU: rank
-layout and exchange lists against the oracle / reference (dist.cpp:78-237),
-and the block exchange protocol over a real torch.distributed gloo group of
-world size 2 (the NCCL path on B200 runs the same code)."""
+"""Multi-rank host logic on the CPU: rank layout and exchange lists against
+the oracle / reference (dist.cpp:78-237), the halo / send-list pairing the
+C++ engine (csrc/dist.cu) relies on, and the launcher side of the
+multi-process path (communicator id broadcast, max-over-ranks timing) over a
+real torch.distributed gloo group of world size 2."""
 import math
 import os
 import socket
@@ -66,116 +67,65 @@ def _free_port():
     return p
 
 
-class FakeStore:
-    """Level block storage on the CPU: owned cones hold f(d, q, k), the rest NaN."""
-
-    def __init__(self, torch, ncones, depth, lay, rank, bd=8):
-        self.torch, self.block_doubles = torch, bd
-        self.lv = {}
-        for d in range(3, depth + 1):
-            t = torch.full((ncones[d], bd), float("nan"), dtype=torch.float64)
-            qb, qe = lay.cones(d, rank)
-            q = torch.arange(qb, qe, dtype=torch.float64)[:, None]
-            t[qb:qe] = d * 1e7 + q * 16 + torch.arange(bd, dtype=torch.float64)[None, :]
-            self.lv[d] = t
-
-    def pack(self, d, idx, buf):
-        buf.copy_(self.lv[d].index_select(0, idx.long()).reshape(-1))
-
-    def unpack(self, d, idx, buf):
-        self.lv[d].index_copy_(0, idx.long(), buf.reshape(len(idx), -1))
-
-
-def _worker(rank, world, port, depth, ncones, lay, ex, out):
-    import torch
+def _boot_worker(rank, world, port, out):
     import torch.distributed as dist
 
-    from paper_2112_15198_b200.dist import INTERP, PROP, TorchExchanger
+    from paper_2112_15198_b200.dist import max_over_ranks, share_comm_id
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
-    store = FakeStore(torch, ncones, depth, lay, rank)
-    x = TorchExchanger(store, ex, rank, torch.device("cpu"))
-    moved = 0
-    # the reference's phase order (dist.cpp:292-327)
-    if depth > 3:
-        moved += x.exchange(depth, PROP)
-    for d in range(depth, 2, -1):
-        moved += x.exchange(d, INTERP)
-        if d > 4:
-            moved += x.exchange(d - 1, PROP)
-    ok = True
-    for d in range(3, depth + 1):
-        need = set()
-        for kind in (INTERP, PROP):
-            if (d, kind) in ex.recv:
-                for p in range(world):
-                    need.update(int(q) for q in ex.recv[(d, kind)][rank][p])
-        t = store.lv[d]
-        for q in need:
-            want = d * 1e7 + q * 16 + np.arange(store.block_doubles)
-            ok &= bool(np.array_equal(t[q].numpy(), want))
-        qb, qe = lay.cones(d, rank)
-        valid = set(np.nonzero(~np.isnan(t[:, 0].numpy()))[0].tolist())
-        ok &= valid == set(range(qb, qe)) | need  # nothing else arrived
-    out.put((rank, ok, moved))
+    # rank 0's id (a stand-in for ifgf_comm_unique_id's 128 NCCL bytes)
+    made = []
+
+    def make():
+        made.append(1)
+        return bytes(range(128))
+
+    cid = share_comm_id(make)
+    slowest = max_over_ranks(0.5 + rank)
+    out.put((rank, cid, len(made), slowest))
     dist.destroy_process_group()
 
 
-def test_block_exchange_over_gloo_world2(oracle):
+def test_rank_bootstrap_over_gloo_world2():
+    """The launcher side of the multi-GPU path (bench.py --gpus N): rank 0
+    alone makes the communicator id and every rank receives the same bytes;
+    step times reduce to the slowest rank's."""
     import torch.multiprocessing as mp
-    prob = _problem(oracle, n=5000, seed=43)
-    lay, ex = _layout_and_plan(prob, 2)
-    ncones = {d: prob.n_cones(d) for d in range(3, prob.depth + 1)}
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    ps = [ctx.Process(target=_worker, args=(r, 2, port, prob.depth, ncones, lay, ex, q))
-          for r in range(2)]
+    ps = [ctx.Process(target=_boot_worker, args=(r, 2, port, q)) for r in range(2)]
     for p in ps:
         p.start()
     res = sorted(q.get(timeout=120) for _ in ps)
     for p in ps:
         p.join(timeout=60)
-    assert all(ok for _, ok, _ in res), res
-    total = sum(len(a) for lists in ex.recv.values() for row in lists for a in row)
-    assert sum(m for _, _, m in res) == total
+    assert [r[0] for r in res] == [0, 1]
+    assert all(r[1] == bytes(range(128)) for r in res)
+    assert [r[2] for r in res] == [1, 0]      # only rank 0 made the id
+    assert all(r[3] == 1.5 for r in res)      # max over ranks
 
 
-def _plan_worker(rank, world, port, lay, depth, needs, out):
-    import torch.distributed as dist
-
-    from paper_2112_15198_b200.dist import build_exchange_plan_rank
-    os.environ["MASTER_ADDR"] = "127.0.0.1"
-    os.environ["MASTER_PORT"] = str(port)
-    dist.init_process_group("gloo", rank=rank, world_size=world)
-    ex = build_exchange_plan_rank(lay, depth, rank, lambda d, k: needs[rank][(d, k)])
-    out.put((rank, {k: ([a.tolist() for a in ex.recv[k][rank]],
-                        [a.tolist() for a in ex.send[k][rank]]) for k in ex.recv}))
-    dist.destroy_process_group()
-
-
-def test_rank_local_exchange_plan_over_gloo(oracle):
-    """build_exchange_plan_rank (own needs + all-to-all) gives every rank the
-    same rows as the full plan computed from everyone's needs."""
-    import torch.multiprocessing as mp
+def test_send_lists_pair_with_halos(oracle):
+    """The request protocol of csrc/dist.cu on host data: rank r's halo at a
+    level is the union of its two exchange sets, sorted; the owner p's send
+    list for r is the slice of r's halo owned by p (contiguous, since owner
+    intervals are), so sends and receives pair up one to one."""
     prob = _problem(oracle, n=5000, seed=47)
-    R = 2
+    R = 3
     lay, ex = _layout_and_plan(prob, R)
-    needs = [{k: np.concatenate(ex.recv[k][r]).astype(np.uint32) for k in ex.recv}
-             for r in range(R)]
-    ctx = mp.get_context("spawn")
-    q = ctx.Queue()
-    port = _free_port()
-    ps = [ctx.Process(target=_plan_worker, args=(r, R, port, lay, prob.depth, needs, q))
-          for r in range(R)]
-    for p in ps:
-        p.start()
-    res = dict(q.get(timeout=120) for _ in ps)
-    for p in ps:
-        p.join(timeout=60)
-    for r in range(R):
-        for k in ex.recv:
-            recv, send = res[r][k]
-            assert recv == [a.tolist() for a in ex.recv[k][r]]
-            assert send == [a.tolist() for a in ex.send[k][r]]
+    for d in range(3, prob.depth + 1):
+        for r in range(R):
+            parts = [np.concatenate(ex.recv[(d, k)][r]) for k in (0, 1) if (d, k) in ex.recv]
+            halo = np.unique(np.concatenate(parts)) if parts else np.zeros(0, np.uint32)
+            owner = lay.cone_owner(d, halo) if len(halo) else np.zeros(0, np.int64)
+            assert np.all(np.diff(owner) >= 0)  # owner runs are contiguous in the halo
+            qb, qe = lay.cones(d, r)
+            below = int(np.sum(halo < qb))
+            assert np.all(halo[below:] >= qe)   # [halo below | owned | halo above]
+            for p in range(R):
+                mine = halo[owner == p]
+                assert p != r or len(mine) == 0
+                pb, pe = lay.cones(d, p)
+                assert np.all((mine >= pb) & (mine < pe))

@@ -1,8 +1,11 @@
-"""Multi-rank path on one B200: R ranks simulated in one process (one plan
-per rank, phases advanced rank by rank, blocks moved through the device
-pack/unpack of the C ABI).  Mirrors test_dist.cpp:107-123 -- the output is
-bitwise identical to the single-GPU apply for every rank count -- and checks
-the device-computed exchange sets against the oracle (dist.cpp:179-237)."""
+"""Multi-GPU engine (csrc/dist.cu) on one B200: R rank plans in one process
+(ifgf_run_distributed, the analogue of dist::run_distributed), each with its
+own partitioned block storage (owned cones + halo), blocks moved rank to rank
+by the device pack + copies that NCCL send/recv replaces across processes.
+Mirrors test_dist.cpp:107-123 -- the output is bitwise identical to the
+single-GPU apply for every rank count -- and pins the per-rank exchange sets
+against the oracle and the reference's CommStats counters
+(dist.cpp:179-237, 253-272)."""
 import math
 
 import numpy as np
@@ -18,6 +21,13 @@ def case(gpu):
     pc = gpu.generate(6000, 0, 1.0, 0, 41)
     cfg = gpu.KernelConfig(gpu.KernelKind.Helmholtz, 2 * math.pi * 3.0)
     return pc, cfg
+
+
+def _single(gpu, pc, cfg, p=None):
+    plan = gpu.Plan.from_cloud(pc, cfg, p or gpu.EngineParams())
+    out = plan.apply(pc.a_re, pc.a_im)
+    plan.close()
+    return out
 
 
 def test_exchange_sets_match_oracle(gpu, oracle, case):
@@ -37,28 +47,65 @@ def test_exchange_sets_match_oracle(gpu, oracle, case):
                                           prob.exchange_set(R, r, d, kind)), (R, r, d, kind)
 
 
-@pytest.mark.parametrize("R", [1, 2, 4])
-def test_simulated_ranks_bitwise_equal_single_gpu(gpu, case, R):
-    from paper_2112_15198_b200.dist import simulate
+@pytest.mark.parametrize("R", [1, 2, 3, 4, 8])
+def test_rank_group_bitwise_equal_single_gpu(gpu, case, R):
+    from paper_2112_15198_b200.dist import run_distributed
     pc, cfg = case
-    single = gpu.Plan.from_cloud(pc, cfg)
-    s_re, s_im, _ = single.apply(pc.a_re, pc.a_im)
-    plans = [gpu.Plan.from_cloud(pc, cfg) for _ in range(R)]
-    i_re, i_im, moved, ex = simulate(plans, pc.a_re, pc.a_im)
-    assert np.array_equal(i_re, s_re) and np.array_equal(i_im, s_im)
-    assert moved == ex.volume_blocks()
+    s_re, s_im, _ = _single(gpu, pc, cfg)
+    q = pc.copy()
+    rep, infos = run_distributed(q, cfg, gpu.EngineParams(), R)
+    assert np.array_equal(q.i_re, s_re) and np.array_equal(q.i_im, s_im)
+    assert [i.rank for i in infos] == list(range(R))
+    # the ranks' point intervals tile [0, N); owned cones tile every level
+    assert infos[0].point_begin == 0 and infos[-1].point_end == len(pc.x1)
+    for a, b in zip(infos, infos[1:]):
+        assert a.point_end == b.point_begin
+    for k, lv in enumerate(infos[0].levels):
+        assert sum(i.levels[k]["owned_cones"] for i in infos) == rep.levels[k].cones
+        # what one rank sends is what the others receive
+        assert sum(i.levels[k]["sent_cones"] for i in infos) == \
+            sum(i.levels[k]["halo_cones"] for i in infos)
     if R == 1:
-        assert moved == 0
+        assert all(lv["halo_cones"] == 0 for lv in infos[0].levels)
+
+
+def test_rank_group_counters_match_reference(gpu, ref, case):
+    """Per level, the ranks' interpolation / propagation fetch counts equal the
+    reference's window counters (dist.cpp:253-272) at R = 4."""
+    from paper_2112_15198_b200.dist import run_distributed
+    pc, cfg = case
+    R = 4
+    _, infos = run_distributed(pc.copy(), cfg, gpu.EngineParams(), R)
+    _, _, comm = ref.run_distributed(pc.x1, pc.x2, pc.x3, pc.a_re, pc.a_im, 0, cfg.wavenumber,
+                                     Params(threads=4), R)
+    for k, row in enumerate(comm):
+        assert sum(i.levels[k]["interp_needed"] for i in infos) == int(row[0])
+        assert sum(i.levels[k]["prop_needed"] for i in infos) == int(row[1])
+
+
+def test_rank_storage_shrinks_with_ranks(gpu):
+    """Block storage is partitioned: per rank it falls ~1/R (owned + halo),
+    while a single-GPU plan holds every level's blocks."""
+    from paper_2112_15198_b200.dist import run_distributed
+    pc = gpu.generate(40000, 0, 1.0, 0, 53)
+    cfg = gpu.KernelConfig(gpu.KernelKind.Helmholtz, 2 * math.pi * 6.0)
+    per = {}
+    for R in (1, 2, 4, 8):
+        q = pc.copy()
+        _, infos = run_distributed(q, cfg, gpu.EngineParams(), R)
+        per[R] = max(i.block_bytes for i in infos)
+    assert per[2] < 0.62 * per[1]
+    assert per[4] < 0.36 * per[1]
+    assert per[8] < 0.22 * per[1]
 
 
 @pytest.mark.parametrize("R", [2, 4, 8])
 def test_work_partition_layout_and_bitwise(gpu, R):
     """IFGF_PARTITION_WORK (contiguous intervals balanced by evaluation work,
     the paper's proposed extension) on a non-uniform spheroid: a valid layout
-    (monotone, covering, whole boxes, point cuts on box boundaries) that
-    differs from the reference's count-balanced one, and the distributed
+    that differs from the reference's count-balanced one, and the rank group
     result is still bitwise the single-GPU apply."""
-    from paper_2112_15198_b200.dist import simulate
+    from paper_2112_15198_b200.dist import run_distributed
     pc = gpu.generate(40000, 1, 0.25, 0, 43)  # oblate spheroid (1,1,0.25)
     cfg = gpu.KernelConfig(gpu.KernelKind.Helmholtz, 2 * math.pi * 6.0)
     single = gpu.Plan.from_cloud(pc, cfg)
@@ -73,65 +120,17 @@ def test_work_partition_layout_and_bitwise(gpu, R):
         row = cb[d - 3]
         assert row[0] == 0 and row[-1] == info.cones[d] and np.all(np.diff(row.astype(np.int64)) >= 0)
     assert not (np.array_equal(bb, bb0) and np.array_equal(cb, cb0))
-    plans = [gpu.Plan.from_cloud(pc, cfg) for _ in range(R)]
-    i_re, i_im, moved, ex = simulate(plans, pc.a_re, pc.a_im, partition=gpu.Plan.PARTITION_WORK)
-    assert np.array_equal(i_re, s_re) and np.array_equal(i_im, s_im)
-    assert moved == ex.volume_blocks()
+    q = pc.copy()
+    _, infos = run_distributed(q, cfg, gpu.EngineParams(partition=gpu.Plan.PARTITION_WORK), R)
+    assert np.array_equal(q.i_re, s_re) and np.array_equal(q.i_im, s_im)
+    assert [i.point_begin for i in infos] + [infos[-1].point_end] == [int(v) for v in pb]
 
 
-def _dplan_worker(rank, world, port, args, out, partition=0):
-    import os
-
-    import torch
-    import torch.distributed as dist
-
-    import paper_2112_15198_b200 as ifgf
-    from paper_2112_15198_b200.dist import DistributedPlan
-    os.environ["MASTER_ADDR"] = "127.0.0.1"
-    os.environ["MASTER_PORT"] = str(port)
-    torch.cuda.set_device(0)
-    dist.init_process_group("gloo", rank=rank, world_size=world)
-    n, shape, c, dens, seed, kappa = args
-    pc = ifgf.generate(n, shape, c, dens, seed)
-    cfg = ifgf.KernelConfig(ifgf.KernelKind.Helmholtz, kappa)
-    dp = DistributedPlan(pc.x1, pc.x2, pc.x3, cfg, partition=partition)
-    i_re, i_im = dp.apply(pc.a_re, pc.a_im)
-    vol = dp.ex.volume_blocks()
-    dp.close()
-    out.put((rank, i_re, i_im, vol))
-    dist.destroy_process_group()
-
-
-@pytest.mark.parametrize("partition", [0, 1])
-def test_distributed_plan_two_ranks_one_gpu(gpu, partition):
-    """The whole DistributedPlan path (rank layout, per-rank exchange sets and
-    the all-to-all that pairs them, per-level block exchange, result gather)
-    on real kernels: two processes share the GPU, blocks travel through gloo
-    (host staging; NCCL moves device buffers on a multi-GPU box).  Ranks only
-    wait on each other at the host exchanges, never inside kernels.  The
-    result equals the single-GPU apply bitwise."""
-    import socket
-
-    import torch.multiprocessing as mp
-    args = (6000, 0, 1.0, 0, 61, 2 * math.pi * 2.0)
-    pc = gpu.generate(*args[:5])
-    cfg = gpu.KernelConfig(gpu.KernelKind.Helmholtz, args[5])
-    plan = gpu.Plan.from_cloud(pc, cfg, gpu.EngineParams())
-    ref = plan.apply(pc.a_re, pc.a_im)
-    plan.close()
-    s = socket.socket()
-    s.bind(("127.0.0.1", 0))
-    port = s.getsockname()[1]
-    s.close()
-    ctx = mp.get_context("spawn")
-    q = ctx.Queue()
-    ps = [ctx.Process(target=_dplan_worker, args=(r, 2, port, args, q, partition))
-          for r in range(2)]
-    for p in ps:
-        p.start()
-    res = [q.get(timeout=300) for _ in ps]
-    for p in ps:
-        p.join(timeout=60)
-    for rank, i_re, i_im, vol in res:
-        assert vol > 0
-        assert np.array_equal(i_re, ref[0]) and np.array_equal(i_im, ref[1]), rank
+def test_rank_group_laplace_and_deeper_tree(gpu):
+    from paper_2112_15198_b200.dist import run_distributed
+    pc = gpu.generate(20000, 0, 1.0, 1, 71)
+    cfg = gpu.KernelConfig(gpu.KernelKind.Laplace, 0.0)
+    s_re, s_im, _ = _single(gpu, pc, cfg)
+    q = pc.copy()
+    run_distributed(q, cfg, gpu.EngineParams(), 3)
+    assert np.array_equal(q.i_re, s_re) and np.array_equal(q.i_im, s_im)

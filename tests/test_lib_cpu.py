@@ -29,7 +29,7 @@ def test_library_exports_every_declared_symbol(ifgf):
         assert hasattr(raw, n), f"{n} declared in ifgf_b200.h but not exported"
         assert n in _lib.SIGNATURES, f"{n} not bound in _lib.SIGNATURES"
     assert set(_lib.SIGNATURES) <= set(names)
-    assert ifgf._lib.lib.ifgf_abi_version() == 1
+    assert ifgf._lib.lib.ifgf_abi_version() == 2
 
 
 def test_library_is_sm100a_only(ifgf):
