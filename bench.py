@@ -45,6 +45,8 @@ def parse():
     ap.add_argument("--config", default="C2")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    # the N>1 code path (rank engine + NCCL) at any N, e.g. N=1 on a one-GPU box
+    ap.add_argument("--dist", action="store_true")
     return ap.parse_args()
 
 
@@ -211,7 +213,7 @@ def run_reference(args):
     print(json.dumps({
         "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": t_matvec * 1e3,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (seeded generator, DESIGN.md Inputs)",
         "config": {"workload": f"{cfg.label} (BASELINE configs[1]), orders (3,5,5), "
                                f"depth {depth}",
@@ -404,7 +406,7 @@ def run_ours(args):
         line = {
             "metric": METRIC, "value": world * n / t_step / 1e6, "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": t_step * 1e3,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (seeded generator, DESIGN.md Inputs)",
             "config": {"workload": f"{cfgd.label} (BASELINE configs[1]), orders (3,5,5), "
                                    f"depth {info.depth}",
@@ -433,59 +435,126 @@ def run_ours(args):
 
 
 def run_ours_dist(args):
-    """N > 1: the C2 matvec split across ranks (strong scaling) with the
-    reference's rank algorithm (dist.cpp:241-361) -- per-level block exchange
-    over NCCL (paper_2112_15198_b200/dist.py).  One step = every rank builds
-    the plan + the distributed apply; inputs and the gathered result are host
-    arrays, so this is also the end-to-end number."""
+    """N > 1: C2 split across N GPUs (strong scaling) by the C++ rank engine
+    (csrc/dist.cu): one process per GPU, NCCL communicator over NVLink;
+    every rank builds the structure (replicated setup) and owns its Morton
+    interval of points and its cone intervals per level; per-level halo
+    exchanges of cone-segment blocks (dist.cpp:241-361).  One step = the rank
+    plan build (setup + exchange lists, collective) + the distributed apply
+    (full result in the caller's order on every rank), device-resident
+    inputs; e2e adds the host copies of the inputs and the result."""
     import torch
     import torch.distributed as dist
 
     import paper_2112_15198_b200 as ifgf
-    from paper_2112_15198_b200.dist import DistributedPlan
+    from paper_2112_15198_b200.dist import Comm, DistPlan, max_over_ranks, share_comm_id
 
     rank, local, world = dist_env()
-    # IFGF_BENCH_BACKEND=gloo: functional check of this path with all ranks on
-    # the visible GPU(s) and host-staged exchanges -- not a performance number
-    backend = os.environ.get("IFGF_BENCH_BACKEND", "nccl")
-    dev_index = local if backend == "nccl" else local % torch.cuda.device_count()
-    torch.cuda.set_device(dev_index)
-    if backend == "nccl":
-        dist.init_process_group("nccl", device_id=torch.device("cuda", dev_index))
-    else:
-        dist.init_process_group(backend)
-    wire = torch.device("cuda", dev_index) if backend == "nccl" else torch.device("cpu")
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+    os.environ.setdefault("MASTER_PORT", "29517")
+    dist.init_process_group("nccl", device_id=dev, rank=rank, world_size=world)
+    if not ifgf.device_ok():
+        raise SystemExit("bench: no usable sm_100 device: " + ifgf._lib.last_error())
     cfgd = ifgf.configs.CONFIGS[args.config]
     kcfg = ifgf.KernelConfig(ifgf.KernelKind(cfgd.kind), cfgd.kappa)
+    params = ifgf.EngineParams(depth=cfgd.depth, device=local)
     n = cfgd.n
     pc = ifgf.generate(n, cfgd.shape, cfgd.c, cfgd.dens, cfgd.seed)
-
-    launches = [0]
+    comm = Comm(share_comm_id(Comm.unique_id), rank, world, local)
+    X = [torch.from_numpy(a).to(dev) for a in (pc.x1, pc.x2, pc.x3, pc.a_re, pc.a_im)]
+    out = [torch.empty(n, dtype=torch.float64, device=dev) for _ in range(2)]
+    flush = torch.empty(256 * 2**20 // 4, dtype=torch.float32, device=dev)
+    s = torch.cuda.Stream(device=dev)
+    sh = s.cuda_stream
+    info = {}
 
     def step():
-        dp = DistributedPlan(pc.x1, pc.x2, pc.x3, kcfg, ifgf.EngineParams(depth=cfgd.depth))
-        out = dp.apply(pc.a_re, pc.a_im)
-        vol = dp.ex.volume_blocks()
-        launches[0] = int(dp.plan._info().launches)  # this rank's kernels in the step
-        dp.close()
-        return out, vol
+        plan = DistPlan(comm, X[0].data_ptr(), X[1].data_ptr(), X[2].data_ptr(), n, kcfg, params,
+                        stream=sh)
+        rep = plan.apply_device(X[3].data_ptr(), X[4].data_ptr(), out[0].data_ptr(),
+                                out[1].data_ptr(), stream=sh)
+        if not info:
+            ri = plan.info()
+            info["rank"] = ri
+            info["launches"] = int(plan.plan_info().launches)
+        plan.close()
+        return rep
+
+    def barrier():
+        torch.cuda.synchronize()
+        dist.barrier()
+        torch.cuda.synchronize()
 
     for _ in range(args.warmup):
         step()
-    times = []
-    with ClockSampler(dev_index) as clocks:
-        for _ in range(args.steps):
-            torch.cuda.synchronize()
-            dist.barrier()
-            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            e0.record()
-            _, vol = step()
-            e1.record()
-            torch.cuda.synchronize()
-            times.append(e0.elapsed_time(e1) / 1e3)
-    t = torch.tensor([statistics.mean(times)], device=wire, dtype=torch.float64)
-    dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    t_step = float(t.item())
+    barrier()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+          for _ in range(args.steps)]
+    with ClockSampler(local) as clocks:
+        for i in range(args.steps):
+            with torch.cuda.stream(s):
+                flush.zero_()
+            ev[i][0].record(s)
+            step()
+            ev[i][1].record(s)
+        torch.cuda.synchronize()
+    barrier()
+    step_ms = [a.elapsed_time(b) for a, b in ev]
+    t_step = max_over_ranks(statistics.mean(step_ms) / 1e3, device=dev)
+
+    # apply only (rank plan reused)
+    plan = DistPlan(comm, X[0].data_ptr(), X[1].data_ptr(), X[2].data_ptr(), n, kcfg, params,
+                    stream=sh)
+    for _ in range(2):
+        plan.apply_device(X[3].data_ptr(), X[4].data_ptr(), out[0].data_ptr(),
+                          out[1].data_ptr(), stream=sh)
+    barrier()
+    ev2 = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+           for _ in range(args.steps)]
+    for i in range(args.steps):
+        with torch.cuda.stream(s):
+            flush.zero_()
+        ev2[i][0].record(s)
+        plan.apply_device(X[3].data_ptr(), X[4].data_ptr(), out[0].data_ptr(),
+                          out[1].data_ptr(), stream=sh)
+        ev2[i][1].record(s)
+    torch.cuda.synchronize()
+    t_apply = max_over_ranks(statistics.mean(a.elapsed_time(b) for a, b in ev2) / 1e3,
+                             device=dev)
+    plan.close()
+
+    # e2e: pinned host inputs in, result out, every step
+    e2e = None
+    if not args.no_e2e:
+        host = [torch.from_numpy(a).pin_memory() for a in (pc.x1, pc.x2, pc.x3, pc.a_re, pc.a_im)]
+        hout = [torch.empty(n, dtype=torch.float64).pin_memory() for _ in range(2)]
+        et = []
+        for i in range(args.warmup + args.steps):
+            barrier()
+            t0 = time.perf_counter()
+            with torch.cuda.stream(s):
+                for d_, h_ in zip(X, host):
+                    d_.copy_(h_, non_blocking=True)
+            step()
+            with torch.cuda.stream(s):
+                hout[0].copy_(out[0], non_blocking=True)
+                hout[1].copy_(out[1], non_blocking=True)
+            s.synchronize()
+            if i >= args.warmup:
+                et.append(time.perf_counter() - t0)
+        te = max_over_ranks(statistics.mean(et), device=dev)
+        e2e = {"value": n / te / 1e6, "unit": UNIT, "h2d_bytes_per_step": 5 * n * 8,
+               "d2h_bytes_per_step": 2 * n * 8, "ms_per_step": te * 1e3,
+               "api": "ifgf_dist_plan_create_device + ifgf_dist_plan_apply_device (C ABI), "
+                      "pinned host buffers, every rank"}
+    ri = info.get("rank")
+    halo = None
+    if ri is not None:
+        halo = {"rank0_block_bytes": ri.block_bytes,
+                "rank0_levels": [{k: lv[k] for k in ("d", "owned_cones", "halo_cones")}
+                                 for lv in ri.levels]}
     if rank == 0:
         print(json.dumps({
             "metric": METRIC, "value": n / t_step / 1e6, "unit": UNIT, "n_gpus": world,
@@ -493,14 +562,18 @@ def run_ours_dist(args):
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (seeded generator, DESIGN.md Inputs)",
             "config": {"workload": f"{cfgd.label} (BASELINE configs[1]) split over {world} GPUs",
-                       "n": n, "parallelism": f"rank layout dist.cpp:78-130 x{world}",
-                       "exchanged_blocks_per_step": vol,
-                       "step": "plan build (replicated) + distributed apply, host in/out"},
-            "e2e": {"value": n / t_step / 1e6, "unit": UNIT, "h2d_bytes_per_step": 5 * n * 8,
-                    "d2h_bytes_per_step": 2 * n * 8, "note": "the step is host-to-host"},
-            "gpu_launches": launches[0], "roofline": None, "cpu_baseline": None,
-            "clocks": clocks.summary(),
+                       "n": n, "kappa": cfgd.kappa, "orders": [3, 5, 5],
+                       "parallelism": f"rank layout dist.cpp:78-130 x{world}, NCCL halo exchange",
+                       "l2": "flushed between steps (256 MB write)",
+                       "step": "rank plan build (replicated setup + exchange lists) + "
+                               "distributed apply, device-resident inputs"},
+            "apply_only": {"value": n / t_apply / 1e6, "unit": UNIT, "ms_per_step": t_apply * 1e3},
+            "setup_ms": (t_step - t_apply) * 1e3,
+            "partition": halo,
+            "e2e": e2e, "gpu_launches": info.get("launches", 0), "roofline": None,
+            "cpu_baseline": None, "clocks": clocks.summary(), "step_ms_all": step_ms,
         }), flush=True)
+    comm.close()
     dist.destroy_process_group()
 
 
@@ -508,7 +581,7 @@ def main():
     args = parse()
     if args.impl == "reference":
         run_reference(args)
-    elif dist_env()[2] > 1:
+    elif dist_env()[2] > 1 or args.dist:
         run_ours_dist(args)
     else:
         run_ours(args)

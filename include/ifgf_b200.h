@@ -103,28 +103,21 @@ void ifgf_plan_destroy(ifgf_plan* plan);
  * IFGF_OPT_SERIAL = 1: every apply kernel on one stream (no near-field /
  *   interpolation overlap) so per-pass event times are exclusive.
  * IFGF_OPT_PROP_KERNEL selects the propagation kernel:
- *   IFGF_PROP_NODE  (0) thread per (parent cone, node), locate per child;
- *   IFGF_PROP_TILES (1) per node from the precomputed (gamma, octant) geometry;
- *   IFGF_PROP_DMMA  (2) FP64 tensor-core batched GEMM over cones sharing gamma;
+ *   IFGF_PROP_NODE  (0) thread per (parent cone, node), locate per child
+ *                       (the generic path: any orders);
+ *   IFGF_PROP_DMMA  (2) box-batched FP64 tensor-core GEMM: up to 64 parent
+ *                       cones sharing gamma per CTA, mma.sync.m8n8k4.f64 with
+ *                       the node basis held in registers (whole levels only;
+ *                       ranges and levels without the precomputed geometry
+ *                       run ROWS / FLY);
  *   IFGF_PROP_ROWS  (3, default) thread per (parent cone, child, row of <= 3
  *                       nodes that share a child cone) from the precomputed
  *                       geometry, one block load per row; levels without
  *                       the precomputed geometry run IFGF_PROP_FLY;
  *   IFGF_PROP_FLY   (4) the same rows grouped per parent cone on the fly
- *                       (no precomputed geometry);
- *   IFGF_PROP_STREAM(5) the precomputed rows evaluated with the
- *                       child block held in registers (one s-plane per
- *                       lane of a 3-lane group) while the nodes of a run
- *                       of rows sharing the child cone stream past; orders
- *                       whose planes do not fit in registers run ROWS,
- *                       levels without the precomputed geometry run FLY.
- *   IFGF_PROP_PIPE  (6) warp-specialised: a producer warp TMA-stages each
- *                       unit's tile rows and child blocks in a ring of
- *                       shared-memory stages, consumer warps evaluate from
- *                       shared memory only; levels without the
- *                       precomputed geometry run FLY.
- *   Where the precomputed geometry is not built (too few parent cones per
- *   gamma, P > 255) TILES and DMMA run IFGF_PROP_NODE.
+ *                       (no precomputed geometry).
+ *   Values 1, 5, 6 (TILES, STREAM, PIPE of ABI 1) were measured slower than
+ *   ROWS and removed; they fail with IFGF_EINVAL.
  *   All agree to rounding; DESIGN.md records their measured times.
  * IFGF_OPT_NEAR_KERNEL selects the near-field kernel:
  *   IFGF_NEAR_POINT (0) thread per target point, neighbour sources in order;
@@ -148,12 +141,9 @@ enum { IFGF_NEAR_POINT = 0, IFGF_NEAR_BOX = 1 };
 enum { IFGF_PARTITION_COUNT = 0, IFGF_PARTITION_WORK = 1 };
 enum {
   IFGF_PROP_NODE = 0,
-  IFGF_PROP_TILES = 1,
   IFGF_PROP_DMMA = 2,
   IFGF_PROP_ROWS = 3,
-  IFGF_PROP_FLY = 4,
-  IFGF_PROP_STREAM = 5,
-  IFGF_PROP_PIPE = 6
+  IFGF_PROP_FLY = 4
 };
 int ifgf_plan_set_option(ifgf_plan* plan, int option, int value);
 
@@ -268,6 +258,8 @@ typedef struct ifgf_dist_info {
   ifgf_dist_level levels[IFGF_MAX_LEVELS]; /* index d - 3 */
   size_t block_bytes;                 /* this rank's block storage (owned + halo) */
   size_t device_bytes;                /* all of this rank plan's device memory */
+  double compute_seconds;             /* ifgf_run_distributed with IFGF_DIST_RANK_TIMING=1:
+                                         this rank's kernels, ranks serialised (load balance) */
 } ifgf_dist_info;
 int ifgf_dist_plan_info(const ifgf_plan* plan, ifgf_dist_info* info);
 

@@ -223,6 +223,7 @@ class COracle(_Checker):
         L.oc_apply.argtypes = [C.c_size_t] + [_dp] * 5 + [C.c_int, C.c_double,
                                                            C.POINTER(_OcParams), _dp, _dp,
                                                            C.POINTER(_OcReport)]
+        L.oc_apply_lean.argtypes = L.oc_apply.argtypes
         L.oc_direct_eval.argtypes = [C.c_size_t] + [_dp] * 5 + [C.c_int, C.c_double, C.c_void_p,
                                                                  C.c_size_t, _dp, _dp]
         L.oc_sample_indices.argtypes = [C.c_size_t, C.c_size_t, C.c_uint64, _u32p]
@@ -268,6 +269,17 @@ class COracle(_Checker):
         self.lib.oc_set_threads(max(1, p.threads))
         self._check(self.lib.oc_apply(n, _c(x1), _c(x2), _c(x3), _c(ar), _c(ai), kind, k,
                                       C.byref(_OcParams.of(p)), ir, ii, C.byref(rep)))
+        return ir, ii, {"seconds": list(rep.seconds), "depth": rep.depth,
+                        "peak_live_blocks": rep.peak_live_blocks}
+
+    def apply_lean(self, x1, x2, x3, ar, ai, kind, k, p: Params):
+        """oc_apply_lean: depth-first, O(depth) live blocks (C5 in a few GB)."""
+        n = len(x1)
+        ir, ii = np.zeros(n), np.zeros(n)
+        rep = _OcReport()
+        self.lib.oc_set_threads(max(1, p.threads))
+        self._check(self.lib.oc_apply_lean(n, _c(x1), _c(x2), _c(x3), _c(ar), _c(ai), kind, k,
+                                           C.byref(_OcParams.of(p)), ir, ii, C.byref(rep)))
         return ir, ii, {"seconds": list(rep.seconds), "depth": rep.depth,
                         "peak_live_blocks": rep.peak_live_blocks}
 

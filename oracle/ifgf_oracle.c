@@ -1261,6 +1261,238 @@ int oc_apply(size_t n, const double* x1, const double* x2, const double* x3,
   return rc;
 }
 
+/* ------------------------------------------------------------ lean apply
+ * oc_apply_lean: the same matvec as oc_apply with O(depth) live blocks
+ * instead of the reference's two full levels (engine.cpp:280-308), so C5
+ * (25 M points, ~1.1e8 live blocks = 132 GB in the level-by-level form) runs
+ * in a few GB.  Depth-first over the tree: a box's blocks are built from its
+ * children's (recursively, children in Morton order: the propagation sums of
+ * engine.cpp:138-189 in the reference's per-node child order, the same
+ * arithmetic as oc_propagation_pass), then pushed to the targets that see
+ * the box as a cousin (cousin relation is symmetric: the interpolation of
+ * engine.cpp:191-231 reorganised by source box instead of by target), then
+ * dropped once the parent has consumed them.  Level-3 subtrees are split
+ * round-robin over the threads, each with its own result accumulators, summed
+ * in thread order at the end: deterministic for a given thread count.  Only
+ * the order in which a target's cousin contributions are added differs from
+ * the level-by-level form (agreement to rounding, tests/test_oracle_cpu.py). */
+typedef struct {
+  const oc_problem* P;
+  double *out_re, *out_im; /* this thread's result accumulators (sorted order) */
+  double* nodes;           /* 3 * np scratch */
+} lean_ctx;
+
+/* engine.cpp:107-136 for the cones of box b at level D, local indexing */
+static int lean_level_d(const oc_problem* P, uint32_t b, double* br, double* bi, double* nodes) {
+  const int D = P->depth, np = P_total(P);
+  const oc_level* L = &P->lv[D];
+  double vr[OC_MAXORDER * OC_MAXORDER * OC_MAXORDER], vi[OC_MAXORDER * OC_MAXORDER * OC_MAXORDER];
+  for (uint32_t q = L->box_cone[b]; q < L->box_cone[b + 1]; ++q) {
+    const size_t o = (size_t)(q - L->box_cone[b]) * np;
+    interp_nodes(&P->p, &L->g, L->cone_gamma[q], &L->ctr[3 * b], L->h, nodes);
+    for (int m = 0; m < np; ++m)
+      factored_sum(P->x1, P->x2, P->x3, P->ar, P->ai, L->first[b], L->first[b] + L->count[b],
+                   &nodes[3 * m], &L->ctr[3 * b], P->kappa, &vr[m], &vi[m]);
+    for (int m = 0; m < np; ++m)
+      if (!isfinite(vr[m]) || !isfinite(vi[m])) return fail(OC_EINVAL, "cheb_fit: non-finite node value");
+    oc_cheb_fit(P->p.p_s, P->p.p_theta, P->p.p_phi, vr, vi, br + o, bi + o);
+  }
+  return OC_OK;
+}
+
+/* engine.cpp:191-231 pushed from source box b at level d (blocks br/bi of
+ * b's cones, local order) to every point of every cousin of b */
+static int lean_push(lean_ctx* X, int d, uint32_t b, const double* br, const double* bi) {
+  const oc_problem* P = X->P;
+  const int np = P_total(P);
+  const oc_level* L = &P->lv[d];
+  const double rad = sqrt(3.0) * L->h / 2.0;
+  const double q4 = 1.0 / (4.0 * OC_PI);
+  const double* c = &L->ctr[3 * b];
+  for (uint32_t k = L->cous_off[b]; k < L->cous_off[b + 1]; ++k) {
+    const uint32_t t = L->cous.v[k];
+    for (uint32_t i = L->first[t]; i < L->first[t] + L->count[t]; ++i) {
+      const double x[3] = {P->x1[i], P->x2[i], P->x3[i]};
+      uint64_t g;
+      double tl[3];
+      const int rc = locate_cone(&L->g, rad, c, x, &g, tl);
+      if (rc) return rc;
+      const uint32_t q = find_cone(L, b, g);
+      if (q == OC_NOCONE)
+        return fail(OC_ELOGIC, "interpolation: cousin point not covered by a relevant cone");
+      const size_t o = (size_t)(q - L->box_cone[b]) * np;
+      double vr, vi;
+      oc_cheb_eval(P->p.p_s, P->p.p_theta, P->p.p_phi, br + o, bi + o, tl[0], tl[1], tl[2], &vr, &vi);
+      const double dx = x[0] - c[0], dy = x[1] - c[1], dz = x[2] - c[2];
+      const double r = sqrt(dx * dx + dy * dy + dz * dz);
+      const double inv = q4 / r;
+      double sn, cn;
+      oc_sincos_fast(P->kappa * r, &sn, &cn);
+      const double gr = cn * inv, gi = sn * inv;
+      X->out_re[i] += vr * gr - vi * gi;
+      X->out_im[i] += vr * gi + vi * gr;
+    }
+  }
+  return OC_OK;
+}
+
+/* blocks of box b at level d (local cone order) into *pr/*pi (malloc'd) */
+static int lean_box(lean_ctx* X, int d, uint32_t b, double** pr, double** pi) {
+  const oc_problem* P = X->P;
+  const int D = P->depth, np = P_total(P);
+  const oc_level* U = &P->lv[d];
+  const size_t nbc = U->box_cone[b + 1] - U->box_cone[b];
+  double* br = (double*)calloc(nbc * np + 1, sizeof(double));
+  double* bi = (double*)calloc(nbc * np + 1, sizeof(double));
+  int rc = OC_OK;
+  if (d == D) {
+    rc = lean_level_d(P, b, br, bi, X->nodes);
+  } else {
+    /* children first (their own pushes happen inside), then the propagation
+     * of engine.cpp:138-189 restricted to b's cones */
+    const uint32_t c0 = U->child_begin[b], c1 = U->child_begin[b + 1];
+    double **cr = (double**)calloc(c1 - c0 + 1, sizeof(double*)),
+           **ci = (double**)calloc(c1 - c0 + 1, sizeof(double*));
+    for (uint32_t cb = c0; cb < c1 && rc == OC_OK; ++cb)
+      rc = lean_box(X, d + 1, cb, &cr[cb - c0], &ci[cb - c0]);
+    const oc_level* L = &P->lv[d + 1];
+    const double rad = sqrt(3.0) * L->h / 2.0;
+    double* nodes = X->nodes;
+    double rp[OC_MAXORDER * OC_MAXORDER * OC_MAXORDER];
+    double acr[OC_MAXORDER * OC_MAXORDER * OC_MAXORDER], aci[OC_MAXORDER * OC_MAXORDER * OC_MAXORDER];
+    const double* pc = &U->ctr[3 * b];
+    for (uint32_t q = U->box_cone[b]; q < U->box_cone[b + 1] && rc == OC_OK; ++q) {
+      interp_nodes(&P->p, &U->g, U->cone_gamma[q], pc, U->h, nodes);
+      for (int m = 0; m < np; ++m) {
+        const double dx = nodes[3 * m] - pc[0], dy = nodes[3 * m + 1] - pc[1],
+                     dz = nodes[3 * m + 2] - pc[2];
+        rp[m] = sqrt(dx * dx + dy * dy + dz * dz);
+        acr[m] = aci[m] = 0.0;
+      }
+      for (uint32_t cb = c0; cb < c1 && rc == OC_OK; ++cb) {
+        const double* cc = &L->ctr[3 * cb];
+        for (int m = 0; m < np; ++m) {
+          uint64_t g;
+          double t[3];
+          if ((rc = locate_cone(&L->g, rad, cc, &nodes[3 * m], &g, t))) break;
+          const uint32_t cq = find_cone(L, cb, g);
+          if (cq == OC_NOCONE) {
+            rc = fail(OC_ELOGIC, "propagation: node not covered by a relevant child cone");
+            break;
+          }
+          const size_t o = (size_t)(cq - L->box_cone[cb]) * np;
+          double vr, vi;
+          oc_cheb_eval(P->p.p_s, P->p.p_theta, P->p.p_phi, cr[cb - c0] + o, ci[cb - c0] + o, t[0],
+                       t[1], t[2], &vr, &vi);
+          const double dx = nodes[3 * m] - cc[0], dy = nodes[3 * m + 1] - cc[1],
+                       dz = nodes[3 * m + 2] - cc[2];
+          const double rc_ = sqrt(dx * dx + dy * dy + dz * dz);
+          const double ratio = rp[m] / rc_;
+          double sn, cn;
+          oc_sincos_fast(P->kappa * (rc_ - rp[m]), &sn, &cn);
+          const double tr = ratio * cn, ti = ratio * sn;
+          acr[m] += vr * tr - vi * ti;
+          aci[m] += vr * ti + vi * tr;
+        }
+      }
+      const size_t o = (size_t)(q - U->box_cone[b]) * np;
+      if (rc == OC_OK) oc_cheb_fit(P->p.p_s, P->p.p_theta, P->p.p_phi, acr, aci, br + o, bi + o);
+    }
+    for (uint32_t k = 0; k < c1 - c0; ++k) {
+      free(cr[k]);
+      free(ci[k]);
+    }
+    free(cr);
+    free(ci);
+  }
+  if (rc == OC_OK) rc = lean_push(X, d, b, br, bi);
+  *pr = br;
+  *pi = bi;
+  return rc;
+}
+
+typedef struct {
+  const oc_problem* P;
+  int T;
+  lean_ctx* ctx; /* per thread */
+} lean_job;
+
+/* thread t takes level-3 boxes t, t + T, ... (deterministic split) */
+static int lean_thread_range(void* v, size_t t0, size_t t1) {
+  lean_job* J = (lean_job*)v;
+  for (size_t t = t0; t < t1; ++t) {
+    lean_ctx* X = &J->ctx[t];
+    const oc_level* L3 = &J->P->lv[3];
+    for (size_t b = t; b < L3->nb; b += (size_t)J->T) {
+      double *br, *bi;
+      const int rc = lean_box(X, 3, (uint32_t)b, &br, &bi);
+      free(br);
+      free(bi);
+      if (rc) return rc;
+    }
+  }
+  return OC_OK;
+}
+
+int oc_apply_lean(size_t n, const double* x1, const double* x2, const double* x3,
+                  const double* a_re, const double* a_im, int kind, double wavenumber,
+                  const oc_params* p, double* i_re, double* i_im, oc_report* rep) {
+  if (n < 2) return fail(OC_EINVAL, "apply: need at least two points");
+  const double t_all = now_s();
+  double t0 = now_s();
+  oc_problem* P;
+  int rc = oc_problem_build(n, x1, x2, x3, a_re, a_im, kind, wavenumber, p, &P);
+  if (rc) return rc;
+  oc_report r;
+  memset(&r, 0, sizeof r);
+  r.seconds[0] = now_s() - t0;
+  const int np = P_total(P);
+  double* sr = (double*)calloc(n, sizeof(double));
+  double* si = (double*)calloc(n, sizeof(double));
+  t0 = now_s();
+  {
+    pass_ctx X = {P, 0, NULL, NULL, sr, si};
+    rc = par_for(n, 4096, par_singular, &X);
+  }
+  r.seconds[1] = now_s() - t0;
+  const int T = g_threads;
+  lean_job J = {P, T, (lean_ctx*)calloc((size_t)T, sizeof(lean_ctx))};
+  for (int t = 0; t < T && !rc; ++t) {
+    J.ctx[t].P = P;
+    J.ctx[t].out_re = (double*)calloc(n, sizeof(double));
+    J.ctx[t].out_im = (double*)calloc(n, sizeof(double));
+    J.ctx[t].nodes = (double*)malloc(3 * (size_t)np * sizeof(double));
+    if (!J.ctx[t].out_re || !J.ctx[t].out_im) rc = fail(OC_ERUNTIME, "lean apply: out of memory");
+  }
+  t0 = now_s();
+  if (!rc) rc = par_for((size_t)T, 1, lean_thread_range, &J);
+  r.seconds[4] = now_s() - t0; /* propagation + interpolation, interleaved */
+  if (!rc) {
+    for (int t = 0; t < T; ++t)
+      for (size_t i = 0; i < n; ++i) {
+        sr[i] += J.ctx[t].out_re[i];
+        si[i] += J.ctx[t].out_im[i];
+      }
+    for (size_t i = 0; i < n; ++i) {
+      i_re[P->perm[i]] = sr[i];
+      i_im[P->perm[i]] = si[i];
+    }
+  }
+  for (int t = 0; t < T; ++t) {
+    free(J.ctx[t].out_re);
+    free(J.ctx[t].out_im);
+    free(J.ctx[t].nodes);
+  }
+  free(J.ctx);
+  free(sr);
+  free(si);
+  r.depth = P->depth;
+  oc_problem_free(P);
+  r.seconds[5] = now_s() - t_all;
+  if (rep) *rep = r;
+  return rc;
+}
+
 typedef struct {
   size_t n;
   const double *x1, *x2, *x3, *ar, *ai;

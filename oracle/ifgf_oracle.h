@@ -100,6 +100,12 @@ int oc_apply(size_t n, const double* x1, const double* x2, const double* x3,
              const double* a_re, const double* a_im, int kind, double wavenumber,
              const oc_params* p, double* i_re, double* i_im, oc_report* rep);
 
+/* The same operator depth-first with O(depth) live blocks (C5-sized runs in a
+ * few GB); agrees with oc_apply to rounding (cousin sums in another order). */
+int oc_apply_lean(size_t n, const double* x1, const double* x2, const double* x3,
+                  const double* a_re, const double* a_im, int kind, double wavenumber,
+                  const oc_params* p, double* i_re, double* i_im, oc_report* rep);
+
 int oc_direct_eval(size_t n, const double* x1, const double* x2, const double* x3,
                    const double* a_re, const double* a_im, int kind, double wavenumber,
                    const uint32_t* targets, size_t m, double* o_re, double* o_im);

@@ -55,7 +55,7 @@ class CDistInfo(C.Structure):
     _fields_ = [("rank", C.c_int), ("world", C.c_int), ("depth", C.c_int),
                 ("point_begin", C.c_size_t), ("point_end", C.c_size_t),
                 ("levels", CDistLevel * MAX_LEVELS), ("block_bytes", C.c_size_t),
-                ("device_bytes", C.c_size_t)]
+                ("device_bytes", C.c_size_t), ("compute_seconds", C.c_double)]
 
 
 COMM_ID_BYTES = 128

@@ -622,8 +622,10 @@ int ifgf_plan_set_option(ifgf_plan* P, int option, int value) {
     if (option == IFGF_OPT_SERIAL) {
       P->serial = value != 0;
     } else if (option == IFGF_OPT_PROP_KERNEL) {
-      if (value < IFGF_PROP_NODE || value > IFGF_PROP_PIPE)
-        throw Error(IFGF_EINVAL, "unknown propagation kernel");
+      if (value != IFGF_PROP_NODE && value != IFGF_PROP_DMMA && value != IFGF_PROP_ROWS &&
+          value != IFGF_PROP_FLY)
+        throw Error(IFGF_EINVAL, "unknown propagation kernel (TILES, STREAM and PIPE were "
+                                 "measured slower than ROWS and removed; DESIGN.md section 3)");
       P->prop_kernel = value;
     } else if (option == IFGF_OPT_PARTITION) {
       if (value < IFGF_PARTITION_COUNT || value > IFGF_PARTITION_WORK)

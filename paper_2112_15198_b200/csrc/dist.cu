@@ -43,6 +43,7 @@
 
 #include <algorithm>
 #include <chrono>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <string>
@@ -136,6 +137,7 @@ struct DistState {
   std::vector<uint32_t> cone_begin;              // (D-2)*(R+1), level-major from d=3
   DistLevel lv[IFGF_MAX_LEVELS];
   size_t block_bytes = 0;
+  double compute_seconds = 0.0;  // IFGF_DIST_RANK_TIMING (run_local_group)
   std::vector<cudaEvent_t> evs;  // scratch events of the in-process schedule
   ~DistState() {
     for (auto e : evs) cudaEventDestroy(e);
@@ -304,12 +306,12 @@ void dist_prepare(ifgf_plan* P, int R, int rank) {
     V.c1 = cb[rank + 1];
     IFGF_CUDA(cudaMemsetAsync(need, 0, L.nc + 1, s));
     const uint32_t* d_cbl = d_cb + (size_t)(d - 3) * (R + 1);
-    if (p1 > p0) {
+    if (R > 1 && p1 > p0) {
       k_need_interp<<<nblocks(p1 - p0, 128), 128, 0, s>>>(L.dev(), L.ptbox, P->xs, P->ys, P->zs,
                                                          p0, p1, d_cbl, R, rank, need, P->err);
       ++P->launches;
     }
-    if (d > 3) {
+    if (R > 1 && d > 3) {
       const uint32_t* cu = S->cone_begin.data() + (size_t)(d - 4) * (R + 1);
       const uint32_t q0 = cu[rank], q1 = cu[rank + 1];
       const size_t work = (size_t)(q1 - q0) * P->K.P;
@@ -357,8 +359,8 @@ void dist_prepare(ifgf_plan* P, int R, int rank) {
     if (V.recv_off[rank + 1] != V.hb)
       throw Error(IFGF_ELOGIC, "dist: a rank's halo contains its own cones");
     // storage and the rank's bitmap of present cones
+    // every slot is written each apply (owned: K2/K3, halo: the exchange)
     V.store = dalloc<double2>(P, (size_t)V.nslot * Pst + 2);
-    IFGF_CUDA(cudaMemsetAsync(V.store, 0, ((size_t)V.nslot * Pst + 2) * sizeof(double2), s));
     S->block_bytes += (size_t)V.nslot * Pst * sizeof(double2);
     uint64_t* lb = dalloc<uint64_t>(P, L.nwords);
     uint32_t* lr = dalloc<uint32_t>(P, L.nwords + 1);
@@ -679,14 +681,36 @@ void run_local_group(std::vector<ifgf_plan*>& G, const double* a_re, const doubl
       }
     }
   };
+  // IFGF_DIST_RANK_TIMING=1: ranks' compute phases serialised and timed one
+  // by one (the load-balance measure of ifgf_dist_info.compute_seconds;
+  // exchanges excluded), else ranks overlap on the device(s)
+  static const bool timing = [] {
+    const char* v = std::getenv("IFGF_DIST_RANK_TIMING");
+    return v && std::atoi(v) != 0;
+  }();
+  std::vector<double> secs(R, 0.0);
+  std::chrono::steady_clock::time_point tr;
+  auto t_begin = [&](ifgf_plan* P) {
+    if (!timing) return;
+    IFGF_CUDA(cudaDeviceSynchronize());
+    tr = std::chrono::steady_clock::now();
+    (void)P;
+  };
+  auto t_end = [&](int r) {
+    if (!timing) return;
+    IFGF_CUDA(cudaDeviceSynchronize());
+    secs[r] += std::chrono::duration<double>(std::chrono::steady_clock::now() - tr).count();
+  };
   for (int r = 0; r < R; ++r) {
     ifgf_plan* P = G[r];
     DistState* S = P->dist;
     IFGF_CUDA(cudaSetDevice(P->device));
+    t_begin(P);
     launch_gather_density(P, dens[r], a_im ? dens[r] + n : nullptr, P->s_main);
     IFGF_CUDA(cudaStreamWaitEvent(P->s_aux, ev_on(P, P->s_main), 0));
     launch_singular(P, S->point_begin[r], S->point_begin[r + 1], P->s_aux);
     launch_level_d(P, S->lv[D].c0, S->lv[D].c1, S->lv[D].owned_base(Pst), P->s_main);
+    t_end(r);
   }
   exchange_all(D);
   for (int d = D; d >= 3; --d) {
@@ -694,6 +718,7 @@ void run_local_group(std::vector<ifgf_plan*>& G, const double* a_re, const doubl
       ifgf_plan* P = G[r];
       DistState* S = P->dist;
       IFGF_CUDA(cudaSetDevice(P->device));
+      t_begin(P);
       IFGF_CUDA(cudaStreamWaitEvent(P->s_aux, ev_on(P, P->s_main), 0));
       launch_interpolation(P, d, S->point_begin[r], S->point_begin[r + 1], S->lv[d].store,
                            P->s_aux);
@@ -701,6 +726,7 @@ void run_local_group(std::vector<ifgf_plan*>& G, const double* a_re, const doubl
         const DistLevel& U = S->lv[d - 1];
         launch_propagation(P, d, U.c0, U.c1, S->lv[d].store, U.owned_base(Pst), P->s_main);
       }
+      t_end(r);
     }
     if (d > 3) exchange_all(d - 1);
   }
@@ -725,6 +751,7 @@ void run_local_group(std::vector<ifgf_plan*>& G, const double* a_re, const doubl
     for (auto e : G[r]->dist->evs) cudaEventDestroy(e);
     G[r]->dist->evs.clear();
   }
+  for (int r = 0; r < R; ++r) G[r]->dist->compute_seconds = secs[r];
   std::vector<uint32_t> perm(n);
   IFGF_CUDA(cudaSetDevice(P0->device));
   IFGF_CUDA(cudaMemcpy(perm.data(), P0->perm, n * 4, cudaMemcpyDeviceToHost));
@@ -843,6 +870,7 @@ void dist_fill_info(const ifgf_plan* P, ifgf_dist_info* info) {
   }
   info->block_bytes = S->block_bytes;
   info->device_bytes = P->bytes;
+  info->compute_seconds = S->compute_seconds;
 }
 
 }  // namespace ifgf_b200

@@ -104,6 +104,7 @@ class RankInfo:
     levels: list  # per d = 3..D: dict(owned_cones, halo_cones, interp_needed, prop_needed, sent_cones)
     block_bytes: int
     device_bytes: int
+    compute_seconds: float = 0.0  # with IFGF_DIST_RANK_TIMING=1 (run_distributed)
 
     @classmethod
     def from_c(cls, c, depth):
@@ -111,7 +112,7 @@ class RankInfo:
                ("owned_cones", "halo_cones", "interp_needed", "prop_needed", "sent_cones")}
               | {"d": d} for d in range(3, depth + 1)]
         return cls(c.rank, c.world, int(c.point_begin), int(c.point_end), lv,
-                   int(c.block_bytes), int(c.device_bytes))
+                   int(c.block_bytes), int(c.device_bytes), float(c.compute_seconds))
 
 
 def run_distributed(pc, cfg, p=None, n_ranks: int = 2, devices=None):

@@ -5,10 +5,13 @@ Run here (where /root/reference exists and oracle/_ref is built):
     python tests/golden/make_config_golden.py --checker oracle --threads 16 C5
 
 Checker: the UNMODIFIED reference library (oracle/_ref, default) or our C
-restatement (oracle/liboracle.so, multi-threaded oc_apply_mt) where the
-reference cannot run -- C5 needs ~4 h of single-threaded reference setup
-(DESIGN.md section 5), so C5 is pinned against the oracle, which is itself
-pinned to the reference at C1-C4 (tests/test_oracle_cpu.py).
+restatement (oracle/liboracle.so) where the reference cannot run: C5 needs
+~4 h of single-threaded reference setup and ~150 GB for its two live block
+levels, so C5 is pinned against the oracle's
+depth-first form (--checker lean: multi-threaded setup, O(depth) live
+blocks), which agrees with the reference's whole output to ~1e-15 at C1/C2
+(tests/test_oracle_cpu.py) and whose level-by-level form is pinned to the
+reference at C1-C4.
 
 Inputs come from the seeded generator, which the tests
 regenerate bit for bit, so a fixture stores, from the checker's apply():
@@ -51,7 +54,7 @@ def load_configs():
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("names", nargs="*", default=["C1"])
-    ap.add_argument("--checker", choices=["reference", "oracle"], default="reference")
+    ap.add_argument("--checker", choices=["reference", "oracle", "lean"], default="reference")
     ap.add_argument("--threads", type=int, default=os.cpu_count() or 8)
     ap.add_argument("--out", default=HERE)
     a = ap.parse_args()
@@ -63,7 +66,10 @@ def main():
         x1, x2, x3, ar, ai = oc.generate(c.n, c.shape, c.c, c.dens, c.seed)
         p = Params(depth=c.depth, threads=a.threads)
         t0 = time.time()
-        ir, ii, rep = chk.apply(x1, x2, x3, ar, ai, c.kind, c.kappa, p)
+        if a.checker == "lean":  # depth-first oracle: O(depth) live blocks (C5 in a few GB)
+            ir, ii, rep = oc.apply_lean(x1, x2, x3, ar, ai, c.kind, c.kappa, p)
+        else:
+            ir, ii, rep = chk.apply(x1, x2, x3, ar, ai, c.kind, c.kappa, p)
         t_apply = time.time() - t0
         err_idx = oc.sample_indices(c.n, 1000, c.seed + 1)
         # exact sums by the oracle's direct_eval (pinned to the reference's)

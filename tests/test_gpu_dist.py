@@ -134,3 +134,30 @@ def test_rank_group_laplace_and_deeper_tree(gpu):
     q = pc.copy()
     run_distributed(q, cfg, gpu.EngineParams(), 3)
     assert np.array_equal(q.i_re, s_re) and np.array_equal(q.i_im, s_im)
+
+
+def test_nccl_rank_plan_world1(gpu, case):
+    """The multi-process entry points on one GPU: an NCCL communicator of one
+    rank (libnccl loaded on first use), a rank plan and its apply through the
+    C ABI (device pointers), bitwise equal to the single-GPU apply.  (Two
+    ranks need two GPUs: NCCL refuses two ranks on one device; the in-process
+    group above covers the multi-rank data path.)"""
+    import torch
+
+    from paper_2112_15198_b200.dist import Comm, DistPlan
+    pc, cfg = case
+    s_re, s_im, _ = _single(gpu, pc, cfg)
+    comm = Comm(Comm.unique_id(), 0, 1, 0)
+    dev = torch.device("cuda", 0)
+    X = [torch.from_numpy(a).to(dev) for a in (pc.x1, pc.x2, pc.x3, pc.a_re, pc.a_im)]
+    out = [torch.empty(len(pc.x1), dtype=torch.float64, device=dev) for _ in range(2)]
+    plan = DistPlan(comm, X[0].data_ptr(), X[1].data_ptr(), X[2].data_ptr(), len(pc.x1), cfg)
+    for _ in range(2):  # plan reuse
+        plan.apply_device(X[3].data_ptr(), X[4].data_ptr(), out[0].data_ptr(), out[1].data_ptr())
+        torch.cuda.synchronize()
+        assert np.array_equal(out[0].cpu().numpy(), s_re)
+        assert np.array_equal(out[1].cpu().numpy(), s_im)
+    ri = plan.info()
+    assert ri.world == 1 and ri.point_begin == 0 and ri.point_end == len(pc.x1)
+    plan.close()
+    comm.close()

@@ -144,19 +144,18 @@ def test_direct_eval(built, gpu, oracle):
 
 
 def test_propagation_kernels_agree(built):
-    """The K3 implementations (per-node locate, precomputed tiles, FP64 DMMA
-    batched GEMM, register-blocked node rows from the tiles and grouped on the
-    fly) compute the same operator up to rounding."""
+    """The K3 implementations (per-node locate, FP64 DMMA box-batched GEMM,
+    register-blocked node rows from the tiles and grouped on the fly)
+    compute the same operator up to rounding; removed kernels are refused."""
     case, pc, cfg, ep, op, plan, prob = built
     res = []
-    kinds = (plan.PROP_NODE, plan.PROP_TILES, plan.PROP_DMMA, plan.PROP_ROWS, plan.PROP_FLY,
-             plan.PROP_STREAM, plan.PROP_PIPE)
+    kinds = (plan.PROP_NODE, plan.PROP_DMMA, plan.PROP_ROWS, plan.PROP_FLY)
     for kind in kinds:
         plan.set_prop_kernel(kind)
         res.append(plan.apply(pc.a_re, pc.a_im)[:2])
     plan.set_prop_kernel(plan.PROP_ROWS)
     for r in res[1:]:
         assert rel_l2(r[0], r[1], res[0][0], res[0][1]) <= 1e-13
-    # the pipelined kernel sums exactly what the rows kernel sums
-    rows, pipe = res[kinds.index(plan.PROP_ROWS)], res[kinds.index(plan.PROP_PIPE)]
-    assert np.array_equal(rows[0], pipe[0]) and np.array_equal(rows[1], pipe[1])
+    for removed in (1, 5, 6):
+        with pytest.raises(Exception):
+            plan.set_prop_kernel(removed)

@@ -1,18 +1,29 @@
-import math, sys
-sys.path.insert(0, '/root/repo')
-import numpy as np
-import paper_2112_15198_b200 as ifgf
-from paper_2112_15198_b200.dist import simulate
-for (n, shape, c, kap, R) in [(400000, 1, 0.25, 2*math.pi*16, 4), (400000, 1, 0.25, 2*math.pi*16, 8), (400000, 0, 1.0, 2*math.pi*16, 8)]:
-    pc = ifgf.generate(n, shape, c, 0, 43)
-    cfg = ifgf.KernelConfig(ifgf.KernelKind.Helmholtz, kap)
-    for mode in (0, 1):
-        plans = [ifgf.Plan.from_cloud(pc, cfg) for _ in range(R)]
-        res = []
-        for _ in range(3):
-            secs = []
-            simulate(plans, pc.a_re, pc.a_im, partition=mode, rank_seconds=secs)
-            res.append(secs)
-        best = min(res, key=lambda s: max(s))
-        print(n, shape, R, mode, "max/mean %.3f" % (max(best) / (sum(best) / R)), ["%.1f" % (1e3 * x) for x in best], flush=True)
-        for p in plans: p.close()
+"""Load balance of the rank layouts (IFGF_PARTITION_COUNT, the reference's,
+vs IFGF_PARTITION_WORK, the paper's proposed work-balanced extension): the
+in-process rank group (ifgf_run_distributed) with IFGF_DIST_RANK_TIMING=1,
+each rank's kernels timed alone; prints max/mean per layout.
+
+usage: IFGF_DIST_RANK_TIMING=1 python tools/partition_probe.py C4 8
+"""
+import os
+import sys
+
+os.environ.setdefault("IFGF_DIST_RANK_TIMING", "1")
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import paper_2112_15198_b200 as ifgf  # noqa: E402
+from paper_2112_15198_b200.dist import run_distributed  # noqa: E402
+
+c = ifgf.configs.CONFIGS[sys.argv[1] if len(sys.argv) > 1 else "C4"]
+R = int(sys.argv[2]) if len(sys.argv) > 2 else 8
+pc = ifgf.generate(c.n, c.shape, c.c, c.dens, c.seed)
+cfg = ifgf.KernelConfig(ifgf.KernelKind(c.kind), c.kappa)
+for name, mode in (("COUNT", 0), ("WORK", 1)):
+    best = None
+    for _ in range(2):
+        q = pc.copy()
+        _, infos = run_distributed(q, cfg, ifgf.EngineParams(depth=c.depth, partition=mode), R)
+        secs = [i.compute_seconds for i in infos]
+        best = secs if best is None or max(secs) < max(best) else best
+    mean = sum(best) / len(best)
+    print(f"{c.name} R={R} {name}: rank ms {[round(1e3 * v, 1) for v in best]} "
+          f"max/mean {max(best) / mean:.3f}  sum {1e3 * sum(best):.1f} ms", flush=True)
