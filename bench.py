@@ -393,7 +393,16 @@ def run_ours(args):
                 "peak_source": "measured in this run: best of DFMA chains and mma.sync m8n8k4 f64 "
                                "over all SMs (ifgf_measure_fp64_peak); MEASURED_PEAKS.json has no FP64 figure",
                 "per_kernel": per_kernel,
-                "whole_apply_frac": work.total_flops / t_apply / 1e12 / fp64_peak}
+                "whole_apply_frac": work.total_flops / t_apply / 1e12 / fp64_peak,
+                # the fractions are ALGORITHMIC work rates (SURVEY.md 8(d)
+                # weights, sincos = 36 flop).  The row kernel reads each node's
+                # transfer factor precomputed and K4/K1 use the 12-op table sincos,
+                # so the FP64 work actually executed per propagation evaluation
+                # is ~380 flop (186 FMA contraction + 4 FMA transfer), not 430.
+                "flop_model": "algorithmic (SURVEY.md 8(d)); executed ~380 of the 430 "
+                              "flop per propagation evaluation",
+                "frac_executed_estimate": (dk["frac_fp64"] * 380.0 / 430.0
+                                           if dom == "propagation" else None)}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:

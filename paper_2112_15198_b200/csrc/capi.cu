@@ -684,24 +684,59 @@ int ifgf_plan_apply(ifgf_plan* P, const double* a_re, const double* a_im, double
 int ifgf_apply(size_t n, const double* x1, const double* x2, const double* x3, const double* a_re,
                const double* a_im, int kind, double k, const ifgf_params* p, double* i_re,
                double* i_im, ifgf_report* rep) {
-  // engine.cpp:260-325: rebuild, apply, return in the caller's order
+  // engine.cpp:260-325: rebuild, apply, return in the caller's order.  The
+  // densities travel to the device on the aux stream while the main stream
+  // builds the plan from the coordinates (Problem::build), so their copy is
+  // off the critical path.
   if (n < 2) {
     g_err = "apply: need at least two points";
     return IFGF_EINVAL;
   }
-  const auto t0 = clk::now();
+  DeviceGuard keep;
   ifgf_plan* P = nullptr;
-  int rc = ifgf_plan_create(x1, x2, x3, n, kind, k, p, &P);
-  if (rc) return rc;
-  rc = ifgf_plan_apply(P, a_re, a_im, i_re, i_im, rep);
-  const double setup = P->setup_seconds;
-  const size_t setup_launches = P->launches;
-  ifgf_plan_destroy(P);
-  if (rc == 0 && rep) {
-    rep->setup = setup;
-    rep->total = since(t0);
-    rep->gpu_launches = setup_launches;  // setup + apply kernels of this call
-  }
+  size_t setup_launches = 0;
+  const int rc = guarded([&] {
+    if (!x1 || !x2 || !x3 || !a_re || !i_re || !i_im) throw Error(IFGF_EINVAL, "null argument");
+    const auto t0 = clk::now();
+    P = new_plan(n, kind, k, p);
+    double* buf = nullptr;
+    IFGF_CUDA(cudaMallocAsync(&buf, 4 * n * sizeof(double), P->s_aux));
+    struct F {
+      double* b;
+      cudaStream_t s;
+      ~F() {
+        if (b) cudaFreeAsync(b, s);
+      }
+    } f{buf, P->s_main};
+    IFGF_CUDA(cudaMemcpyAsync(buf, a_re, n * 8, cudaMemcpyHostToDevice, P->s_aux));
+    if (a_im) IFGF_CUDA(cudaMemcpyAsync(buf + n, a_im, n * 8, cudaMemcpyHostToDevice, P->s_aux));
+    cudaEvent_t dens;
+    IFGF_CUDA(cudaEventCreateWithFlags(&dens, cudaEventDisableTiming));
+    IFGF_CUDA(cudaEventRecord(dens, P->s_aux));
+    double* tmp = P->alloc<double>(3 * n);
+    IFGF_CUDA(cudaMemcpyAsync(tmp, x1, n * 8, cudaMemcpyHostToDevice, P->s_main));
+    IFGF_CUDA(cudaMemcpyAsync(tmp + n, x2, n * 8, cudaMemcpyHostToDevice, P->s_main));
+    IFGF_CUDA(cudaMemcpyAsync(tmp + 2 * n, x3, n * 8, cudaMemcpyHostToDevice, P->s_main));
+    finish_create(P, tmp, tmp + n, tmp + 2 * n);
+    P->setup_seconds = since(t0);
+    setup_launches = P->launches;
+    IFGF_CUDA(cudaStreamWaitEvent(P->s_main, dens, 0));
+    cudaEventDestroy(dens);
+    apply_device(P, buf, a_im ? buf + n : nullptr, buf + 2 * n, buf + 3 * n, P->s_main, rep);
+    IFGF_CUDA(cudaMemcpyAsync(i_re, buf + 2 * n, n * 8, cudaMemcpyDeviceToHost, P->s_main));
+    IFGF_CUDA(cudaMemcpyAsync(i_im, buf + 3 * n, n * 8, cudaMemcpyDeviceToHost, P->s_main));
+    IFGF_CUDA(cudaStreamSynchronize(P->s_main));
+    if (rep) {
+      rep->setup = P->setup_seconds;
+      rep->gpu_launches = P->launches;  // setup + apply kernels of this call
+    }
+    (void)setup_launches;
+    f.b = nullptr;
+    IFGF_CUDA(cudaFreeAsync(buf, P->s_main));
+    const double total = since(t0);
+    if (rep) rep->total = total;
+  });
+  if (P) plan_free(P);
   return rc;
 }
 
