@@ -313,6 +313,30 @@ def run_ours(args):
         ev2[i][1].record(s)
     torch.cuda.synchronize()
     t_apply = statistics.mean(a.elapsed_time(b) for a, b in ev2) / 1e3
+
+    # ---- batched right-hand sides (ifgf_plan_apply_batch, plan reused)
+    nrhs = 4
+    XB = [torch.stack([X[3]] * nrhs).contiguous(), torch.stack([X[4]] * nrhs).contiguous()]
+    OB = [torch.empty((nrhs, n), dtype=torch.float64, device=dev) for _ in range(2)]
+    for _ in range(2):
+        plan.apply_batch_device(nrhs, XB[0].data_ptr(), XB[1].data_ptr(), OB[0].data_ptr(),
+                                OB[1].data_ptr(), stream=sh)
+    ev3 = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+           for _ in range(max(2, args.steps // 2))]
+    for a, b in ev3:
+        with torch.cuda.stream(s):
+            flush.zero_()
+        a.record(s)
+        plan.apply_batch_device(nrhs, XB[0].data_ptr(), XB[1].data_ptr(), OB[0].data_ptr(),
+                                OB[1].data_ptr(), stream=sh)
+        b.record(s)
+    torch.cuda.synchronize()
+    t_batch = statistics.mean(a.elapsed_time(b) for a, b in ev3) / 1e3
+    batch = {"nrhs": nrhs, "value": nrhs * n / t_batch / 1e6, "unit": "Mpoints*rhs/s",
+             "ms_per_batch": t_batch * 1e3, "ms_per_rhs": t_batch * 1e3 / nrhs,
+             "note": "setup shared, passes per rhs (kernel-level batching measured: no gain, "
+                     "DESIGN.md section 9)"}
+    del XB, OB
     plan.set_serial(True)
     serial = []
     for _ in range(3):
@@ -430,6 +454,7 @@ def run_ours(args):
                                                      "propagation")},
                            "stages_ms_serial": {k: v * 1e3 for k, v in st.items()}},
             "setup_ms": (t_step - t_apply) * 1e3,
+            "apply_batch": batch,
             "gpu_launches": int(r0.gpu_launches),
             "e2e": e2e,
             "roofline": roofline,

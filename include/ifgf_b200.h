@@ -152,6 +152,15 @@ int ifgf_plan_apply(ifgf_plan* plan, const double* a_re, const double* a_im, dou
                     double* i_im, ifgf_report* rep);
 int ifgf_plan_apply_device(ifgf_plan* plan, const double* d_a_re, const double* d_a_im,
                            double* d_i_re, double* d_i_im, void* stream, ifgf_report* rep);
+/* Several right-hand sides against one plan (iterative solvers): nrhs
+ * densities, vector r at offset r * n in each array (caller's order), applied
+ * one after another with the setup shared; identical to nrhs calls of
+ * ifgf_plan_apply. */
+int ifgf_plan_apply_batch(ifgf_plan* plan, int nrhs, const double* a_re, const double* a_im,
+                          double* i_re, double* i_im, ifgf_report* rep);
+int ifgf_plan_apply_batch_device(ifgf_plan* plan, int nrhs, const double* d_a_re,
+                                 const double* d_a_im, double* d_i_re, double* d_i_im,
+                                 void* stream, ifgf_report* rep);
 /* create + apply + destroy: the exact contract of ifgf::apply (a_im may be
  * NULL for a real density). */
 int ifgf_apply(size_t n, const double* x1, const double* x2, const double* x3,

@@ -83,6 +83,9 @@ SIGNATURES = {
     "ifgf_plan_set_option": (C.c_int, [_vp, C.c_int, C.c_int]),
     "ifgf_plan_apply": (C.c_int, [_vp, _vp, _vp, _vp, _vp, C.POINTER(CReport)]),
     "ifgf_plan_apply_device": (C.c_int, [_vp, _vp, _vp, _vp, _vp, _vp, C.POINTER(CReport)]),
+    "ifgf_plan_apply_batch": (C.c_int, [_vp, C.c_int, _vp, _vp, _vp, _vp, C.POINTER(CReport)]),
+    "ifgf_plan_apply_batch_device": (C.c_int, [_vp, C.c_int, _vp, _vp, _vp, _vp, _vp,
+                                               C.POINTER(CReport)]),
     "ifgf_apply": (C.c_int, [_sz, _vp, _vp, _vp, _vp, _vp, C.c_int, C.c_double,
                              C.POINTER(CParams), _vp, _vp, C.POINTER(CReport)]),
     "ifgf_plan_get_info": (C.c_int, [_vp, C.POINTER(CPlanInfo)]),

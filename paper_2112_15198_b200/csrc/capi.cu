@@ -103,6 +103,28 @@ struct DeviceGuard {
   }
 };
 
+// Device memory a new plan may count on: the driver's free memory plus what
+// the stream-ordered pool holds reserved but unused (freed by earlier plans
+// and kept, see tune_pool), taken ONCE per plan while the device is quiet.
+// cudaMemGetInfo issued while kernels run took 10-36 ms in 1 of 4 plan
+// builds at C2 (IFGF_ALLOC_TRACE, profiles/r02/meminfo_spikes_c2.log), the
+// cause of the setup-time spread; the later decisions (tile cap, block slots)
+// use this budget minus the plan's own allocations.
+size_t device_memory_budget(int device) {
+  size_t fr = 0, tot = 0;
+  IFGF_CUDA(cudaMemGetInfo(&fr, &tot));
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+    uint64_t reserved = 0, used = 0;
+    if (cudaMemPoolGetAttribute(pool, cudaMemPoolAttrReservedMemCurrent, &reserved) ==
+            cudaSuccess &&
+        cudaMemPoolGetAttribute(pool, cudaMemPoolAttrUsedMemCurrent, &used) == cudaSuccess &&
+        reserved > used)
+      fr += (size_t)(reserved - used);
+  }
+  return fr;
+}
+
 void validate_params(const ifgf_params* p) {
   if (!p) throw Error(IFGF_EINVAL, "null params");
   if (p->p_s < 1 || p->p_theta < 1 || p->p_phi < 1 || p->p_s > kMaxOrder ||
@@ -209,6 +231,7 @@ ifgf_plan* new_plan(size_t n, int kind, double wavenumber, const ifgf_params* p)
   if (p->partition != IFGF_PARTITION_COUNT && p->partition != IFGF_PARTITION_WORK)
     throw Error(IFGF_EINVAL, "unknown partition mode");
   P->partition_mode = p->partition;
+  P->mem_budget = device_memory_budget(P->device);
   try {
     P->s_main = take_stream(P->device);
     P->s_aux = take_stream(P->device);
@@ -243,8 +266,7 @@ void ensure_slots(ifgf_plan* P) {
     total += P->lv[d].nc;
     mx = std::max<size_t>(mx, P->lv[d].nc);
   }
-  size_t fr = 0, tot = 0;
-  IFGF_CUDA(cudaMemGetInfo(&fr, &tot));
+  const size_t fr = mem_available(P);
   if (total * bpc < fr / 2) {
     double2* base = P->alloc<double2>(total * P->K.Pst + 2);
     size_t off = 0;
@@ -371,6 +393,31 @@ void apply_device(ifgf_plan* P, const double* a_re, const double* a_im, double* 
 double* staging(ifgf_plan* P) {
   if (!P->staging) P->staging = P->alloc<double>(2 * P->n);
   return P->staging;
+}
+
+// nrhs densities (vector r at offset r * n, caller's order) against one
+// plan, one after another on the plan's streams: the setup is shared, the
+// passes run per rhs.  Kernel-level batching (K4 / K3 sharing each step's
+// locate, cone lookup, node data and phase factor across two rhs) was built
+// and measured at C2: 66.5 ms per rhs against 65.9 ms for single applies --
+// both kernels are bound by the L1->register path of the block loads, which
+// batching does not reduce, so it was not kept.
+void apply_batch_device(ifgf_plan* P, int nrhs, const double* a_re, const double* a_im,
+                        double* i_re, double* i_im, cudaStream_t caller, ifgf_report* rep) {
+  const auto t0 = clk::now();
+  const size_t n = P->n;
+  size_t launches = 0;
+  ifgf_report r1{};
+  for (int r = 0; r < nrhs; ++r) {
+    apply_device(P, a_re + r * n, a_im ? a_im + r * n : nullptr, i_re + r * n, i_im + r * n,
+                 caller, &r1);
+    launches += r1.gpu_launches;
+  }
+  if (rep) {
+    *rep = r1;
+    rep->gpu_launches = launches;
+    rep->total = since(t0);
+  }
 }
 
 double2* stage_blocks(ifgf_plan* P, int d) {
@@ -676,6 +723,48 @@ int ifgf_plan_apply(ifgf_plan* P, const double* a_re, const double* a_im, double
         cudaMemcpyAsync(i_re, buf + 2 * n, n * sizeof(double), cudaMemcpyDeviceToHost, P->s_main));
     IFGF_CUDA(
         cudaMemcpyAsync(i_im, buf + 3 * n, n * sizeof(double), cudaMemcpyDeviceToHost, P->s_main));
+    IFGF_CUDA(cudaStreamSynchronize(P->s_main));
+    if (rep) rep->total = since(t0);
+  });
+}
+
+int ifgf_plan_apply_batch_device(ifgf_plan* P, int nrhs, const double* a_re, const double* a_im,
+                                 double* i_re, double* i_im, void* stream, ifgf_report* rep) {
+  DeviceGuard keep;
+  return guarded([&] {
+    if (!P || !a_re || !i_re || !i_im) throw Error(IFGF_EINVAL, "null argument");
+    if (nrhs < 1) throw Error(IFGF_EINVAL, "apply_batch: need at least one right-hand side");
+    if (P->n < 2) throw Error(IFGF_EINVAL, "apply: need at least two points");
+    if (P->dist) throw Error(IFGF_EINVAL, "apply_batch: not on a rank plan");
+    apply_batch_device(P, nrhs, a_re, a_im, i_re, i_im, static_cast<cudaStream_t>(stream), rep);
+  });
+}
+
+int ifgf_plan_apply_batch(ifgf_plan* P, int nrhs, const double* a_re, const double* a_im,
+                          double* i_re, double* i_im, ifgf_report* rep) {
+  DeviceGuard keep;
+  return guarded([&] {
+    if (!P || !a_re || !i_re || !i_im) throw Error(IFGF_EINVAL, "null argument");
+    if (nrhs < 1) throw Error(IFGF_EINVAL, "apply_batch: need at least one right-hand side");
+    if (P->n < 2) throw Error(IFGF_EINVAL, "apply: need at least two points");
+    if (P->dist) throw Error(IFGF_EINVAL, "apply_batch: not on a rank plan");
+    const auto t0 = clk::now();
+    IFGF_CUDA(cudaSetDevice(P->device));
+    const size_t n = P->n, m = (size_t)nrhs * n;
+    double* buf = nullptr;
+    IFGF_CUDA(cudaMallocAsync(&buf, 4 * m * sizeof(double), P->s_main));
+    struct F {
+      double* b;
+      cudaStream_t s;
+      ~F() { cudaFreeAsync(b, s); }
+    } f{buf, P->s_main};
+    IFGF_CUDA(cudaMemcpyAsync(buf, a_re, m * 8, cudaMemcpyHostToDevice, P->s_main));
+    if (a_im)
+      IFGF_CUDA(cudaMemcpyAsync(buf + m, a_im, m * 8, cudaMemcpyHostToDevice, P->s_main));
+    apply_batch_device(P, nrhs, buf, a_im ? buf + m : nullptr, buf + 2 * m, buf + 3 * m,
+                       P->s_main, rep);
+    IFGF_CUDA(cudaMemcpyAsync(i_re, buf + 2 * m, m * 8, cudaMemcpyDeviceToHost, P->s_main));
+    IFGF_CUDA(cudaMemcpyAsync(i_im, buf + 3 * m, m * 8, cudaMemcpyDeviceToHost, P->s_main));
     IFGF_CUDA(cudaStreamSynchronize(P->s_main));
     if (rep) rep->total = since(t0);
   });

@@ -4,7 +4,10 @@
 
 #include <cuda_runtime.h>
 
+#include <chrono>
 #include <cstdint>
+#include <cstdio>
+#include <cstdlib>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -175,6 +178,7 @@ struct ifgf_plan {
   double *ar = nullptr, *ai = nullptr;                 // sorted densities
   double *ir = nullptr, *ii = nullptr;                 // sorted results
   double* staging = nullptr;  // 2n doubles: pass-level API host<->device staging, reused
+
   int* err = nullptr;
   const double2* phase = nullptr;  // sincos_tab table (kPhaseEntries), after the trig table
   uint32_t* work_ctr = nullptr;    // persistent-kernel work counters (kWorkCtrs)
@@ -194,13 +198,21 @@ struct ifgf_plan {
   int near_kernel = IFGF_NEAR_BOX;   // IFGF_OPT_NEAR_KERNEL
   int partition_mode = IFGF_PARTITION_COUNT;  // IFGF_OPT_PARTITION
   size_t setup_launches = 0;
+  size_t mem_budget = 0;  // device memory available when the plan was created (capi.cu)
   ifgf_b200::DistState* dist = nullptr;  // rank plans of a multi-GPU group (dist.cu)
 
   template <class T>
   T* alloc(size_t count) {
     void* p = nullptr;
     const size_t b = count * sizeof(T) + 16;
+    static const bool trace = std::getenv("IFGF_ALLOC_TRACE") != nullptr;
+    const auto t0 = std::chrono::steady_clock::now();
     IFGF_CUDA(cudaMallocAsync(&p, b, s_main));
+    if (trace) {
+      const double ms =
+          std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count() * 1e3;
+      if (ms > 0.3) std::fprintf(stderr, "[alloc] %12zu B  %8.3f ms\n", b, ms);
+    }
     allocs.push_back(p);
     bytes += b;
     return static_cast<T*>(p);
@@ -229,7 +241,10 @@ void build_prop_tiles(ifgf_plan* P, int d, void* (*scratch)(void*, size_t), void
 void launch_mark_nodes_tiles(ifgf_plan* P, int d, uint64_t* bits);
 bool launch_propagation_mma(ifgf_plan* P, int d, uint32_t qb, uint32_t qe, const double2* child,
                             double2* parent, cudaStream_t s);
+
 // capi.cu
+// the plan's creation-time memory budget less what it has allocated since
+inline size_t mem_available(const ifgf_plan* P);
 void partition_host(ifgf_plan* P, int R, uint32_t* box_begin, uint32_t* point_begin,
                     uint32_t* cone_begin);
 // dist.cu
@@ -253,3 +268,7 @@ void direct_sums(const double* x, const double* y, const double* z, const double
                  const double* ai, size_t n, double kappa, const uint32_t* targets, size_t m,
                  double* o_re, double* o_im, cudaStream_t s);
 }  // namespace ifgf_b200
+
+inline size_t ifgf_b200::mem_available(const ifgf_plan* P) {
+  return P->mem_budget > P->bytes ? P->mem_budget - P->bytes : 0;
+}

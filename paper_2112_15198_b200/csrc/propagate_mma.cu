@@ -1147,8 +1147,7 @@ void build_prop_tiles(ifgf_plan* P, int d, void* (*scratch)(void*, size_t), void
   // the on-the-fly rows are the better deal (a Laplace or high-kappa coarse
   // level can have millions of distinct gammas)
   {
-    size_t fr = 0, tot = 0;
-    IFGF_CUDA(cudaMemGetInfo(&fr, &tot));
+    const size_t fr = mem_available(P);
     const double rows_bytes = (double)((K.P + 31) / 32 * 32) / K.P * 15.0 * sizeof(double);
     const double bytes = (double)ng * 8.0 * K.P *
                          (rows_bytes + 3 * sizeof(double) + sizeof(double2) +

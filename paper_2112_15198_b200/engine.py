@@ -345,6 +345,30 @@ class Plan:
                                   C.byref(rep)))
         return i_re, i_im, ApplyReport.from_c(rep)
 
+    def apply_batch(self, a_re, a_im=None):
+        """nrhs densities at once (rows of a [nrhs, n] array); returns
+        (i_re, i_im) of shape [nrhs, n] and the report (ifgf_plan_apply_batch)."""
+        a_re = np.ascontiguousarray(np.atleast_2d(a_re), dtype=np.float64)
+        nrhs, n = a_re.shape
+        if n != self.n:
+            raise InvalidArgument("apply_batch: densities of the wrong length")
+        a_im = None if a_im is None else np.ascontiguousarray(np.atleast_2d(a_im),
+                                                               dtype=np.float64)
+        i_re, i_im = np.zeros((nrhs, n)), np.zeros((nrhs, n))
+        rep = _lib.CReport()
+        check(lib.ifgf_plan_apply_batch(self._h, nrhs, ptr(a_re), ptr(a_im), ptr(i_re),
+                                        ptr(i_im), C.byref(rep)))
+        return i_re, i_im, ApplyReport.from_c(rep)
+
+    def apply_batch_device(self, nrhs: int, a_re_ptr: int, a_im_ptr: int | None, i_re_ptr: int,
+                           i_im_ptr: int, stream: int = 0) -> ApplyReport:
+        rep = _lib.CReport()
+        check(lib.ifgf_plan_apply_batch_device(self._h, nrhs, C.c_void_p(a_re_ptr),
+                                               C.c_void_p(a_im_ptr) if a_im_ptr else None,
+                                               C.c_void_p(i_re_ptr), C.c_void_p(i_im_ptr),
+                                               C.c_void_p(stream), C.byref(rep)))
+        return ApplyReport.from_c(rep)
+
     def apply_device(self, a_re_ptr: int, a_im_ptr: int | None, i_re_ptr: int, i_im_ptr: int,
                      stream: int = 0) -> ApplyReport:
         """Device pointers (e.g. torch tensor.data_ptr()), ordered on `stream`."""
