@@ -103,26 +103,48 @@ struct DeviceGuard {
   }
 };
 
-// Device memory a new plan may count on: the driver's free memory plus what
-// the stream-ordered pool holds reserved but unused (freed by earlier plans
-// and kept, see tune_pool), taken ONCE per plan while the device is quiet.
-// cudaMemGetInfo issued while kernels run took 10-36 ms in 1 of 4 plan
-// builds at C2 (IFGF_ALLOC_TRACE, profiles/r02/meminfo_spikes_c2.log), the
-// cause of the setup-time spread; the later decisions (tile cap, block slots)
-// use this budget minus the plan's own allocations.
+// Device memory a new plan may count on.  cudaMemGetInfo stalls for 10-78 ms
+// in a good fraction of calls while other driver clients are active (NCCL's
+// proxy thread, the NVML sampler; IFGF_ALLOC_TRACE,
+// profiles/r02/meminfo_spikes_c2.log), which was the whole setup-time
+// spread.  So it is sampled at most every 30 s per device; in between the
+// budget follows the stream-ordered pool's own counters (cheap attribute
+// reads): free memory at the sample, plus what the pool had reserved then,
+// minus what the pool has in use now.  Allocations by other allocators
+// after the sample are not seen, so the block-storage decision also
+// recovers from an out-of-memory by falling back to two rotating slots.
 size_t device_memory_budget(int device) {
-  size_t fr = 0, tot = 0;
-  IFGF_CUDA(cudaMemGetInfo(&fr, &tot));
-  cudaMemPool_t pool;
-  if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
-    uint64_t reserved = 0, used = 0;
-    if (cudaMemPoolGetAttribute(pool, cudaMemPoolAttrReservedMemCurrent, &reserved) ==
-            cudaSuccess &&
-        cudaMemPoolGetAttribute(pool, cudaMemPoolAttrUsedMemCurrent, &used) == cudaSuccess &&
-        reserved > used)
-      fr += (size_t)(reserved - used);
+  struct Sample {
+    bool valid = false;
+    size_t free = 0;
+    uint64_t reserved = 0;
+    clk::time_point when;
+  };
+  static std::mutex mu;
+  static Sample cache[64];
+  auto pool_counters = [&](uint64_t& reserved, uint64_t& used) {
+    reserved = used = 0;
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+      cudaMemPoolGetAttribute(pool, cudaMemPoolAttrReservedMemCurrent, &reserved);
+      cudaMemPoolGetAttribute(pool, cudaMemPoolAttrUsedMemCurrent, &used);
+    }
+  };
+  std::lock_guard<std::mutex> g(mu);
+  Sample& c = cache[device >= 0 && device < 64 ? device : 0];
+  uint64_t reserved = 0, used = 0;
+  if (!c.valid || since(c.when) > 30.0) {
+    static const bool trace = std::getenv("IFGF_ALLOC_TRACE") != nullptr;
+    const auto t0 = clk::now();
+    size_t fr = 0, tot = 0;
+    IFGF_CUDA(cudaMemGetInfo(&fr, &tot));
+    if (trace) std::fprintf(stderr, "[meminfo] %8.3f ms\n", since(t0) * 1e3);
+    pool_counters(reserved, used);
+    c = {true, fr, reserved, clk::now()};
   }
-  return fr;
+  pool_counters(reserved, used);
+  const uint64_t have = (uint64_t)c.free + c.reserved;
+  return have > used ? (size_t)(have - used) : 0;
 }
 
 void validate_params(const ifgf_params* p) {
@@ -267,8 +289,21 @@ void ensure_slots(ifgf_plan* P) {
     mx = std::max<size_t>(mx, P->lv[d].nc);
   }
   const size_t fr = mem_available(P);
+  double2* base = nullptr;
   if (total * bpc < fr / 2) {
-    double2* base = P->alloc<double2>(total * P->K.Pst + 2);
+    // one slot per level; an out-of-memory (memory taken by other allocators
+    // since the budget's sample) falls back to the two rotating slots
+    void* p = nullptr;
+    const size_t b = (total * P->K.Pst + 2) * sizeof(double2) + 16;
+    if (cudaMallocAsync(&p, b, P->s_main) == cudaSuccess) {
+      P->allocs.push_back(p);
+      P->bytes += b;
+      base = static_cast<double2*>(p);
+    } else {
+      cudaGetLastError();
+    }
+  }
+  if (base) {
     size_t off = 0;
     for (int d = 3; d <= D; ++d) {
       P->slots[d] = base + off * P->K.Pst;

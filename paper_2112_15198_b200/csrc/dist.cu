@@ -43,6 +43,7 @@
 
 #include <algorithm>
 #include <chrono>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <memory>
@@ -276,6 +277,17 @@ T* dalloc(ifgf_plan* P, size_t n) {
 // ------------------------------------------------------------------ building
 // Phase 1 (every rank alone): layout, need sets, halo, local bitmaps, storage.
 void dist_prepare(ifgf_plan* P, int R, int rank) {
+  static const bool trace = std::getenv("IFGF_ALLOC_TRACE") != nullptr;
+  const auto tp0 = std::chrono::steady_clock::now();
+  struct TraceEnd {
+    bool on;
+    std::chrono::steady_clock::time_point t0;
+    ~TraceEnd() {
+      if (on)
+        std::fprintf(stderr, "[dist_prepare] %8.3f ms\n",
+                     std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count() * 1e3);
+    }
+  } trace_end{trace, tp0};
   auto* S = new DistState;
   P->dist = S;
   S->rank = rank;
