@@ -428,6 +428,30 @@ def run_ours(args):
                 "frac_executed_estimate": (dk["frac_fp64"] * 380.0 / 430.0
                                            if dom == "propagation" else None)}
 
+    # ---- setup (Problem::build) against the HBM roofline.
+    # Algorithmic bytes: coordinates read for the bounding
+    # cube (24 N), Morton keys (36 N), two sort passes (48 N), the sorted
+    # gather (52 N), per level the points' box ordinals and coordinates read
+    # once by the clause-1 marking (28 N per level), and 2 x 8 B per relevant
+    # cone for the bitmap compaction.  The setup is bound by the clause-1
+    # locates (one per (point, cousin box) and level, the same count as K4's
+    # evaluations), not by HBM: this fraction documents that.
+    t_setup = max(t_step - t_apply, 1e-9)
+    hbm_peak = None
+    try:
+        hbm_peak = float(json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"])
+    except Exception:
+        hbm_peak = 6525.6  # B200_PROFILING.md fallback
+    n_cones = sum(info.cones[d] for d in range(3, info.depth + 1))
+    setup_bytes = (24 + 36 + 48 + 52 + 28 * info.depth) * n + 16 * n_cones
+    setup_roofline = {"bound": "locate compute (clause-1 marking)", "ms": t_setup * 1e3,
+                      "algorithmic_bytes": setup_bytes,
+                      "achieved_GBps": setup_bytes / t_setup / 1e9, "peak_GBps": hbm_peak,
+                      "frac_hbm": setup_bytes / t_setup / 1e9 / hbm_peak,
+                      "clause1_locates": int(sum(work.interp_evals.values())),
+                      "clause1_locates_per_s": sum(work.interp_evals.values()) / t_setup,
+                      "peak_source": "MEASURED_PEAKS.json hbm_gbs"}
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cn, ct, kind, cores, sample = cpu_sample_run(1, 0)
@@ -454,6 +478,7 @@ def run_ours(args):
                                                      "propagation")},
                            "stages_ms_serial": {k: v * 1e3 for k, v in st.items()}},
             "setup_ms": (t_step - t_apply) * 1e3,
+            "setup_roofline": setup_roofline,
             "apply_batch": batch,
             "gpu_launches": int(r0.gpu_launches),
             "e2e": e2e,

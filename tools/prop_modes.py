@@ -1,7 +1,7 @@
 """Time the K3 propagation kernels on one config (serial stage timing) and
 check they agree.
 
-usage: python tools/prop_modes.py C2 [node tiles dmma rows]
+usage: python tools/prop_modes.py C2 [node dmma rows fly]
 """
 import os
 import sys
@@ -11,7 +11,7 @@ import numpy as np
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import paper_2112_15198_b200 as ifgf  # noqa: E402
 
-KINDS = {"node": 0, "tiles": 1, "dmma": 2, "rows": 3, "fly": 4, "stream": 5, "pipe": 6}
+KINDS = {"node": 0, "dmma": 2, "rows": 3, "fly": 4}
 c = ifgf.configs.CONFIGS[sys.argv[1]]
 modes = sys.argv[2:] or list(KINDS)
 pc = ifgf.generate(c.n, c.shape, c.c, c.dens, c.seed)
