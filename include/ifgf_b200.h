@@ -105,7 +105,7 @@ void ifgf_plan_destroy(ifgf_plan* plan);
  * IFGF_OPT_PROP_KERNEL selects the propagation kernel:
  *   IFGF_PROP_NODE  (0) thread per (parent cone, node), locate per child
  *                       (the generic path: any orders);
- *   IFGF_PROP_DMMA  (2) box-batched FP64 tensor-core GEMM: up to 64 parent
+ *   IFGF_PROP_DMMA  (2) box-batched FP64 tensor-core GEMM: up to 32 parent
  *                       cones sharing gamma per CTA, mma.sync.m8n8k4.f64 with
  *                       the node basis held in registers (whole levels only;
  *                       ranges and levels without the precomputed geometry

@@ -154,7 +154,7 @@ struct PropTiles {
   double* rdat = nullptr;       // row data (ts, tt, tp, tr, ti per slot), 32-row chunks,
                                 // SoA inside (propagate_mma.cu row_field)
   uint32_t* rnode = nullptr;    // per row (tile * P + r): node of slot j in byte j
-  // IFGF_PROP_DMMA CTA chunks of <= 64 parent cones sharing one gamma
+  // IFGF_PROP_DMMA CTA chunks of <= kG3Cones (32) parent cones sharing one gamma
   uint32_t nchunks = 0;
   uint32_t box_group = 0;  // parent boxes per chunk group (IFGF_PROP_DMMA)
   uint32_t* qsorted = nullptr;

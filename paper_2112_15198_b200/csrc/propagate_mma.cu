@@ -14,7 +14,7 @@
 //     recomputed per box with the reference's exact formulas),
 //   * the nodes grouped by gamma_c into row tiles of 8.
 // k_propagate_rows evaluates rows of <= 3 nodes sharing a child cone per
-// block load; k_propagate_gemm (IFGF_PROP_DMMA) batches up to 64 parent cones
+// block load; k_propagate_gemm (IFGF_PROP_DMMA) batches up to 32 parent cones
 // that share gamma and computes V[node][cone] = sum_k B_k(t_node) *
 // C_{child cone}[k] with mma.sync.m8n8k4.f64.  Same result up to rounding.
 #include <cub/cub.cuh>
@@ -471,11 +471,13 @@ __host__ __device__ __forceinline__ int gemm_koff(int st, int k, int& ks, int& k
 // dmma_peak.cu: mixed time = sum), so the gain is bandwidth and issue, not
 // peak.  Flagged nodes take the exact per-box path; cones are fitted per
 // warp at the end of the chunk.
+// 4 warps x 32 cones per CTA measured best among 2-8 warps x 16-64 cones
+// (profiles/r02/g3_sweep.log)
 #ifndef IFGF_G3_WARPS
-#define IFGF_G3_WARPS 8
+#define IFGF_G3_WARPS 4
 #endif
 #ifndef IFGF_G3_CONES
-#define IFGF_G3_CONES 64
+#define IFGF_G3_CONES 32
 #endif
 constexpr int kG3Warps = IFGF_G3_WARPS;
 constexpr int kG3Cones = IFGF_G3_CONES;  // parent cones per chunk (8 per column tile)
