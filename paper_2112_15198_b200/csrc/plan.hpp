@@ -159,6 +159,14 @@ struct PropTiles {
   uint32_t box_group = 0;  // parent boxes per chunk group (IFGF_PROP_DMMA)
   uint32_t* qsorted = nullptr;
   uint32_t* chunk_start = nullptr;
+  // warp GEMM (k_propagate_wgemm): per row tile and node slot one record of
+  // node data; parent cones sorted by (box group, gamma, child mask) and cut
+  // into warp units of <= 8 * kG4Nct cones sharing (group, gamma, mask)
+  char* rtab = nullptr;
+  uint32_t nunits = 0;
+  uint32_t* usorted = nullptr;
+  uint32_t* unit_start = nullptr;
+  double2* zblock = nullptr;   // one zero block (absent children's B operand)
 };
 
 }  // namespace ifgf_b200

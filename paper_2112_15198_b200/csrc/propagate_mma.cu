@@ -68,12 +68,14 @@ struct TilesDev {
   const uint2* rw;
   const double* rdat;
   const uint32_t* rnode;
+  const uint32_t* usorted;
+  const uint32_t* unit_start;
 };
 
 TilesDev tiles_dev(const PropTiles& t) {
   return {t.ngamma,   t.cone_gidx,   t.gamma_of, t.e_t,    t.e_T,  t.e_gc, t.rt_off,
           t.rt,       t.fl_cnt,      t.fl_node,  t.qsorted, t.chunk_start, t.e_perm,
-          t.rw_cnt,   t.rw,          t.rdat,     t.rnode};
+          t.rw_cnt,   t.rw,          t.rdat,     t.rnode,   t.usorted, t.unit_start};
 }
 
 inline unsigned nblk(size_t n, int t = 256) { return (unsigned)((n + t - 1) / t); }
@@ -161,7 +163,8 @@ __global__ void k_tile_entries(const __grid_constant__ LevelDev U, const __grid_
 // node order) into row tiles of 8; list flagged nodes.  Pass 1 counts.
 __global__ void k_tile_rows(uint32_t ntiles, int P, const uint32_t* e_gc, uint32_t* rt_cnt,
                             uint32_t* fl_cnt, const uint32_t* rt_off, uint4* rt,
-                            const uint32_t* fl_off, uint16_t* fl_node, uint8_t* e_perm) {
+                            const uint32_t* fl_off, uint16_t* fl_node, uint8_t* e_perm,
+                            uint32_t* rt_tile = nullptr) {
   uint32_t wp = 0;
   const uint32_t tile = blockIdx.x * blockDim.x + threadIdx.x;
   if (tile >= ntiles) return;
@@ -195,6 +198,7 @@ __global__ void k_tile_rows(uint32_t ntiles, int P, const uint32_t* e_gc, uint32
       if (k < 4) R.y = (R.y & ~(0xffu << sh)) | ((uint32_t)m << sh);
       else R.z = (R.z & ~(0xffu << sh)) | ((uint32_t)m << sh);
       if (++k == 8) {
+        if (rt_tile) rt_tile[wr] = tile;
         if (rt) rt[wr++] = R;
         ++nrt;
         R = make_uint4(cur, 0xffffffffu, 0xffffffffu, 0);
@@ -202,6 +206,7 @@ __global__ void k_tile_rows(uint32_t ntiles, int P, const uint32_t* e_gc, uint32
       }
     }
     if (k) {
+      if (rt_tile) rt_tile[wr] = tile;
       if (rt) rt[wr++] = R;
       ++nrt;
     }
@@ -344,7 +349,8 @@ __global__ void k_gemm_keys(const __grid_constant__ LevelDev U, const uint32_t* 
   qidx[q] = q;
 }
 
-__global__ void k_chunk_flags(const uint64_t* gsorted, uint32_t n, uint32_t chunk, uint32_t* flag) {
+__global__ void k_chunk_flags(const uint64_t* gsorted, uint32_t n, uint32_t chunk, uint32_t* flag,
+                              int shift = 0) {
   const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i > n) return;
   if (i == n) {
@@ -353,10 +359,10 @@ __global__ void k_chunk_flags(const uint64_t* gsorted, uint32_t n, uint32_t chun
   }
   // chunk starts: every chunk-th element of each run of equal gamma index
   uint32_t lo = 0, hi = i;
-  const uint64_t g = gsorted[i];
+  const uint64_t g = gsorted[i] >> shift;
   while (lo < hi) {  // run start = lower_bound(g)
     const uint32_t mid = (lo + hi) >> 1;
-    if (gsorted[mid] < g) lo = mid + 1;
+    if ((gsorted[mid] >> shift) < g) lo = mid + 1;
     else hi = mid;
   }
   flag[i] = ((i - lo) % chunk == 0) ? 1u : 0u;
@@ -367,6 +373,53 @@ __global__ void k_chunk_starts(const uint32_t* flag, const uint32_t* pos, uint32
   const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n && flag[i]) chunk_start[pos[i]] = i;
   if (i == 0) chunk_start[nchunks] = n;
+}
+
+
+// Warp-GEMM keys: (box group, gamma index, child-octant mask).  Sorting by the
+// mask inside a (group, gamma) run puts cones whose boxes have the same
+// children next to each other, so the 8 columns of an MMA column tile mostly
+// share their present octants.
+__global__ void k_wgemm_keys(const __grid_constant__ LevelDev U, const __grid_constant__ LevelDev L,
+                             const uint32_t* __restrict__ gidx, uint32_t ngamma,
+                             uint32_t box_group, uint64_t* key, uint32_t* qidx) {
+  const uint32_t q = blockIdx.x * blockDim.x + threadIdx.x;
+  if (q >= U.nc) return;
+  const uint32_t pb = U.cone_box[q];
+  uint32_t mask = 0;
+  for (uint32_t cb = U.child_begin[pb]; cb < U.child_begin[pb + 1]; ++cb)
+    mask |= 1u << (uint32_t)(L.code[cb] & 7);
+  key[q] = (((uint64_t)(pb / box_group) * ngamma + gidx[q]) << 8) | mask;
+  qidx[q] = q;
+}
+
+// Per row tile and node slot: the node's local coordinates in its child cone,
+// its re-centring factor and its index (-1: empty slot) in one 48-byte
+// record, so the warp GEMM reads a row tile's node data with one dependent
+// load instead of three.
+struct WgRow {
+  double ts, tt, tp, tfx, tfy;
+  long long m;
+};
+
+__global__ void k_wgemm_rtab(uint32_t nrt, int P, const uint4* __restrict__ rt,
+                             const uint32_t* __restrict__ rt_tile, const double* __restrict__ e_t,
+                             const double2* __restrict__ e_T, WgRow* __restrict__ rtab) {
+  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= nrt * 8) return;
+  const uint32_t r = i >> 3;
+  const int m = rt_node(rt[r], (int)(i & 7));
+  WgRow w = {0.0, 0.0, 0.0, 0.0, 0.0, -1};
+  if (m != 0xff) {
+    const size_t e = (size_t)rt_tile[r] * P + m;
+    w.ts = e_t[3 * e];
+    w.tt = e_t[3 * e + 1];
+    w.tp = e_t[3 * e + 2];
+    w.tfx = e_T[e].x;
+    w.tfy = e_T[e].y;
+    w.m = m;
+  }
+  rtab[i] = w;
 }
 
 // Clause 2 of compute_relevant_cones (cones.cpp:108-119) from the tiles: a
@@ -713,6 +766,298 @@ __global__ void __launch_bounds__(kG3Warps * 32, 16 / kG3Warps)
       __syncwarp();
     }
     __syncthreads();
+  }
+}
+
+// ---------------------------------------------------------------- K3 v4
+// Warp GEMM.  A warp owns a unit of <= 8 * kG4Nct parent cones that share
+// gamma (and the octants of their children) from start to finish: node values
+// in its own shared-memory accumulator, children in Morton order, then the
+// fit.  No CTA barriers and no work shared between warps, so a warp's stalls
+// are its own.  Per child octant and row tile (<= 8 nodes sharing a child
+// cone):
+//   V[node][cone] = sum_k A[node][k] C_{cone's child, gamma_c}[k]
+// with mma.sync.m8n8k4.f64.  K runs over the child block in memory order, 8
+// coefficients per chunk: one 256-bit load per lane brings two complex
+// coefficients (a quad covers 128 contiguous bytes of one block, so a warp's
+// load touches 8 lines for 1 KB -- the 128-bit version touched 8 lines for
+// 512 B and was bound by L1 wavefronts), feeding four MMAs (2 K steps x re,
+// im).  The loads run kPF chunks ahead in a register ring that continues into
+// the next row tile.  A (basis products of the lane's node at its own 2
+// coefficients per chunk) is formed in registers per row tile: the 25
+// theta-phi products once, then a 4-way select by the lane's position in the
+// quad -- no table, no memory traffic.
+#ifndef IFGF_G4_WARPS
+#define IFGF_G4_WARPS 8
+#endif
+#ifndef IFGF_G4_NCT
+#define IFGF_G4_NCT 2
+#endif
+constexpr int kG4Warps = IFGF_G4_WARPS;
+constexpr int kG4Nct = IFGF_G4_NCT;       // column tiles (of 8 cones) per warp unit
+constexpr int kG4Cones = 8 * kG4Nct;
+constexpr int kG4Batch = 16;              // row tiles whose child cones are resolved at once
+
+constexpr int g4_prefetch(int nch) {
+  for (int pf = 6; pf > 1; --pf)
+    if (nch % pf == 0) return pf;
+  return 1;
+}
+
+template <int PS, int PT, int PP>
+struct G4Shape {
+  static constexpr int P = PS * PT * PP;
+  static constexpr size_t per_warp = ((size_t)kG4Cones + 1) * P * sizeof(double2);
+  static constexpr int warps = kG4Warps;
+  static constexpr bool ok = P <= 80;  // A fragments and the load ring in registers
+};
+
+// a if p else b, as a select (the compiler turns ?: chains of doubles into
+// divergent branches)
+__device__ __forceinline__ double selp_f64(double a, double b, int p) {
+  double d;
+  asm("{\n\t.reg .pred q;\n\tsetp.ne.s32 q, %3, 0;\n\tselp.f64 %0, %1, %2, q;\n\t}"
+      : "=d"(d)
+      : "d"(a), "d"(b), "r"(p));
+  return d;
+}
+__device__ __forceinline__ double sel4(int kq, double a, double b, double c, double d) {
+  return selp_f64(a, selp_f64(b, selp_f64(c, d, kq == 2), kq == 1), kq == 0);
+}
+
+template <int PS, int PT, int PP, bool LAP>
+__global__ void __launch_bounds__(kG4Warps * 32, 1)
+    k_propagate_wgemm(const __grid_constant__ LevelDev U, const __grid_constant__ LevelDev L,
+                      const __grid_constant__ InterpConsts K, const TilesDev T,
+                      const WgRow* __restrict__ rtab, double kappa, uint32_t nunits,
+                      const double2* __restrict__ child, const double2* __restrict__ zblock,
+                      double2* parent, int* err) {
+  using BL = BlockLayout<PS, PT, PP>;
+  constexpr int P = PS * PT * PP, NCH = (BL::Pst + 7) / 8, PF = g4_prefetch(NCH);
+  constexpr bool kTail = (BL::Pst % 8) != 0;  // last chunk reaches past the block
+  extern __shared__ double2 smem[];
+  __shared__ double sM[PP * PP + PT * PT + PS * PS];
+  __shared__ uint32_t s_q[kG4Warps][kG4Cones];
+  __shared__ uint32_t s_cb[kG4Warps][8][kG4Cones];   // child box per octant (kNone: absent)
+  __shared__ uint32_t s_cq[kG4Warps][kG4Batch][kG4Cones];
+  stage_fit_matrices<PS, PT, PP>(K, sM);
+  __syncthreads();
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, NW = blockDim.x >> 5;
+  const int kq = lane & 3, nn = lane >> 2;
+  double2* acc = smem + (size_t)w * (kG4Cones + 1) * P;  // [kG4Cones][P] node values
+  double2* scr = acc + (size_t)kG4Cones * P;              // fit scratch, one cone
+  // chunk cc of the block at p (already offset by the lane's 2 kq coefficients)
+  auto bload = [&](const double2* p, int cc) -> double4 {
+    if (kTail && cc == NCH - 1) {
+      double4 b = make_double4(0.0, 0.0, 0.0, 0.0);
+      if (8 * cc + 2 * kq < BL::Pst) b = ldg256(p + 8 * cc);
+      return b;
+    }
+    return ldg256(p + 8 * cc);
+  };
+  for (uint32_t unit = blockIdx.x * NW + w; unit < nunits; unit += gridDim.x * NW) {
+    const uint32_t c0 = T.unit_start[unit], c1 = T.unit_start[unit + 1];
+    const int nq = (int)(c1 - c0);
+    for (int i = lane; i < kG4Cones * P; i += 32) acc[i] = make_double2(0.0, 0.0);
+    uint32_t omask = 0;
+    if (lane < kG4Cones) {
+      const uint32_t q = lane < nq ? T.usorted[c0 + lane] : kNone;
+      s_q[w][lane] = q;
+      uint32_t cbo[8];
+#pragma unroll
+      for (int o = 0; o < 8; ++o) cbo[o] = kNone;
+      if (q != kNone) {
+        const uint32_t pb = U.cone_box[q];
+        for (uint32_t cb = U.child_begin[pb]; cb < U.child_begin[pb + 1]; ++cb) {
+          const int o = (int)(L.code[cb] & 7);
+          omask |= 1u << o;
+#pragma unroll
+          for (int oo = 0; oo < 8; ++oo)
+            if (oo == o) cbo[oo] = cb;
+        }
+      }
+#pragma unroll
+      for (int o = 0; o < 8; ++o) s_cb[w][o][lane] = cbo[o];
+    }
+    omask = __reduce_or_sync(0xffffffffu, omask);
+    const uint32_t gi = T.cone_gidx[T.usorted[c0]];
+    __syncwarp();
+    for (int o = 0; o < 8; ++o) {
+      if (!((omask >> o) & 1u)) continue;  // warp-uniform
+      const uint32_t tile = gi * 8 + (uint32_t)o;
+      const uint32_t r0 = T.rt_off[tile], r1 = T.rt_off[tile + 1];
+      // column tiles with a child in this octant (cones are sorted by child
+      // mask, so a tile's 8 cones mostly agree)
+      const uint32_t has =
+          __ballot_sync(0xffffffffu, lane < kG4Cones && s_cb[w][o][lane < kG4Cones ? lane : 0] != kNone);
+      // NU column tiles from tile ub on, row tiles [rb, rb + nb)
+      auto run_batch = [&](auto NUc, int ub, uint32_t rb, int nb) {
+        constexpr int NU = decltype(NUc)::value;
+        WgRow rec = rtab[(size_t)rb * 8 + nn];
+        const double2* bp[NU];
+        double4 bq[PF][NU];
+#pragma unroll
+        for (int u = 0; u < NU; ++u) {
+          const uint32_t cq = s_cq[w][0][(ub + u) * 8 + nn];  // this lane's B column cone
+          bp[u] = (cq == kNone ? zblock : child + (size_t)cq * BL::Pst) + 2 * kq;
+        }
+#pragma unroll
+        for (int c = 0; c < PF; ++c)
+#pragma unroll
+          for (int u = 0; u < NU; ++u) bq[c][u] = bload(bp[u], c);
+        for (int rl = 0; rl < nb; ++rl) {
+          // the next row tile's node record and block pointers (the last row
+          // tile prefetches the zero block)
+          const bool more = rl + 1 < nb;
+          const WgRow recn = rtab[((size_t)rb + (more ? rl + 1 : rl)) * 8 + nn];
+          const double2* bpn[NU];
+#pragma unroll
+          for (int u = 0; u < NU; ++u) {
+            const uint32_t cq = more ? s_cq[w][rl + 1][(ub + u) * 8 + nn] : kNone;
+            bpn[u] = (cq == kNone ? zblock : child + (size_t)cq * BL::Pst) + 2 * kq;
+          }
+          // basis of this lane's node: Ts and the theta-phi products
+          double Ts[PS], WP[PT * PP];
+          {
+            double Tt[PT], Tp[PP];
+            cheb_basis<PS>(rec.ts, Ts);
+            cheb_basis<PT>(rec.tt, Tt);
+            cheb_basis<PP>(rec.tp, Tp);
+            if (rec.m < 0) {
+#pragma unroll
+              for (int k2 = 0; k2 < PS; ++k2) Ts[k2] = 0.0;
+            }
+#pragma unroll
+            for (int t = 0; t < PT; ++t)
+#pragma unroll
+              for (int p2 = 0; p2 < PP; ++p2) WP[t * PP + p2] = Tt[t] * Tp[p2];
+          }
+          double dr[NU][2], di[NU][2];
+#pragma unroll
+          for (int u = 0; u < NU; ++u) dr[u][0] = dr[u][1] = di[u][0] = di[u][1] = 0.0;
+#pragma unroll
+          for (int c = 0; c < NCH; ++c) {
+            // A fragments of the chunk: the lane's two coefficients
+            double a[2];
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+              double wv[4], sv[4];
+#pragma unroll
+              for (int k2 = 0; k2 < 4; ++k2) {
+                const int e = 8 * c + 2 * k2 + h;
+                const bool real = e < BL::Pst && e % BL::PL < PT * PP;
+                wv[k2] = real ? WP[real ? e % BL::PL : 0] : 0.0;
+                sv[k2] = real ? Ts[real ? e / BL::PL : 0] : 0.0;
+              }
+              a[h] = sel4(kq, sv[0], sv[1], sv[2], sv[3]) * sel4(kq, wv[0], wv[1], wv[2], wv[3]);
+            }
+            double4 b[NU];
+#pragma unroll
+            for (int u = 0; u < NU; ++u) b[u] = bq[c % PF][u];
+#pragma unroll
+            for (int u = 0; u < NU; ++u) {
+              dmma(dr[u][0], dr[u][1], a[0], b[u].x);
+              dmma(di[u][0], di[u][1], a[0], b[u].y);
+            }
+#pragma unroll
+            for (int u = 0; u < NU; ++u) {
+              dmma(dr[u][0], dr[u][1], a[1], b[u].z);
+              dmma(di[u][0], di[u][1], a[1], b[u].w);
+              bq[c % PF][u] = c + PF < NCH ? bload(bp[u], c + PF) : bload(bpn[u], c + PF - NCH);
+            }
+          }
+          // epilogue: D row nn = node m, columns 2 kq + h = cones of the tile
+          if (rec.m >= 0) {
+            const int m = (int)rec.m;
+#pragma unroll
+            for (int u = 0; u < NU; ++u)
+#pragma unroll
+              for (int h = 0; h < 2; ++h) {
+                const double vr = dr[u][h], vi = di[u][h];
+                double2* p = acc + (size_t)((ub + u) * 8 + 2 * kq + h) * P + m;
+                double2 v = *p;
+                if (LAP) {
+                  v.x = fma(vr, rec.tfx, v.x);
+                  v.y = fma(vi, rec.tfx, v.y);
+                } else {
+                  v.x = fma(vr, rec.tfx, fma(-vi, rec.tfy, v.x));
+                  v.y = fma(vr, rec.tfy, fma(vi, rec.tfx, v.y));
+                }
+                *p = v;
+              }
+          }
+          rec = recn;
+#pragma unroll
+          for (int u = 0; u < NU; ++u) bp[u] = bpn[u];
+        }
+      };
+      for (uint32_t rb = r0; rb < r1; rb += kG4Batch) {
+        const int nb = (int)min((uint32_t)kG4Batch, r1 - rb);
+        // child cone of every (row tile, cone) of the batch: independent
+        // lookups across lanes
+        for (int i = lane; i < nb * kG4Cones; i += 32) {
+          const int rl = i / kG4Cones, j = i % kG4Cones;
+          const uint32_t cb = s_cb[w][o][j];
+          uint32_t cq = kNone;
+          if (cb != kNone) {
+            cq = find_cone(L, cb, __ldg(&T.rt[rb + rl].x));
+            if (cq == kNone) raise_err(err, kErrPropCover);
+          }
+          s_cq[w][rl][j] = cq;
+        }
+        __syncwarp();
+        if (kG4Nct == 2) {
+          if ((has & 0xffu) && (has & 0xff00u)) run_batch(std::integral_constant<int, kG4Nct>{}, 0, rb, nb);
+          else run_batch(std::integral_constant<int, 1>{}, (has & 0xffu) ? 0 : 1, rb, nb);
+        } else {
+          run_batch(std::integral_constant<int, kG4Nct>{}, 0, rb, nb);
+        }
+        __syncwarp();  // s_cq readers done before the next batch
+      }
+      // flagged nodes: per-box exact locate + evaluation (rare)
+      const size_t f0 = (size_t)tile * P;
+      const uint32_t nfl = T.fl_cnt[tile];
+      for (uint32_t i = lane; i < nfl * (uint32_t)kG4Cones; i += 32) {
+        const int c = (int)(i % kG4Cones);
+        const uint32_t cb = s_cb[w][o][c];
+        if (cb == kNone) continue;
+        const int m = T.fl_node[f0 + i / kG4Cones];
+        const uint32_t q = s_q[w][c], pb = U.cone_box[q];
+        const int jp = m % PP, jt = (m / PP) % PT, js = m / (PP * PT);
+        const SegMid sg = segment_mid(U, U.cone_gamma[q]);
+        const double pcx = U.cx[pb], pcy = U.cy[pb], pcz = U.cz[pb];
+        double x, y, z;
+        node_position(sg, U.rad, pcx, pcy, pcz, K.ns[js], K.nt[jt], K.np[jp], x, y, z);
+        const double ux = x - pcx, uy = y - pcy, uz = z - pcz;
+        const double rp = sqrt(fma(uz, uz, fma(uy, uy, ux * ux)));
+        Loc lo;
+        const int e = locate_fast(L, L.cx[cb], L.cy[cb], L.cz[cb], x, y, z, lo);
+        if (e) {
+          raise_err(err, e);
+          continue;
+        }
+        const uint32_t cq = find_cone(L, cb, lo.gamma);
+        if (cq == kNone) {
+          raise_err(err, kErrPropCover);
+          continue;
+        }
+        double vr, vi;
+        eval_block<PS, PT, PP>(child + (size_t)cq * BL::Pst, lo.ts, lo.tt, lo.tp, vr, vi);
+        const double ratio = rp * lo.rinv;
+        double sn = 0.0, cn = 1.0;
+        if (!LAP) sincos_fast(kappa * (lo.r - rp), sn, cn);
+        const double tr = ratio * cn, ti = ratio * sn;
+        double2 v = acc[(size_t)c * P + m];
+        v.x = fma(vr, tr, fma(-vi, ti, v.x));
+        v.y = fma(vr, ti, fma(vi, tr, v.y));
+        acc[(size_t)c * P + m] = v;
+      }
+      __syncwarp();  // the next octant's row tiles touch the same (cone, node) slots
+    }
+    for (int c = 0; c < nq; ++c) {
+      fit_cones_warp<PS, PT, PP>(sM, acc + (size_t)c * P, scr, 1, parent, err, &s_q[w][c]);
+      __syncwarp();
+    }
   }
 }
 
@@ -1354,6 +1699,114 @@ bool launch_propagation_gemm(ifgf_plan* P, int d, const double2* child, double2*
   return done;
 }
 
+
+// Warp-GEMM tables of child level d, built on first use: the A operand of
+// every row tile, the zero block, and the parent cones sorted (stably) by
+// (group of consecutive parent boxes, gamma index, child mask) and cut into
+// units of <= kG4Cones cones sharing (group, gamma).  The group is sized for
+// ~8 units per gamma, capped so its child blocks (~48 MB) stay in L2 while
+// its units run.
+void build_wgemm_extras(ifgf_plan* P, int d, cudaStream_t s) {
+  PropTiles& T = P->tiles[d];
+  const Level& U = P->lv[d - 1];
+  const Level& L = P->lv[d];
+  const InterpConsts& K = P->K;
+  const uint32_t ntiles = T.ngamma * 8;
+  auto tmp = [&](size_t b) { return (void*)P->alloc<char>(b); };
+  uint32_t nrt = 0;
+  IFGF_CUDA(cudaMemcpyAsync(&nrt, T.rt_off + ntiles, 4, cudaMemcpyDeviceToHost, s));
+  IFGF_CUDA(cudaStreamSynchronize(s));
+  uint32_t* rt_tile = P->alloc<uint32_t>(nrt + 1);
+  k_tile_rows<<<nblk(ntiles, 64), 64, 0, s>>>(ntiles, K.P, T.e_gc, nullptr, nullptr, T.rt_off,
+                                              T.rt, nullptr, nullptr, nullptr, rt_tile);
+  T.rtab = P->alloc<char>((size_t)(nrt + 1) * 8 * sizeof(WgRow));
+  k_wgemm_rtab<<<nblk((size_t)nrt * 8, 256), 256, 0, s>>>(nrt, K.P, T.rt, rt_tile, T.e_t, T.e_T,
+                                                        reinterpret_cast<WgRow*>(T.rtab));
+  T.zblock = P->alloc<double2>((size_t)K.Pst + 8);
+  IFGF_CUDA(cudaMemsetAsync(T.zblock, 0, ((size_t)K.Pst + 8) * sizeof(double2), s));
+  // One box group = the whole level (gamma-major order) measured best at C2
+  // (d = 8: 5.8 ms against 6.8 ms with 193-box groups sized for L2): longer
+  // (gamma, mask) runs fill the units and align their child masks, and the
+  // child blocks' re-reads come from DRAM at a rate the kernel does not feel.
+  static const int bg_env = [] {
+    const char* v = std::getenv("IFGF_G4_BOXGROUP");
+    return v ? std::atoi(v) : 0;
+  }();
+  const uint32_t bg = bg_env > 0 ? (uint32_t)bg_env : std::max<uint32_t>(1, U.nb);
+  uint32_t* qidx = P->alloc<uint32_t>(U.nc);
+  uint64_t* key = P->alloc<uint64_t>(U.nc);
+  uint64_t* gsorted = P->alloc<uint64_t>(U.nc);
+  T.usorted = P->alloc<uint32_t>(U.nc);
+  {
+    k_wgemm_keys<<<nblk(U.nc), 256, 0, s>>>(U.dev(), L.dev(), T.cone_gidx, T.ngamma, bg, key, qidx);
+    size_t tb = 0;
+    int bits = 1;
+    const uint64_t kmax = (((uint64_t)U.nb / bg + 1) * T.ngamma) << 8;
+    while ((1ull << bits) < kmax && bits < 64) ++bits;
+    cub::DeviceRadixSort::SortPairs(nullptr, tb, key, gsorted, qidx, T.usorted, (int)U.nc, 0, bits,
+                                    s);
+    IFGF_CUDA(cub::DeviceRadixSort::SortPairs(tmp(tb), tb, key, gsorted, qidx, T.usorted,
+                                              (int)U.nc, 0, bits, s));
+  }
+  uint32_t* flag = P->alloc<uint32_t>(U.nc + 1);
+  uint32_t* pos = P->alloc<uint32_t>(U.nc + 1);
+  // units end where (group, gamma) changes and, unless IFGF_G4_MASKCUT=0,
+  // where the child mask changes (every column of a unit then has the same
+  // octants: no MMA columns spent on absent children)
+  static const bool maskcut = [] {
+    const char* v = std::getenv("IFGF_G4_MASKCUT");
+    return !v || std::atoi(v) != 0;
+  }();
+  k_chunk_flags<<<nblk(U.nc + 1), 256, 0, s>>>(gsorted, U.nc, kG4Cones, flag, maskcut ? 0 : 8);
+  {
+    size_t tb = 0;
+    cub::DeviceScan::ExclusiveSum(nullptr, tb, flag, pos, (int)(U.nc + 1), s);
+    IFGF_CUDA(cub::DeviceScan::ExclusiveSum(tmp(tb), tb, flag, pos, (int)(U.nc + 1), s));
+  }
+  uint32_t nu = 0;
+  IFGF_CUDA(cudaMemcpyAsync(&nu, pos + U.nc, 4, cudaMemcpyDeviceToHost, s));
+  IFGF_CUDA(cudaStreamSynchronize(s));
+  T.nunits = nu;
+  T.unit_start = P->alloc<uint32_t>(nu + 1);
+  k_chunk_starts<<<nblk(U.nc + 1), 256, 0, s>>>(flag, pos, U.nc, T.unit_start, nu);
+  IFGF_CUDA(cudaGetLastError());
+  P->launches += 7;
+  if (std::getenv("IFGF_G4_TRACE"))
+    std::fprintf(stderr, "[wgemm] d=%d cones %u gammas %u row tiles %u box group %u units %u (%.2f cones/unit)\n",
+                 d, U.nc, T.ngamma, nrt, bg, nu, (double)U.nc / std::max(1u, nu));
+}
+
+bool launch_propagation_wgemm(ifgf_plan* P, int d, const double2* child, double2* parent,
+                              cudaStream_t s) {
+  PropTiles& T = P->tiles[d];
+  const Level& U = P->lv[d - 1];
+  const Level& L = P->lv[d];
+  const InterpConsts& K = P->K;
+  bool done = false;
+  dispatch_mma_orders(K.ps, K.pt, K.pp, [&](auto A, auto B, auto C) {
+    constexpr int PS = decltype(A)::value, PT = decltype(B)::value, PP = decltype(C)::value;
+    using S4 = G4Shape<PS, PT, PP>;
+    if constexpr (S4::ok) {
+      constexpr int NW = S4::warps;
+      const size_t sm = S4::per_warp * NW;
+      const unsigned grid = (unsigned)std::max<size_t>(
+          1, std::min<size_t>((T.nunits + NW - 1) / NW, (size_t)148));
+      auto launch = [&](auto kern) {
+        IFGF_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+        kern<<<grid, NW * 32, sm, s>>>(U.dev(), L.dev(), K, tiles_dev(T),
+                                       reinterpret_cast<const WgRow*>(T.rtab), P->kappa, T.nunits,
+                                       child, T.zblock, parent, P->err);
+        IFGF_CUDA(cudaGetLastError());
+      };
+      P->kappa == 0.0 ? launch(k_propagate_wgemm<PS, PT, PP, true>)
+                      : launch(k_propagate_wgemm<PS, PT, PP, false>);
+      ++P->launches;
+      done = true;
+    }
+  });
+  return done;
+}
+
 bool launch_propagation_mma(ifgf_plan* P, int d, uint32_t qb, uint32_t qe, const double2* child,
                             double2* parent, cudaStream_t s) {
   PropTiles& T = P->tiles[d];
@@ -1364,6 +1817,14 @@ bool launch_propagation_mma(ifgf_plan* P, int d, uint32_t qb, uint32_t qe, const
   const bool full = qb == 0 && qe == P->lv[d - 1].nc;
   if (P->prop_kernel == IFGF_PROP_DMMA && full) {
     if (!T.rt) build_dmma_extras(P, d, s);
+    static const bool v3 = [] {
+      const char* v = std::getenv("IFGF_G4");
+      return v && std::atoi(v) == 0;
+    }();
+    if (!v3) {
+      if (!T.rtab) build_wgemm_extras(P, d, s);
+      if (T.nunits > 0 && launch_propagation_wgemm(P, d, child, parent, s)) return true;
+    }
     if (T.nchunks > 0 && launch_propagation_gemm(P, d, child, parent, s)) return true;
   }
   const Level& U = P->lv[d - 1];
