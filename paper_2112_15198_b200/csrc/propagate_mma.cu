@@ -796,7 +796,6 @@ __global__ void __launch_bounds__(kG3Warps * 32, 16 / kG3Warps)
 constexpr int kG4Warps = IFGF_G4_WARPS;
 constexpr int kG4Nct = IFGF_G4_NCT;       // column tiles (of 8 cones) per warp unit
 constexpr int kG4Cones = 8 * kG4Nct;
-constexpr int kG4Batch = 16;              // row tiles whose child cones are resolved at once
 
 constexpr int g4_prefetch(int nch) {
   for (int pf = 6; pf > 1; --pf)
@@ -807,7 +806,7 @@ constexpr int g4_prefetch(int nch) {
 template <int PS, int PT, int PP>
 struct G4Shape {
   static constexpr int P = PS * PT * PP;
-  static constexpr size_t per_warp = ((size_t)kG4Cones + 1) * P * sizeof(double2);
+  static constexpr size_t per_warp = (size_t)kG4Cones * P * sizeof(double2);
   static constexpr int warps = kG4Warps;
   static constexpr bool ok = P <= 80;  // A fragments and the load ring in registers
 };
@@ -836,16 +835,11 @@ __global__ void __launch_bounds__(kG4Warps * 32, 1)
   constexpr int P = PS * PT * PP, NCH = (BL::Pst + 7) / 8, PF = g4_prefetch(NCH);
   constexpr bool kTail = (BL::Pst % 8) != 0;  // last chunk reaches past the block
   extern __shared__ double2 smem[];
-  __shared__ double sM[PP * PP + PT * PT + PS * PS];
   __shared__ uint32_t s_q[kG4Warps][kG4Cones];
   __shared__ uint32_t s_cb[kG4Warps][8][kG4Cones];   // child box per octant (kNone: absent)
-  __shared__ uint32_t s_cq[kG4Warps][kG4Batch][kG4Cones];
-  stage_fit_matrices<PS, PT, PP>(K, sM);
-  __syncthreads();
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, NW = blockDim.x >> 5;
   const int kq = lane & 3, nn = lane >> 2;
-  double2* acc = smem + (size_t)w * (kG4Cones + 1) * P;  // [kG4Cones][P] node values
-  double2* scr = acc + (size_t)kG4Cones * P;              // fit scratch, one cone
+  double2* acc = smem + (size_t)w * kG4Cones * P;  // [kG4Cones][P] node values
   // chunk cc of the block at p (already offset by the lane's 2 kq coefficients)
   auto bload = [&](const double2* p, int cc) -> double4 {
     if (kTail && cc == NCH - 1) {
@@ -880,141 +874,179 @@ __global__ void __launch_bounds__(kG4Warps * 32, 1)
       for (int o = 0; o < 8; ++o) s_cb[w][o][lane] = cbo[o];
     }
     omask = __reduce_or_sync(0xffffffffu, omask);
-    const uint32_t gi = T.cone_gidx[T.usorted[c0]];
+    const uint32_t tbase = T.cone_gidx[T.usorted[c0]] * 8;
     __syncwarp();
-    for (int o = 0; o < 8; ++o) {
-      if (!((omask >> o) & 1u)) continue;  // warp-uniform
-      const uint32_t tile = gi * 8 + (uint32_t)o;
-      const uint32_t r0 = T.rt_off[tile], r1 = T.rt_off[tile + 1];
-      // column tiles with a child in this octant (cones are sorted by child
-      // mask, so a tile's 8 cones mostly agree)
-      const uint32_t has =
-          __ballot_sync(0xffffffffu, lane < kG4Cones && s_cb[w][o][lane < kG4Cones ? lane : 0] != kNone);
-      // NU column tiles from tile ub on, row tiles [rb, rb + nb)
-      auto run_batch = [&](auto NUc, int ub, uint32_t rb, int nb) {
-        constexpr int NU = decltype(NUc)::value;
-        WgRow rec = rtab[(size_t)rb * 8 + nn];
-        const double2* bp[NU];
-        double4 bq[PF][NU];
-#pragma unroll
-        for (int u = 0; u < NU; ++u) {
-          const uint32_t cq = s_cq[w][0][(ub + u) * 8 + nn];  // this lane's B column cone
-          bp[u] = (cq == kNone ? zblock : child + (size_t)cq * BL::Pst) + 2 * kq;
+    // The unit's row tiles, octant after octant, as one stream of instances
+    // (octant, row tile).  Everything an instance needs from memory is
+    // requested ahead of its turn: its child gamma three instances ahead,
+    // its cones' bitmap words two ahead (find_cone), its node record and the
+    // first kPF block chunks one ahead.
+    struct Inst {
+      int o;
+      uint32_t r, r1;
+    };
+    auto advance = [&](Inst& it) {  // o = 8: past the end
+      ++it.r;
+      while (it.o < 8 && it.r >= it.r1) {
+        do ++it.o;
+        while (it.o < 8 && !((omask >> it.o) & 1u));
+        if (it.o < 8) {
+          it.r = T.rt_off[tbase + it.o];
+          it.r1 = T.rt_off[tbase + it.o + 1];
         }
-#pragma unroll
-        for (int c = 0; c < PF; ++c)
-#pragma unroll
-          for (int u = 0; u < NU; ++u) bq[c][u] = bload(bp[u], c);
-        for (int rl = 0; rl < nb; ++rl) {
-          // the next row tile's node record and block pointers (the last row
-          // tile prefetches the zero block)
-          const bool more = rl + 1 < nb;
-          const WgRow recn = rtab[((size_t)rb + (more ? rl + 1 : rl)) * 8 + nn];
-          const double2* bpn[NU];
-#pragma unroll
-          for (int u = 0; u < NU; ++u) {
-            const uint32_t cq = more ? s_cq[w][rl + 1][(ub + u) * 8 + nn] : kNone;
-            bpn[u] = (cq == kNone ? zblock : child + (size_t)cq * BL::Pst) + 2 * kq;
-          }
-          // basis of this lane's node: Ts and the theta-phi products
-          double Ts[PS], WP[PT * PP];
-          {
-            double Tt[PT], Tp[PP];
-            cheb_basis<PS>(rec.ts, Ts);
-            cheb_basis<PT>(rec.tt, Tt);
-            cheb_basis<PP>(rec.tp, Tp);
-            if (rec.m < 0) {
-#pragma unroll
-              for (int k2 = 0; k2 < PS; ++k2) Ts[k2] = 0.0;
-            }
-#pragma unroll
-            for (int t = 0; t < PT; ++t)
-#pragma unroll
-              for (int p2 = 0; p2 < PP; ++p2) WP[t * PP + p2] = Tt[t] * Tp[p2];
-          }
-          double dr[NU][2], di[NU][2];
-#pragma unroll
-          for (int u = 0; u < NU; ++u) dr[u][0] = dr[u][1] = di[u][0] = di[u][1] = 0.0;
-#pragma unroll
-          for (int c = 0; c < NCH; ++c) {
-            // A fragments of the chunk: the lane's two coefficients
-            double a[2];
-#pragma unroll
-            for (int h = 0; h < 2; ++h) {
-              double wv[4], sv[4];
-#pragma unroll
-              for (int k2 = 0; k2 < 4; ++k2) {
-                const int e = 8 * c + 2 * k2 + h;
-                const bool real = e < BL::Pst && e % BL::PL < PT * PP;
-                wv[k2] = real ? WP[real ? e % BL::PL : 0] : 0.0;
-                sv[k2] = real ? Ts[real ? e / BL::PL : 0] : 0.0;
-              }
-              a[h] = sel4(kq, sv[0], sv[1], sv[2], sv[3]) * sel4(kq, wv[0], wv[1], wv[2], wv[3]);
-            }
-            double4 b[NU];
-#pragma unroll
-            for (int u = 0; u < NU; ++u) b[u] = bq[c % PF][u];
-#pragma unroll
-            for (int u = 0; u < NU; ++u) {
-              dmma(dr[u][0], dr[u][1], a[0], b[u].x);
-              dmma(di[u][0], di[u][1], a[0], b[u].y);
-            }
-#pragma unroll
-            for (int u = 0; u < NU; ++u) {
-              dmma(dr[u][0], dr[u][1], a[1], b[u].z);
-              dmma(di[u][0], di[u][1], a[1], b[u].w);
-              bq[c % PF][u] = c + PF < NCH ? bload(bp[u], c + PF) : bload(bpn[u], c + PF - NCH);
-            }
-          }
-          // epilogue: D row nn = node m, columns 2 kq + h = cones of the tile
-          if (rec.m >= 0) {
-            const int m = (int)rec.m;
-#pragma unroll
-            for (int u = 0; u < NU; ++u)
-#pragma unroll
-              for (int h = 0; h < 2; ++h) {
-                const double vr = dr[u][h], vi = di[u][h];
-                double2* p = acc + (size_t)((ub + u) * 8 + 2 * kq + h) * P + m;
-                double2 v = *p;
-                if (LAP) {
-                  v.x = fma(vr, rec.tfx, v.x);
-                  v.y = fma(vi, rec.tfx, v.y);
-                } else {
-                  v.x = fma(vr, rec.tfx, fma(-vi, rec.tfy, v.x));
-                  v.y = fma(vr, rec.tfy, fma(vi, rec.tfx, v.y));
-                }
-                *p = v;
-              }
-          }
-          rec = recn;
-#pragma unroll
-          for (int u = 0; u < NU; ++u) bp[u] = bpn[u];
-        }
-      };
-      for (uint32_t rb = r0; rb < r1; rb += kG4Batch) {
-        const int nb = (int)min((uint32_t)kG4Batch, r1 - rb);
-        // child cone of every (row tile, cone) of the batch: independent
-        // lookups across lanes
-        for (int i = lane; i < nb * kG4Cones; i += 32) {
-          const int rl = i / kG4Cones, j = i % kG4Cones;
-          const uint32_t cb = s_cb[w][o][j];
-          uint32_t cq = kNone;
-          if (cb != kNone) {
-            cq = find_cone(L, cb, __ldg(&T.rt[rb + rl].x));
-            if (cq == kNone) raise_err(err, kErrPropCover);
-          }
-          s_cq[w][rl][j] = cq;
-        }
-        __syncwarp();
-        if (kG4Nct == 2) {
-          if ((has & 0xffu) && (has & 0xff00u)) run_batch(std::integral_constant<int, kG4Nct>{}, 0, rb, nb);
-          else run_batch(std::integral_constant<int, 1>{}, (has & 0xffu) ? 0 : 1, rb, nb);
-        } else {
-          run_batch(std::integral_constant<int, kG4Nct>{}, 0, rb, nb);
-        }
-        __syncwarp();  // s_cq readers done before the next batch
       }
-      // flagged nodes: per-box exact locate + evaluation (rare)
+    };
+    struct Pend {  // find_cone in flight: bitmap word, rank, bit (64: absent child)
+      uint64_t wd;
+      uint32_t rk, bit;
+    };
+    auto lookup = [&](const Inst& it, uint32_t gc, Pend (&pd)[kG4Nct]) {
+#pragma unroll
+      for (int u = 0; u < kG4Nct; ++u) {
+        const uint32_t cb = it.o < 8 ? s_cb[w][it.o][u * 8 + nn] : kNone;
+        pd[u].wd = 0;
+        pd[u].rk = 0;
+        pd[u].bit = 64;
+        if (cb != kNone) {
+          const uint64_t idx = (uint64_t)cb * L.G + gc;
+          pd[u].wd = __ldg(&L.bits[idx >> 6]);
+          pd[u].rk = __ldg(&L.rank[idx >> 6]);
+          pd[u].bit = (uint32_t)(idx & 63);
+        }
+      }
+    };
+    auto resolve = [&](const Pend (&pd)[kG4Nct], const double2* (&bpo)[kG4Nct]) {
+#pragma unroll
+      for (int u = 0; u < kG4Nct; ++u) {
+        const double2* p = zblock;
+        if (pd[u].bit < 64) {
+          const uint64_t bit = 1ull << pd[u].bit;
+          if (pd[u].wd & bit)
+            p = child + (size_t)(pd[u].rk + (uint32_t)__popcll(pd[u].wd & (bit - 1))) * BL::Pst;
+          else
+            raise_err(err, kErrPropCover);
+        }
+        bpo[u] = p + 2 * kq;
+      }
+    };
+    Inst i0 = {-1, 0, 0};
+    advance(i0);
+    Inst i1 = i0;
+    if (i1.o < 8) advance(i1);
+    Inst i2 = i1;
+    if (i2.o < 8) advance(i2);
+    uint32_t g2 = i2.o < 8 ? __ldg(&T.rt[i2.r].x) : 0;
+    const double2* bp[kG4Nct];
+    double4 bq[PF][kG4Nct];
+    Pend pd[kG4Nct];
+    WgRow rec = {0.0, 0.0, 0.0, 0.0, 0.0, -1};
+    if (i0.o < 8) {
+      lookup(i0, __ldg(&T.rt[i0.r].x), pd);
+      rec = rtab[(size_t)i0.r * 8 + nn];
+    } else {
+      lookup(i0, 0, pd);
+    }
+    resolve(pd, bp);
+#pragma unroll
+    for (int c = 0; c < PF; ++c)
+#pragma unroll
+      for (int u = 0; u < kG4Nct; ++u) bq[c][u] = bload(bp[u], c);
+    lookup(i1, i1.o < 8 ? __ldg(&T.rt[i1.r].x) : 0, pd);
+    while (i0.o < 8) {
+      // instance i1: its cones are resolved now (requested one instance ago);
+      // instance i2: request its bitmap words; instance i3: its child gamma
+      const double2* bpn[kG4Nct];
+      resolve(pd, bpn);
+      lookup(i2, g2, pd);
+      Inst i3 = i2;
+      if (i3.o < 8) advance(i3);
+      g2 = i3.o < 8 ? __ldg(&T.rt[i3.r].x) : 0;
+      const WgRow recn = rtab[(size_t)(i1.o < 8 ? i1.r : i0.r) * 8 + nn];
+      // basis of this lane's node: Ts and the theta-phi products
+      double Ts[PS], WP[PT * PP];
+      {
+        double Tt[PT], Tp[PP];
+        cheb_basis<PS>(rec.ts, Ts);
+        cheb_basis<PT>(rec.tt, Tt);
+        cheb_basis<PP>(rec.tp, Tp);
+        if (rec.m < 0) {
+#pragma unroll
+          for (int k2 = 0; k2 < PS; ++k2) Ts[k2] = 0.0;
+        }
+#pragma unroll
+        for (int t = 0; t < PT; ++t)
+#pragma unroll
+          for (int p2 = 0; p2 < PP; ++p2) WP[t * PP + p2] = Tt[t] * Tp[p2];
+      }
+      double dr[kG4Nct][2], di[kG4Nct][2];
+#pragma unroll
+      for (int u = 0; u < kG4Nct; ++u) dr[u][0] = dr[u][1] = di[u][0] = di[u][1] = 0.0;
+#pragma unroll
+      for (int c = 0; c < NCH; ++c) {
+        // A fragments of the chunk: the lane's two coefficients
+        double a[2];
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          double wv[4], sv[4];
+#pragma unroll
+          for (int k2 = 0; k2 < 4; ++k2) {
+            const int e = 8 * c + 2 * k2 + h;
+            const bool real = e < BL::Pst && e % BL::PL < PT * PP;
+            wv[k2] = real ? WP[real ? e % BL::PL : 0] : 0.0;
+            sv[k2] = real ? Ts[real ? e / BL::PL : 0] : 0.0;
+          }
+          a[h] = sel4(kq, sv[0], sv[1], sv[2], sv[3]) * sel4(kq, wv[0], wv[1], wv[2], wv[3]);
+        }
+        double4 b[kG4Nct];
+#pragma unroll
+        for (int u = 0; u < kG4Nct; ++u) b[u] = bq[c % PF][u];
+#pragma unroll
+        for (int u = 0; u < kG4Nct; ++u) {
+          dmma(dr[u][0], dr[u][1], a[0], b[u].x);
+          dmma(di[u][0], di[u][1], a[0], b[u].y);
+        }
+#pragma unroll
+        for (int u = 0; u < kG4Nct; ++u) {
+          dmma(dr[u][0], dr[u][1], a[1], b[u].z);
+          dmma(di[u][0], di[u][1], a[1], b[u].w);
+          bq[c % PF][u] = c + PF < NCH ? bload(bp[u], c + PF) : bload(bpn[u], c + PF - NCH);
+        }
+      }
+      // epilogue: D row nn = node m, columns 2 kq + h = cones of the tile
+      if (rec.m >= 0) {
+        const int m = (int)rec.m;
+#pragma unroll
+        for (int u = 0; u < kG4Nct; ++u)
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const double vr = dr[u][h], vi = di[u][h];
+            double2* p = acc + (size_t)(u * 8 + 2 * kq + h) * P + m;
+            double2 v = *p;
+            if (LAP) {
+              v.x = fma(vr, rec.tfx, v.x);
+              v.y = fma(vi, rec.tfx, v.y);
+            } else {
+              v.x = fma(vr, rec.tfx, fma(-vi, rec.tfy, v.x));
+              v.y = fma(vr, rec.tfy, fma(vi, rec.tfx, v.y));
+            }
+            *p = v;
+          }
+      }
+      // the next octant's row tiles touch the same (cone, node) slots from other lanes
+      if (i1.o != i0.o) __syncwarp();
+      i0 = i1;
+      i1 = i2;
+      i2 = i3;
+      rec = recn;
+#pragma unroll
+      for (int u = 0; u < kG4Nct; ++u) bp[u] = bpn[u];
+    }
+    __syncwarp();
+    // flagged nodes: per-box exact locate + evaluation (rare), after the MMA
+    // contributions, octants in Morton order
+    for (int o = 0; o < 8; ++o) {
+      if (!((omask >> o) & 1u)) continue;
+      const uint32_t tile = tbase + (uint32_t)o;
       const size_t f0 = (size_t)tile * P;
       const uint32_t nfl = T.fl_cnt[tile];
       for (uint32_t i = lane; i < nfl * (uint32_t)kG4Cones; i += 32) {
@@ -1052,12 +1084,10 @@ __global__ void __launch_bounds__(kG4Warps * 32, 1)
         v.y = fma(vr, ti, fma(vi, tr, v.y));
         acc[(size_t)c * P + m] = v;
       }
-      __syncwarp();  // the next octant's row tiles touch the same (cone, node) slots
-    }
-    for (int c = 0; c < nq; ++c) {
-      fit_cones_warp<PS, PT, PP>(sM, acc + (size_t)c * P, scr, 1, parent, err, &s_q[w][c]);
       __syncwarp();
     }
+    fit_cones_inplace<PS, PT, PP>(K, acc, nq, parent, err, s_q[w]);
+    __syncwarp();
   }
 }
 
@@ -1085,14 +1115,10 @@ __global__ void __launch_bounds__(kRowThreads, IFGF_ROWS_MINB)
   extern __shared__ double2 smem[];
   __shared__ uint32_t s_cb0[NW][kRowMaxCpw], s_tile[NW][kRowMaxCpw], s_nrow[NW][kRowMaxCpw],
       s_pre[NW][kRowMaxCpw + 1];
-  __shared__ double sM[PP * PP + PT * PT + PS * PS];
-  stage_fit_matrices<PS, PT, PP>(K, sM);
-  __syncthreads();
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  // per warp: sv, st (cpw * P values each), task meta (<= cpw * P tasks)
-  double2* sv = smem + (size_t)w * 3 * cpw * P;
-  double2* st = sv + cpw * P;
-  uint2* meta = reinterpret_cast<uint2*>(st + cpw * P);
+  // per warp: sv (cpw * P values), task meta (<= cpw * P tasks)
+  double2* sv = smem + (size_t)w * 2 * cpw * P;
+  uint2* meta = reinterpret_cast<uint2*>(sv + cpw * P);
   for (int g = 0; g < groups; ++g) {
     const uint32_t q0 = qb + (((uint32_t)g * gridDim.x + blockIdx.x) * NW + w) * cpw;
     if (q0 >= qe) break;
@@ -1255,7 +1281,7 @@ __global__ void __launch_bounds__(kRowThreads, IFGF_ROWS_MINB)
       }
       __syncwarp();
     }
-    fit_cones_warp<PS, PT, PP>(sM, sv, st, nw, parent + (size_t)q0 * BL::Pst, err);
+    fit_cones_inplace<PS, PT, PP>(K, sv, nw, parent + (size_t)q0 * BL::Pst, err);
     __syncwarp();
   }
 }
@@ -1290,9 +1316,7 @@ __global__ void __launch_bounds__(kRowThreads, IFGF_ROWS_MINB)
   const int NW = blockDim.x >> 5;
   extern __shared__ __align__(16) unsigned char fly_smem[];
   __shared__ double2 trig[kTrigEntries];
-  __shared__ double sM[PP * PP + PT * PT + PS * PS];
   stage_trig(trig, L.trig);
-  stage_fit_matrices<PS, PT, PP>(K, sM);
   __syncthreads();
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   FlyWarp<P>& F = reinterpret_cast<FlyWarp<P>*>(fly_smem)[w];
@@ -1408,7 +1432,7 @@ __global__ void __launch_bounds__(kRowThreads, IFGF_ROWS_MINB)
       }
       __syncwarp();
     }
-    fit_cones_warp<PS, PT, PP>(sM, F.sv, F.st, 1, parent + (size_t)q * BL::Pst, err);
+    fit_cones_inplace<PS, PT, PP>(K, F.sv, 1, parent + (size_t)q * BL::Pst, err);
     __syncwarp();
   }
 }
@@ -1750,12 +1774,11 @@ void build_wgemm_extras(ifgf_plan* P, int d, cudaStream_t s) {
   }
   uint32_t* flag = P->alloc<uint32_t>(U.nc + 1);
   uint32_t* pos = P->alloc<uint32_t>(U.nc + 1);
-  // units end where (group, gamma) changes and, unless IFGF_G4_MASKCUT=0,
-  // where the child mask changes (every column of a unit then has the same
-  // octants: no MMA columns spent on absent children)
+  // units end where (group, gamma) changes; cutting at mask changes as well
+  // (IFGF_G4_MASKCUT=1) leaves units of ~6 cones at C2 and is 2-3x slower
   static const bool maskcut = [] {
     const char* v = std::getenv("IFGF_G4_MASKCUT");
-    return !v || std::atoi(v) != 0;
+    return v && std::atoi(v) != 0;
   }();
   k_chunk_flags<<<nblk(U.nc + 1), 256, 0, s>>>(gsorted, U.nc, kG4Cones, flag, maskcut ? 0 : 8);
   {
@@ -1838,9 +1861,9 @@ bool launch_propagation_mma(ifgf_plan* P, int d, uint32_t qb, uint32_t qe, const
       const char* v = std::getenv("IFGF_ROWS_CPW");
       return v ? std::atoi(v) : 0;
     }();
-    // shared memory for sv + st + task meta: ~96 KB per CTA (the rest of the SRAM is L1)
-    const int per_cone = 3 * Pn * (int)sizeof(double2);
-    const int cpw_fit = (int)(96 * 1024 / IFGF_ROWS_MINB / per_cone / NW);
+    // shared memory for sv + task meta: ~64 KB per CTA (the rest of the SRAM is L1)
+    const int per_cone = 2 * Pn * (int)sizeof(double2);
+    const int cpw_fit = (int)(64 * 1024 / IFGF_ROWS_MINB / per_cone / NW);
     const int cpw = std::max(1, std::min(kRowMaxCpw, cpw_env > 0 ? cpw_env : std::max(1, cpw_fit)));
     const int cpb = NW * cpw;
     const uint32_t nq = qe - qb;
