@@ -105,17 +105,21 @@ void ifgf_plan_destroy(ifgf_plan* plan);
  * IFGF_OPT_PROP_KERNEL selects the propagation kernel:
  *   IFGF_PROP_NODE  (0) thread per (parent cone, node), locate per child
  *                       (the generic path: any orders);
- *   IFGF_PROP_DMMA  (2) box-batched FP64 tensor-core GEMM: up to 32 parent
- *                       cones sharing gamma per CTA, mma.sync.m8n8k4.f64 with
- *                       the node basis held in registers (whole levels only;
+ *   IFGF_PROP_DMMA  (2) warp-level FP64 tensor-core GEMM on every level with
+ *                       the precomputed geometry: a warp owns 16 parent
+ *                       cones that share gamma, mma.sync.m8n8k4.f64 over the
+ *                       child blocks in memory order (whole levels only;
  *                       ranges and levels without the precomputed geometry
  *                       run ROWS / FLY);
- *   IFGF_PROP_ROWS  (3, default) thread per (parent cone, child, row of <= 3
+ *   IFGF_PROP_ROWS  (3) thread per (parent cone, child, row of <= 3
  *                       nodes that share a child cone) from the precomputed
  *                       geometry, one block load per row; levels without
  *                       the precomputed geometry run IFGF_PROP_FLY;
  *   IFGF_PROP_FLY   (4) the same rows grouped per parent cone on the fly
- *                       (no precomputed geometry).
+ *                       (no precomputed geometry);
+ *   IFGF_PROP_AUTO  (7, default) per level: the warp GEMM where at least
+ *                       100 parent cones share each gamma (the fine
+ *                       levels), ROWS / FLY elsewhere.
  *   Values 1, 5, 6 (TILES, STREAM, PIPE of ABI 1) were measured slower than
  *   ROWS and removed; they fail with IFGF_EINVAL.
  *   All agree to rounding; DESIGN.md records their measured times.
@@ -143,7 +147,8 @@ enum {
   IFGF_PROP_NODE = 0,
   IFGF_PROP_DMMA = 2,
   IFGF_PROP_ROWS = 3,
-  IFGF_PROP_FLY = 4
+  IFGF_PROP_FLY = 4,
+  IFGF_PROP_AUTO = 7
 };
 int ifgf_plan_set_option(ifgf_plan* plan, int option, int value);
 

@@ -705,7 +705,7 @@ int ifgf_plan_set_option(ifgf_plan* P, int option, int value) {
       P->serial = value != 0;
     } else if (option == IFGF_OPT_PROP_KERNEL) {
       if (value != IFGF_PROP_NODE && value != IFGF_PROP_DMMA && value != IFGF_PROP_ROWS &&
-          value != IFGF_PROP_FLY)
+          value != IFGF_PROP_FLY && value != IFGF_PROP_AUTO)
         throw Error(IFGF_EINVAL, "unknown propagation kernel (TILES, STREAM and PIPE were "
                                  "measured slower than ROWS and removed; DESIGN.md section 3)");
       P->prop_kernel = value;

@@ -154,16 +154,12 @@ struct PropTiles {
   double* rdat = nullptr;       // row data (ts, tt, tp, tr, ti per slot), 32-row chunks,
                                 // SoA inside (propagate_mma.cu row_field)
   uint32_t* rnode = nullptr;    // per row (tile * P + r): node of slot j in byte j
-  // IFGF_PROP_DMMA CTA chunks of <= kG3Cones (32) parent cones sharing one gamma
-  uint32_t nchunks = 0;
-  uint32_t box_group = 0;  // parent boxes per chunk group (IFGF_PROP_DMMA)
-  uint32_t* qsorted = nullptr;
-  uint32_t* chunk_start = nullptr;
   // warp GEMM (k_propagate_wgemm): per row tile and node slot one record of
   // node data; parent cones sorted by (box group, gamma, child mask) and cut
   // into warp units of <= 8 * kG4Nct cones sharing (group, gamma, mask)
   char* rtab = nullptr;
   uint32_t nunits = 0;
+  uint32_t wg_qb = 0, wg_qe = 0;  // cone range of the units
   uint32_t* usorted = nullptr;
   uint32_t* unit_start = nullptr;
   double2* zblock = nullptr;   // one zero block (absent children's B operand)
@@ -202,7 +198,7 @@ struct ifgf_plan {
   double setup_seconds = 0.0;
   size_t launches = 0;  // kernels launched by this plan since the last reset
   bool serial = false;  // IFGF_OPT_SERIAL
-  int prop_kernel = IFGF_PROP_ROWS;  // IFGF_OPT_PROP_KERNEL
+  int prop_kernel = IFGF_PROP_AUTO;  // IFGF_OPT_PROP_KERNEL
   int near_kernel = IFGF_NEAR_BOX;   // IFGF_OPT_NEAR_KERNEL
   int partition_mode = IFGF_PARTITION_COUNT;  // IFGF_OPT_PARTITION
   size_t setup_launches = 0;

@@ -61,8 +61,6 @@ struct TilesDev {
   const uint4* rt;
   const uint32_t* fl_cnt;   // flagged nodes of tile t: fl_node[t * P + i], i < fl_cnt[t]
   const uint16_t* fl_node;
-  const uint32_t* qsorted;
-  const uint32_t* chunk_start;
   const uint8_t* e_perm;
   const uint32_t* rw_cnt;   // rows of tile t: rw[t * P + i], i < rw_cnt[t]
   const uint2* rw;
@@ -74,7 +72,7 @@ struct TilesDev {
 
 TilesDev tiles_dev(const PropTiles& t) {
   return {t.ngamma,   t.cone_gidx,   t.gamma_of, t.e_t,    t.e_T,  t.e_gc, t.rt_off,
-          t.rt,       t.fl_cnt,      t.fl_node,  t.qsorted, t.chunk_start, t.e_perm,
+          t.rt,       t.fl_cnt,      t.fl_node,  t.e_perm,
           t.rw_cnt,   t.rw,          t.rdat,     t.rnode,   t.usorted, t.unit_start};
 }
 
@@ -336,19 +334,6 @@ __global__ void __launch_bounds__(256)
   }
 }
 
-#ifndef IFGF_GEMM_BOXGROUP
-#define IFGF_GEMM_BOXGROUP 32
-#endif
-constexpr uint32_t kGemmBoxGroup = IFGF_GEMM_BOXGROUP;
-
-__global__ void k_gemm_keys(const __grid_constant__ LevelDev U, const uint32_t* __restrict__ gidx,
-                            uint32_t ngamma, uint32_t box_group, uint64_t* key, uint32_t* qidx) {
-  const uint32_t q = blockIdx.x * blockDim.x + threadIdx.x;
-  if (q >= U.nc) return;
-  key[q] = (uint64_t)(U.cone_box[q] / box_group) * ngamma + gidx[q];
-  qidx[q] = q;
-}
-
 __global__ void k_chunk_flags(const uint64_t* gsorted, uint32_t n, uint32_t chunk, uint32_t* flag,
                               int shift = 0) {
   const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
@@ -382,15 +367,17 @@ __global__ void k_chunk_starts(const uint32_t* flag, const uint32_t* pos, uint32
 // share their present octants.
 __global__ void k_wgemm_keys(const __grid_constant__ LevelDev U, const __grid_constant__ LevelDev L,
                              const uint32_t* __restrict__ gidx, uint32_t ngamma,
-                             uint32_t box_group, uint64_t* key, uint32_t* qidx) {
-  const uint32_t q = blockIdx.x * blockDim.x + threadIdx.x;
-  if (q >= U.nc) return;
+                             uint32_t box_group, uint32_t qb, uint32_t qe, uint64_t* key,
+                             uint32_t* qidx) {
+  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= qe - qb) return;
+  const uint32_t q = qb + i;
   const uint32_t pb = U.cone_box[q];
   uint32_t mask = 0;
   for (uint32_t cb = U.child_begin[pb]; cb < U.child_begin[pb + 1]; ++cb)
     mask |= 1u << (uint32_t)(L.code[cb] & 7);
-  key[q] = (((uint64_t)(pb / box_group) * ngamma + gidx[q]) << 8) | mask;
-  qidx[q] = q;
+  key[i] = (((uint64_t)(pb / box_group) * ngamma + gidx[q]) << 8) | mask;
+  qidx[i] = q;
 }
 
 // Per row tile and node slot: the node's local coordinates in its child cone,
@@ -468,305 +455,6 @@ __device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b)
   asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
                : "+d"(d0), "+d"(d1)
                : "d"(a), "d"(b));
-}
-
-// K order of the FP64 MMA (mma.sync.m8n8k4.f64): part 1 steps (ks, kt, c),
-// lane k of the quad -> kp = 4c + k; part 2 packs the remaining
-// kp >= 4 floor(PP/4) over (kp, ks, kt), four per step.
-template <int PS, int PT, int PP>
-struct GemmK {
-  static constexpr int NC = PP / 4;           // full kp chunks of 4
-  static constexpr int PPF = 4 * NC;
-  static constexpr int N1 = PS * PT * NC;      // part-1 steps
-  static constexpr int N2R = (PP - PPF) * PS * PT;
-  static constexpr int N2 = (N2R + 3) / 4;     // part-2 steps
-  static constexpr int NS = N1 + N2;           // K steps of 4
-  static constexpr int P = PS * PT * PP;
-};
-
-// Coefficient (device block offset, or -1 for a pad entry) of K step st,
-// quad lane k (GemmK order).
-template <int PS, int PT, int PP>
-__host__ __device__ __forceinline__ int gemm_koff(int st, int k, int& ks, int& kt, int& kp) {
-  using G = GemmK<PS, PT, PP>;
-  constexpr int PL = BlockLayout<PS, PT, PP>::PL;
-  if (st < G::N1) {
-    const int c = st % G::NC, pair = st / G::NC;
-    ks = pair / PT;
-    kt = pair % PT;
-    kp = 4 * c + k;
-  } else {
-    const int p = 4 * (st - G::N1) + k;
-    if (p >= G::N2R) return -1;
-    const int e = p / (PS * PT), pr = p % (PS * PT);
-    ks = pr / PT;
-    kt = pr % PT;
-    kp = G::PPF + e;
-  }
-  return ks * PL + kt * PP + kp;
-}
-
-// ---------------------------------------------------------------- K3 v3
-// IFGF_PROP_DMMA: box-batched FP64 tensor-core GEMM.  One CTA takes a chunk
-// of up to kG3Cones parent cones that share gamma (box-group-major order, so
-// concurrently running CTAs share the child blocks of one group of parent
-// boxes in L2).  For each child octant o (Morton order, CTA barrier between
-// octants: the reference's per-node child order) and each row tile of
-// tile (gamma, o) -- <= 8 nodes sharing a child cone gamma_c --
-//   V[node][cone] = sum_k A[node][k] C_{cone's child, gamma_c}[k]
-// with mma.sync.m8n8k4.f64: A (box-independent basis products) is formed
-// once per row tile in registers and reused for every 8-cone column tile of
-// the chunk; B (the child blocks) streams from L1/L2, one 16-byte load per
-// lane per K step feeding two MMAs (re, im).  Per coefficient byte moved
-// into registers that is 1 FMA (the row kernel: 0.375), which is what the
-// row kernel's L1->register path (75 % busy at 35 % of the FP64 pipe)
-// needs.  The FP64 MMA shares the DFMA pipe on B200 (tools/micro/
-// dmma_peak.cu: mixed time = sum), so the gain is bandwidth and issue, not
-// peak.  Flagged nodes take the exact per-box path; cones are fitted per
-// warp at the end of the chunk.
-// 4 warps x 32 cones per CTA measured best among 2-8 warps x 16-64 cones
-// (profiles/r02/g3_sweep.log)
-#ifndef IFGF_G3_WARPS
-#define IFGF_G3_WARPS 4
-#endif
-#ifndef IFGF_G3_CONES
-#define IFGF_G3_CONES 32
-#endif
-constexpr int kG3Warps = IFGF_G3_WARPS;
-constexpr int kG3Cones = IFGF_G3_CONES;  // parent cones per chunk (8 per column tile)
-constexpr int kG3MaxRt = 80;    // row tiles of one tile (<= P for P <= 80)
-constexpr int kG3MaxGroups = 16;  // child-gamma groups with resolved cones in smem
-
-template <int PS, int PT, int PP>
-struct G3Shape {
-  static constexpr int P = PS * PT * PP;
-  static constexpr size_t smem = ((size_t)kG3Cones + kG3Warps) * P * sizeof(double2);
-  static constexpr bool ok = P <= kG3MaxRt;
-};
-
-template <int PS, int PT, int PP, bool LAP>
-__global__ void __launch_bounds__(kG3Warps * 32, 16 / kG3Warps)
-    k_propagate_gemm(const __grid_constant__ LevelDev U, const __grid_constant__ LevelDev L,
-                     const __grid_constant__ InterpConsts K, const TilesDev T, double kappa,
-                     uint32_t nchunks, const double2* __restrict__ child, double2* parent,
-                     int* err) {
-  using BL = BlockLayout<PS, PT, PP>;
-  using G = GemmK<PS, PT, PP>;
-  constexpr int P = G::P, NS = G::NS;
-  extern __shared__ double2 smem[];
-  double2* acc = smem;                        // [kG3Cones][P] node values
-  double2* scr = smem + (size_t)kG3Cones * P;  // [kG3Warps][P] fit scratch
-  __shared__ double sM[PP * PP + PT * PT + PS * PS];
-  __shared__ uint32_t s_q[kG3Cones];
-  __shared__ uint32_t s_cb[8][kG3Cones];       // child box per octant (kNone: absent)
-  __shared__ uint8_t s_list[kG3Cones];         // cones with a child in octant o
-  __shared__ uint4 s_rt[kG3MaxRt];
-  __shared__ uint8_t s_rg[kG3MaxRt];           // group of each row tile
-  __shared__ uint32_t s_gc[kG3MaxRt];          // child gamma of each group
-  __shared__ uint32_t s_cq[kG3MaxGroups][kG3Cones];
-  __shared__ int s_cnt[3];                     // cones with child o, row tiles, groups
-  stage_fit_matrices<PS, PT, PP>(K, sM);
-  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
-  const int kq = lane & 3, nn = lane >> 2;
-  for (uint32_t ch = blockIdx.x; ch < nchunks; ch += gridDim.x) {
-    const uint32_t c0 = T.chunk_start[ch], c1 = T.chunk_start[ch + 1];
-    const int nq = (int)(c1 - c0);
-    const uint32_t gi = T.cone_gidx[T.qsorted[c0]];
-    for (int i = tid; i < nq * P; i += blockDim.x) acc[i] = make_double2(0.0, 0.0);
-    if (tid < kG3Cones) {
-      const uint32_t q = tid < nq ? T.qsorted[c0 + tid] : kNone;
-      s_q[tid] = q;
-      uint32_t cbo[8];
-#pragma unroll
-      for (int o = 0; o < 8; ++o) cbo[o] = kNone;
-      if (q != kNone) {
-        const uint32_t pb = U.cone_box[q];
-        for (uint32_t cb = U.child_begin[pb]; cb < U.child_begin[pb + 1]; ++cb) {
-          const int o = (int)(L.code[cb] & 7);
-#pragma unroll
-          for (int oo = 0; oo < 8; ++oo)
-            if (oo == o) cbo[oo] = cb;
-        }
-      }
-#pragma unroll
-      for (int o = 0; o < 8; ++o) s_cb[o][tid] = cbo[o];
-    }
-    __syncthreads();
-    for (int o = 0; o < 8; ++o) {
-      const uint32_t tile = gi * 8 + (uint32_t)o;
-      const uint32_t r0 = T.rt_off[tile], r1 = T.rt_off[tile + 1];
-      const int nrt = (int)(r1 - r0);
-      // cones with a child in octant o, compacted in cone order (warp 0)
-      if (w == 0) {
-        int base = 0;
-#pragma unroll
-        for (int half = 0; half < (kG3Cones + 31) / 32; ++half) {
-          const int c = half * 32 + lane;
-          const bool has = c < kG3Cones && s_cb[o][c] != kNone;
-          const unsigned bal = __ballot_sync(0xffffffffu, has);
-          if (has) s_list[base + __popc(bal & ((1u << lane) - 1))] = (uint8_t)c;
-          base += __popc(bal);
-        }
-        if (lane == 0) s_cnt[0] = base;
-      }
-      for (int i = tid; i < nrt; i += blockDim.x) s_rt[i] = T.rt[r0 + i];
-      __syncthreads();
-      if (tid == 0) {  // groups: runs of row tiles sharing a child gamma
-        int g = -1;
-        for (int i = 0; i < nrt; ++i) {
-          if (i == 0 || s_rt[i].x != s_rt[i - 1].x) s_gc[++g] = s_rt[i].x;
-          s_rg[i] = (uint8_t)g;
-        }
-        s_cnt[1] = nrt;
-        s_cnt[2] = g + 1;
-      }
-      __syncthreads();
-      const int no = s_cnt[0], ng = s_cnt[2];
-      if (no == 0) continue;  // uniform
-      // child cone of every (group, cone): independent lookups across threads
-      for (int i = tid; i < min(ng, kG3MaxGroups) * no; i += blockDim.x) {
-        const int g = i / no, jj = i % no;
-        const uint32_t cq = find_cone(L, s_cb[o][s_list[jj]], s_gc[g]);
-        if (cq == kNone) raise_err(err, kErrPropCover);
-        s_cq[g][jj] = cq;
-      }
-      __syncthreads();
-      const int nct = (no + 7) >> 3;  // column tiles of 8 cones
-      for (int rt = w; rt < nrt; rt += kG3Warps) {
-        const uint4 R = s_rt[rt];
-        const int g = s_rg[rt];
-        const int m = rt_node(R, nn);  // this lane's A row (node), 0xff = empty slot
-        double ts = 0.0, tt = 0.0, tp = 0.0;
-        if (m != 0xff) {
-          const double* tv = T.e_t + ((size_t)tile * P + m) * 3;
-          ts = tv[0];
-          tt = tv[1];
-          tp = tv[2];
-        }
-        double Ts[PS], Tt[PT], Tp[PP];
-        cheb_basis<PS>(ts, Ts);
-        cheb_basis<PT>(tt, Tt);
-        cheb_basis<PP>(tp, Tp);
-        if (m == 0xff) {
-#pragma unroll
-          for (int k2 = 0; k2 < PS; ++k2) Ts[k2] = 0.0;
-        }
-        // A fragments of all K steps (GemmK order), kept for every column tile
-        double a[NS];
-        int off[NS];
-#pragma unroll
-        for (int st = 0; st < NS; ++st) {
-          double v = 0.0;
-          int of = 0;
-#pragma unroll
-          for (int kk = 0; kk < 4; ++kk) {
-            int ks, kt, kp;
-            const int o2 = gemm_koff<PS, PT, PP>(st, kk, ks, kt, kp);
-            if (o2 >= 0 && kq == kk) {
-              v = Ts[ks] * Tt[kt] * Tp[kp];
-              of = o2;
-            }
-          }
-          a[st] = v;
-          off[st] = of;
-        }
-        const double2 Tf = m != 0xff ? __ldg(&T.e_T[(size_t)tile * P + m]) : make_double2(0.0, 0.0);
-        // two column tiles per pass: four independent MMA chains
-        for (int ct = 0; ct < nct; ct += 2) {
-          const double2* bb[2];
-#pragma unroll
-          for (int u = 0; u < 2; ++u) {
-            const int jj = (ct + u) * 8 + nn;  // this lane's B column cone
-            uint32_t cq = kNone;
-            if (jj < no) {
-              if (g < kG3MaxGroups) {
-                cq = s_cq[g][jj];
-              } else {
-                cq = find_cone(L, s_cb[o][s_list[jj]], s_gc[g]);
-                if (cq == kNone) raise_err(err, kErrPropCover);
-              }
-            }
-            bb[u] = child + (cq == kNone ? (size_t)0 : (size_t)cq * BL::Pst);
-          }
-          double dr[2][2] = {}, di[2][2] = {};
-#pragma unroll
-          for (int st = 0; st < NS; ++st) {
-#pragma unroll
-            for (int u = 0; u < 2; ++u) {
-              const double2 b = __ldg(bb[u] + off[st]);
-              dmma(dr[u][0], dr[u][1], a[st], b.x);
-              dmma(di[u][0], di[u][1], a[st], b.y);
-            }
-          }
-          // epilogue: D row nn = node m, columns 2 kq + h = cones
-          if (m != 0xff) {
-#pragma unroll
-            for (int u = 0; u < 2; ++u)
-#pragma unroll
-              for (int h = 0; h < 2; ++h) {
-                const int jj = (ct + u) * 8 + 2 * kq + h;
-                if (jj < no) {
-                  double2* p = acc + (size_t)s_list[jj] * P + m;
-                  double2 v = *p;
-                  if (LAP) {
-                    v.x = fma(dr[u][h], Tf.x, v.x);
-                    v.y = fma(di[u][h], Tf.x, v.y);
-                  } else {
-                    v.x = fma(dr[u][h], Tf.x, fma(-di[u][h], Tf.y, v.x));
-                    v.y = fma(dr[u][h], Tf.y, fma(di[u][h], Tf.x, v.y));
-                  }
-                  *p = v;
-                }
-              }
-          }
-        }
-      }
-      // flagged nodes: per-box exact locate + evaluation (rare)
-      const size_t f0 = (size_t)tile * P;
-      const uint32_t nfl = T.fl_cnt[tile];
-      for (uint32_t i = tid; i < nfl * (uint32_t)no; i += blockDim.x) {
-        const int c = s_list[i % no];
-        const uint32_t cb = s_cb[o][c];
-        const int m = T.fl_node[f0 + i / no];
-        const uint32_t q = s_q[c], pb = U.cone_box[q];
-        const int jp = m % PP, jt = (m / PP) % PT, js = m / (PP * PT);
-        const SegMid sg = segment_mid(U, U.cone_gamma[q]);
-        const double pcx = U.cx[pb], pcy = U.cy[pb], pcz = U.cz[pb];
-        double x, y, z;
-        node_position(sg, U.rad, pcx, pcy, pcz, K.ns[js], K.nt[jt], K.np[jp], x, y, z);
-        const double ux = x - pcx, uy = y - pcy, uz = z - pcz;
-        const double rp = sqrt(fma(uz, uz, fma(uy, uy, ux * ux)));
-        Loc lo;
-        const int e = locate_fast(L, L.cx[cb], L.cy[cb], L.cz[cb], x, y, z, lo);
-        if (e) {
-          raise_err(err, e);
-          continue;
-        }
-        const uint32_t cq = find_cone(L, cb, lo.gamma);
-        if (cq == kNone) {
-          raise_err(err, kErrPropCover);
-          continue;
-        }
-        double vr, vi;
-        eval_block<PS, PT, PP>(child + (size_t)cq * BL::Pst, lo.ts, lo.tt, lo.tp, vr, vi);
-        const double ratio = rp * lo.rinv;
-        double sn = 0.0, cn = 1.0;
-        if (!LAP) sincos_fast(kappa * (lo.r - rp), sn, cn);
-        const double tr = ratio * cn, ti = ratio * sn;
-        double2 v = acc[(size_t)c * P + m];
-        v.x = fma(vr, tr, fma(-vi, ti, v.x));
-        v.y = fma(vr, ti, fma(vi, tr, v.y));
-        acc[(size_t)c * P + m] = v;
-      }
-      __syncthreads();
-    }
-    for (int c = w; c < nq; c += kG3Warps) {
-      fit_cones_warp<PS, PT, PP>(sM, acc + (size_t)c * P, scr + (size_t)w * P, 1, parent, err,
-                                 &s_q[c]);
-      __syncwarp();
-    }
-    __syncthreads();
-  }
 }
 
 // ---------------------------------------------------------------- K3 v4
@@ -1617,11 +1305,14 @@ bool launch_propagation_fly(ifgf_plan* P, int d, uint32_t qb, uint32_t qe, const
   });
 }
 
-// Row tiles of 8 and gamma-sorted cone chunks for IFGF_PROP_DMMA, built on
-// first use (the default kernels do not need them).
-void build_dmma_extras(ifgf_plan* P, int d, cudaStream_t s) {
+// Warp-GEMM tables of child level d, built on first use: row tiles of <= 8
+// nodes sharing a child cone (CSR over tiles), one node record per row tile
+// slot, the zero block, and the parent cones sorted (stably) by (gamma index,
+// child mask) and cut into warp units of <= kG4Cones cones sharing gamma.
+void build_wgemm_extras(ifgf_plan* P, int d, cudaStream_t s) {
   PropTiles& T = P->tiles[d];
   const Level& U = P->lv[d - 1];
+  const Level& L = P->lv[d];
   const InterpConsts& K = P->K;
   const uint32_t ntiles = T.ngamma * 8;
   uint32_t* rt_cnt = P->alloc<uint32_t>(ntiles + 1);
@@ -1640,106 +1331,6 @@ void build_dmma_extras(ifgf_plan* P, int d, cudaStream_t s) {
   IFGF_CUDA(cudaMemcpyAsync(&nrt, T.rt_off + ntiles, 4, cudaMemcpyDeviceToHost, s));
   IFGF_CUDA(cudaStreamSynchronize(s));
   T.rt = P->alloc<uint4>(nrt + 1);
-  k_tile_rows<<<nblk(ntiles, 64), 64, 0, s>>>(ntiles, K.P, T.e_gc, nullptr, nullptr, T.rt_off,
-                                              T.rt, nullptr, nullptr, nullptr);
-  // parent cones sorted (stably) by (group of consecutive parent boxes, gamma
-  // index) -> chunks of <= kG3Cones cones sharing gamma.  The group is sized
-  // for ~kG3Cones cones per gamma (mean cones per box and gamma from the
-  // level's counts), capped so the group's child blocks (~48 MB) stay in L2
-  // while its chunks run: gamma order alone re-reads them from DRAM.
-  uint32_t bg = kGemmBoxGroup;
-  {
-    static const int bg_env = [] {
-      const char* v = std::getenv("IFGF_GEMM_BOXGROUP");
-      return v ? std::atoi(v) : 0;
-    }();
-    const double per = (double)U.nc / ((double)U.nb * T.ngamma);  // cones per (box, gamma)
-    const double child_bytes = (double)P->lv[d].nc / std::max<uint32_t>(1, U.nb) * (double)P->K.Pst *
-                               sizeof(double2);  // child blocks per parent box (order-agnostic estimate)
-    double g = kG3Cones / std::max(per, 1e-9);
-    g = std::min(g, 48.0 * (1 << 20) / std::max(child_bytes, 1.0));
-    bg = bg_env > 0 ? (uint32_t)bg_env : (uint32_t)std::max(8.0, std::min(g, (double)U.nb));
-    T.box_group = bg;
-  }
-  uint32_t* qidx = P->alloc<uint32_t>(U.nc);
-  uint64_t* key = P->alloc<uint64_t>(U.nc);
-  uint64_t* gsorted = P->alloc<uint64_t>(U.nc);
-  T.qsorted = P->alloc<uint32_t>(U.nc);
-  {
-    k_gemm_keys<<<nblk(U.nc), 256, 0, s>>>(U.dev(), T.cone_gidx, T.ngamma, bg, key, qidx);
-    size_t tb = 0;
-    int bits = 1;
-    const uint64_t kmax = ((uint64_t)U.nb / bg + 1) * T.ngamma;
-    while ((1ull << bits) < kmax && bits < 64) ++bits;
-    cub::DeviceRadixSort::SortPairs(nullptr, tb, key, gsorted, qidx, T.qsorted, (int)U.nc, 0,
-                                    bits, s);
-    IFGF_CUDA(cub::DeviceRadixSort::SortPairs(tmp(tb), tb, key, gsorted, qidx, T.qsorted,
-                                              (int)U.nc, 0, bits, s));
-    IFGF_CUDA(cudaStreamSynchronize(s));
-  }
-  uint32_t* flag = P->alloc<uint32_t>(U.nc + 1);
-  uint32_t* pos = P->alloc<uint32_t>(U.nc + 1);
-  k_chunk_flags<<<nblk(U.nc + 1), 256, 0, s>>>(gsorted, U.nc, kG3Cones, flag);
-  {
-    size_t tb = 0;
-    cub::DeviceScan::ExclusiveSum(nullptr, tb, flag, pos, (int)(U.nc + 1), s);
-    IFGF_CUDA(cub::DeviceScan::ExclusiveSum(tmp(tb), tb, flag, pos, (int)(U.nc + 1), s));
-  }
-  uint32_t nch = 0;
-  IFGF_CUDA(cudaMemcpyAsync(&nch, pos + U.nc, 4, cudaMemcpyDeviceToHost, s));
-  IFGF_CUDA(cudaStreamSynchronize(s));
-  T.nchunks = nch;
-  T.chunk_start = P->alloc<uint32_t>(nch + 1);
-  k_chunk_starts<<<nblk(U.nc + 1), 256, 0, s>>>(flag, pos, U.nc, T.chunk_start, nch);
-  IFGF_CUDA(cudaGetLastError());
-  P->launches += 5;
-}
-
-// IFGF_PROP_DMMA over a whole level (chunks from build_dmma_extras).
-bool launch_propagation_gemm(ifgf_plan* P, int d, const double2* child, double2* parent,
-                             cudaStream_t s) {
-  PropTiles& T = P->tiles[d];
-  const Level& U = P->lv[d - 1];
-  const Level& L = P->lv[d];
-  const InterpConsts& K = P->K;
-  bool done = false;
-  dispatch_mma_orders(K.ps, K.pt, K.pp, [&](auto A, auto B, auto C) {
-    constexpr int PS = decltype(A)::value, PT = decltype(B)::value, PP = decltype(C)::value;
-    using S3 = G3Shape<PS, PT, PP>;
-    if constexpr (S3::ok) {
-      const size_t sm = S3::smem;
-      auto launch = [&](auto kern) {
-        IFGF_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-        kern<<<T.nchunks, kG3Warps * 32, sm, s>>>(U.dev(), L.dev(), K, tiles_dev(T), P->kappa,
-                                                   T.nchunks, child, parent, P->err);
-        IFGF_CUDA(cudaGetLastError());
-      };
-      P->kappa == 0.0 ? launch(k_propagate_gemm<PS, PT, PP, true>)
-                      : launch(k_propagate_gemm<PS, PT, PP, false>);
-      ++P->launches;
-      done = true;
-    }
-  });
-  return done;
-}
-
-
-// Warp-GEMM tables of child level d, built on first use: the A operand of
-// every row tile, the zero block, and the parent cones sorted (stably) by
-// (group of consecutive parent boxes, gamma index, child mask) and cut into
-// units of <= kG4Cones cones sharing (group, gamma).  The group is sized for
-// ~8 units per gamma, capped so its child blocks (~48 MB) stay in L2 while
-// its units run.
-void build_wgemm_extras(ifgf_plan* P, int d, cudaStream_t s) {
-  PropTiles& T = P->tiles[d];
-  const Level& U = P->lv[d - 1];
-  const Level& L = P->lv[d];
-  const InterpConsts& K = P->K;
-  const uint32_t ntiles = T.ngamma * 8;
-  auto tmp = [&](size_t b) { return (void*)P->alloc<char>(b); };
-  uint32_t nrt = 0;
-  IFGF_CUDA(cudaMemcpyAsync(&nrt, T.rt_off + ntiles, 4, cudaMemcpyDeviceToHost, s));
-  IFGF_CUDA(cudaStreamSynchronize(s));
   uint32_t* rt_tile = P->alloc<uint32_t>(nrt + 1);
   k_tile_rows<<<nblk(ntiles, 64), 64, 0, s>>>(ntiles, K.P, T.e_gc, nullptr, nullptr, T.rt_off,
                                               T.rt, nullptr, nullptr, nullptr, rt_tile);
@@ -1748,6 +1339,20 @@ void build_wgemm_extras(ifgf_plan* P, int d, cudaStream_t s) {
                                                         reinterpret_cast<WgRow*>(T.rtab));
   T.zblock = P->alloc<double2>((size_t)K.Pst + 8);
   IFGF_CUDA(cudaMemsetAsync(T.zblock, 0, ((size_t)K.Pst + 8) * sizeof(double2), s));
+  P->launches += 4;
+}
+
+// Warp units of the parent cones [qb, qe) of level d - 1 (the whole level, or
+// a rank's interval): sorted (stably) by (gamma index, child mask), cut into
+// units of <= kG4Cones cones sharing gamma.  A cone's result does not depend
+// on the unit it lands in (MMA columns are independent), so a rank plan's
+// blocks equal the single-GPU plan's bitwise.
+void build_wgemm_units(ifgf_plan* P, int d, uint32_t qb, uint32_t qe, cudaStream_t s) {
+  PropTiles& T = P->tiles[d];
+  const Level& U = P->lv[d - 1];
+  const Level& L = P->lv[d];
+  const uint32_t n = qe - qb;
+  auto tmp = [&](size_t b) { return (void*)P->alloc<char>(b); };
   // One box group = the whole level (gamma-major order) measured best at C2
   // (d = 8: 5.8 ms against 6.8 ms with 193-box groups sized for L2): longer
   // (gamma, mask) runs fill the units and align their child masks, and the
@@ -1757,46 +1362,49 @@ void build_wgemm_extras(ifgf_plan* P, int d, cudaStream_t s) {
     return v ? std::atoi(v) : 0;
   }();
   const uint32_t bg = bg_env > 0 ? (uint32_t)bg_env : std::max<uint32_t>(1, U.nb);
-  uint32_t* qidx = P->alloc<uint32_t>(U.nc);
-  uint64_t* key = P->alloc<uint64_t>(U.nc);
-  uint64_t* gsorted = P->alloc<uint64_t>(U.nc);
-  T.usorted = P->alloc<uint32_t>(U.nc);
+  uint32_t* qidx = P->alloc<uint32_t>(n);
+  uint64_t* key = P->alloc<uint64_t>(n);
+  uint64_t* gsorted = P->alloc<uint64_t>(n);
+  T.usorted = P->alloc<uint32_t>(n);
   {
-    k_wgemm_keys<<<nblk(U.nc), 256, 0, s>>>(U.dev(), L.dev(), T.cone_gidx, T.ngamma, bg, key, qidx);
+    k_wgemm_keys<<<nblk(n), 256, 0, s>>>(U.dev(), L.dev(), T.cone_gidx, T.ngamma, bg, qb, qe, key,
+                                         qidx);
     size_t tb = 0;
     int bits = 1;
     const uint64_t kmax = (((uint64_t)U.nb / bg + 1) * T.ngamma) << 8;
     while ((1ull << bits) < kmax && bits < 64) ++bits;
-    cub::DeviceRadixSort::SortPairs(nullptr, tb, key, gsorted, qidx, T.usorted, (int)U.nc, 0, bits,
+    cub::DeviceRadixSort::SortPairs(nullptr, tb, key, gsorted, qidx, T.usorted, (int)n, 0, bits,
                                     s);
     IFGF_CUDA(cub::DeviceRadixSort::SortPairs(tmp(tb), tb, key, gsorted, qidx, T.usorted,
-                                              (int)U.nc, 0, bits, s));
+                                              (int)n, 0, bits, s));
   }
-  uint32_t* flag = P->alloc<uint32_t>(U.nc + 1);
-  uint32_t* pos = P->alloc<uint32_t>(U.nc + 1);
+  uint32_t* flag = P->alloc<uint32_t>(n + 1);
+  uint32_t* pos = P->alloc<uint32_t>(n + 1);
   // units end where (group, gamma) changes; cutting at mask changes as well
   // (IFGF_G4_MASKCUT=1) leaves units of ~6 cones at C2 and is 2-3x slower
   static const bool maskcut = [] {
     const char* v = std::getenv("IFGF_G4_MASKCUT");
     return v && std::atoi(v) != 0;
   }();
-  k_chunk_flags<<<nblk(U.nc + 1), 256, 0, s>>>(gsorted, U.nc, kG4Cones, flag, maskcut ? 0 : 8);
+  k_chunk_flags<<<nblk(n + 1), 256, 0, s>>>(gsorted, n, kG4Cones, flag, maskcut ? 0 : 8);
   {
     size_t tb = 0;
-    cub::DeviceScan::ExclusiveSum(nullptr, tb, flag, pos, (int)(U.nc + 1), s);
-    IFGF_CUDA(cub::DeviceScan::ExclusiveSum(tmp(tb), tb, flag, pos, (int)(U.nc + 1), s));
+    cub::DeviceScan::ExclusiveSum(nullptr, tb, flag, pos, (int)(n + 1), s);
+    IFGF_CUDA(cub::DeviceScan::ExclusiveSum(tmp(tb), tb, flag, pos, (int)(n + 1), s));
   }
   uint32_t nu = 0;
-  IFGF_CUDA(cudaMemcpyAsync(&nu, pos + U.nc, 4, cudaMemcpyDeviceToHost, s));
+  IFGF_CUDA(cudaMemcpyAsync(&nu, pos + n, 4, cudaMemcpyDeviceToHost, s));
   IFGF_CUDA(cudaStreamSynchronize(s));
   T.nunits = nu;
   T.unit_start = P->alloc<uint32_t>(nu + 1);
-  k_chunk_starts<<<nblk(U.nc + 1), 256, 0, s>>>(flag, pos, U.nc, T.unit_start, nu);
+  k_chunk_starts<<<nblk(n + 1), 256, 0, s>>>(flag, pos, n, T.unit_start, nu);
   IFGF_CUDA(cudaGetLastError());
-  P->launches += 7;
+  P->launches += 5;
+  T.wg_qb = qb;
+  T.wg_qe = qe;
   if (std::getenv("IFGF_G4_TRACE"))
-    std::fprintf(stderr, "[wgemm] d=%d cones %u gammas %u row tiles %u box group %u units %u (%.2f cones/unit)\n",
-                 d, U.nc, T.ngamma, nrt, bg, nu, (double)U.nc / std::max(1u, nu));
+    std::fprintf(stderr, "[wgemm] d=%d cones [%u, %u) of %u gammas %u units %u (%.2f cones/unit)\n",
+                 d, qb, qe, U.nc, T.ngamma, nu, (double)n / std::max(1u, nu));
 }
 
 bool launch_propagation_wgemm(ifgf_plan* P, int d, const double2* child, double2* parent,
@@ -1835,20 +1443,30 @@ bool launch_propagation_mma(ifgf_plan* P, int d, uint32_t qb, uint32_t qe, const
   PropTiles& T = P->tiles[d];
   if (P->prop_kernel == IFGF_PROP_FLY || !T.enabled)
     return launch_propagation_fly(P, d, qb, qe, child, parent, s);
-  // IFGF_PROP_DMMA covers whole levels (its chunks span the level's cones);
-  // ranges (the pass-level API, rank plans) run the rows kernel
-  const bool full = qb == 0 && qe == P->lv[d - 1].nc;
-  if (P->prop_kernel == IFGF_PROP_DMMA && full) {
-    if (!T.rt) build_dmma_extras(P, d, s);
-    static const bool v3 = [] {
-      const char* v = std::getenv("IFGF_G4");
-      return v && std::atoi(v) == 0;
+  // The warp GEMM runs on the cone range its units were built for -- the
+  // first range a plan propagates at this level (the whole level, or a rank
+  // plan's interval); other ranges (pass-level API) run the rows kernel.
+  // IFGF_PROP_AUTO takes it where enough parent cones share each gamma to
+  // fill the units (C2: d = 8, 7, 6 with 12,280 / 1,679 / 216 cones per gamma;
+  // d = 5 with 23 stays with the rows: 12 cones per unit, 7.4 ms against 6.8)
+  if (P->prop_kernel == IFGF_PROP_DMMA || P->prop_kernel == IFGF_PROP_AUTO) {
+    static const double min_share = [] {
+      const char* v = std::getenv("IFGF_G4_MIN_SHARE");
+      return v ? std::atof(v) : 100.0;
     }();
-    if (!v3) {
+    const bool want = P->prop_kernel == IFGF_PROP_DMMA ||
+                      (double)P->lv[d - 1].nc >= min_share * (double)T.ngamma;
+    bool ok = false;
+    dispatch_mma_orders(P->K.ps, P->K.pt, P->K.pp, [&](auto A, auto B, auto C) {
+      ok = G4Shape<decltype(A)::value, decltype(B)::value, decltype(C)::value>::ok;
+    });
+    if (want && ok) {
       if (!T.rtab) build_wgemm_extras(P, d, s);
-      if (T.nunits > 0 && launch_propagation_wgemm(P, d, child, parent, s)) return true;
+      if (!T.usorted) build_wgemm_units(P, d, qb, qe, s);
+      if (T.wg_qb == qb && T.wg_qe == qe && T.nunits > 0 &&
+          launch_propagation_wgemm(P, d, child, parent, s))
+        return true;
     }
-    if (T.nchunks > 0 && launch_propagation_gemm(P, d, child, parent, s)) return true;
   }
   const Level& U = P->lv[d - 1];
   const Level& L = P->lv[d];

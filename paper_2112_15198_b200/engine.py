@@ -287,13 +287,13 @@ class Plan:
         """Run all apply kernels on one stream (exclusive per-pass timings)."""
         check(lib.ifgf_plan_set_option(self._h, 1, 1 if on else 0))
 
-    PROP_NODE, PROP_DMMA, PROP_ROWS, PROP_FLY = 0, 2, 3, 4
+    PROP_NODE, PROP_DMMA, PROP_ROWS, PROP_FLY, PROP_AUTO = 0, 2, 3, 4, 7
 
     NEAR_POINT, NEAR_BOX = 0, 1
 
     def set_option(self, option: int, value: int):
         """IFGF_OPT_* (include/ifgf_b200.h): 1 serial streams, 2 propagation
-        kernel (PROP_NODE, PROP_DMMA, PROP_ROWS default, PROP_FLY), 3 near-field kernel (NEAR_POINT, NEAR_BOX default),
+        kernel (PROP_NODE, PROP_DMMA, PROP_ROWS, PROP_FLY, PROP_AUTO default), 3 near-field kernel (NEAR_POINT, NEAR_BOX default),
         4 rank layout (PARTITION_COUNT default, PARTITION_WORK)."""
         check(lib.ifgf_plan_set_option(self._h, option, value))
 

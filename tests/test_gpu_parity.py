@@ -144,16 +144,17 @@ def test_direct_eval(built, gpu, oracle):
 
 
 def test_propagation_kernels_agree(built):
-    """The K3 implementations (per-node locate, FP64 DMMA box-batched GEMM,
-    register-blocked node rows from the tiles and grouped on the fly)
+    """The K3 implementations (per-node locate, the FP64 tensor-core warp GEMM
+    on every level, register-blocked node rows from the tiles and grouped on
+    the fly, and the default per-level choice between warp GEMM and rows)
     compute the same operator up to rounding; removed kernels are refused."""
     case, pc, cfg, ep, op, plan, prob = built
     res = []
-    kinds = (plan.PROP_NODE, plan.PROP_DMMA, plan.PROP_ROWS, plan.PROP_FLY)
+    kinds = (plan.PROP_NODE, plan.PROP_DMMA, plan.PROP_ROWS, plan.PROP_FLY, plan.PROP_AUTO)
     for kind in kinds:
         plan.set_prop_kernel(kind)
         res.append(plan.apply(pc.a_re, pc.a_im)[:2])
-    plan.set_prop_kernel(plan.PROP_ROWS)
+    plan.set_prop_kernel(plan.PROP_AUTO)
     for r in res[1:]:
         assert rel_l2(r[0], r[1], res[0][0], res[0][1]) <= 1e-13
     for removed in (1, 5, 6):

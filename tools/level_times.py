@@ -10,7 +10,7 @@ import time
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import paper_2112_15198_b200 as ifgf  # noqa: E402
 
-KINDS = {"node": 0, "dmma": 2, "rows": 3, "fly": 4}
+KINDS = {"node": 0, "dmma": 2, "rows": 3, "fly": 4, "auto": 7}
 c = ifgf.configs.CONFIGS[sys.argv[1]]
 pc = ifgf.generate(c.n, c.shape, c.c, c.dens, c.seed)
 cfg = ifgf.KernelConfig(ifgf.KernelKind(c.kind), c.kappa)
