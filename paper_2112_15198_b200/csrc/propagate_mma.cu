@@ -483,10 +483,17 @@ __device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b)
 #endif
 constexpr int kG4Warps = IFGF_G4_WARPS;
 constexpr int kG4Nct = IFGF_G4_NCT;       // column tiles (of 8 cones) per warp unit
-constexpr int kG4Cones = 8 * kG4Nct;
+#ifndef IFGF_G4_CONES
+#define IFGF_G4_CONES (8 * IFGF_G4_NCT)
+#endif
+constexpr int kG4Cones = IFGF_G4_CONES;   // cones per unit (<= 8 * kG4Nct)
+constexpr int kG4Cols = 8 * kG4Nct;
+#ifndef IFGF_G4_PF
+#define IFGF_G4_PF 6
+#endif
 
 constexpr int g4_prefetch(int nch) {
-  for (int pf = 6; pf > 1; --pf)
+  for (int pf = IFGF_G4_PF; pf > 1; --pf)
     if (nch % pf == 0) return pf;
   return 1;
 }
@@ -523,8 +530,8 @@ __global__ void __launch_bounds__(kG4Warps * 32, 1)
   constexpr int P = PS * PT * PP, NCH = (BL::Pst + 7) / 8, PF = g4_prefetch(NCH);
   constexpr bool kTail = (BL::Pst % 8) != 0;  // last chunk reaches past the block
   extern __shared__ double2 smem[];
-  __shared__ uint32_t s_q[kG4Warps][kG4Cones];
-  __shared__ uint32_t s_cb[kG4Warps][8][kG4Cones];   // child box per octant (kNone: absent)
+  __shared__ uint32_t s_q[kG4Warps][kG4Cols];
+  __shared__ uint32_t s_cb[kG4Warps][8][kG4Cols];   // child box per octant (kNone: absent)
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, NW = blockDim.x >> 5;
   const int kq = lane & 3, nn = lane >> 2;
   double2* acc = smem + (size_t)w * kG4Cones * P;  // [kG4Cones][P] node values
@@ -542,7 +549,7 @@ __global__ void __launch_bounds__(kG4Warps * 32, 1)
     const int nq = (int)(c1 - c0);
     for (int i = lane; i < kG4Cones * P; i += 32) acc[i] = make_double2(0.0, 0.0);
     uint32_t omask = 0;
-    if (lane < kG4Cones) {
+    if (lane < kG4Cols) {
       const uint32_t q = lane < nq ? T.usorted[c0 + lane] : kNone;
       s_q[w][lane] = q;
       uint32_t cbo[8];
@@ -584,151 +591,158 @@ __global__ void __launch_bounds__(kG4Warps * 32, 1)
         }
       }
     };
-    struct Pend {  // find_cone in flight: bitmap word, rank, bit (64: absent child)
-      uint64_t wd;
-      uint32_t rk, bit;
-    };
-    auto lookup = [&](const Inst& it, uint32_t gc, Pend (&pd)[kG4Nct]) {
-#pragma unroll
-      for (int u = 0; u < kG4Nct; ++u) {
-        const uint32_t cb = it.o < 8 ? s_cb[w][it.o][u * 8 + nn] : kNone;
-        pd[u].wd = 0;
-        pd[u].rk = 0;
-        pd[u].bit = 64;
-        if (cb != kNone) {
-          const uint64_t idx = (uint64_t)cb * L.G + gc;
-          pd[u].wd = __ldg(&L.bits[idx >> 6]);
-          pd[u].rk = __ldg(&L.rank[idx >> 6]);
-          pd[u].bit = (uint32_t)(idx & 63);
-        }
-      }
-    };
-    auto resolve = [&](const Pend (&pd)[kG4Nct], const double2* (&bpo)[kG4Nct]) {
-#pragma unroll
-      for (int u = 0; u < kG4Nct; ++u) {
-        const double2* p = zblock;
-        if (pd[u].bit < 64) {
-          const uint64_t bit = 1ull << pd[u].bit;
-          if (pd[u].wd & bit)
-            p = child + (size_t)(pd[u].rk + (uint32_t)__popcll(pd[u].wd & (bit - 1))) * BL::Pst;
-          else
-            raise_err(err, kErrPropCover);
-        }
-        bpo[u] = p + 2 * kq;
-      }
-    };
-    Inst i0 = {-1, 0, 0};
-    advance(i0);
-    Inst i1 = i0;
-    if (i1.o < 8) advance(i1);
-    Inst i2 = i1;
-    if (i2.o < 8) advance(i2);
-    uint32_t g2 = i2.o < 8 ? __ldg(&T.rt[i2.r].x) : 0;
-    const double2* bp[kG4Nct];
-    double4 bq[PF][kG4Nct];
-    Pend pd[kG4Nct];
-    WgRow rec = {0.0, 0.0, 0.0, 0.0, 0.0, -1};
-    if (i0.o < 8) {
-      lookup(i0, __ldg(&T.rt[i0.r].x), pd);
-      rec = rtab[(size_t)i0.r * 8 + nn];
-    } else {
-      lookup(i0, 0, pd);
-    }
-    resolve(pd, bp);
-#pragma unroll
-    for (int c = 0; c < PF; ++c)
-#pragma unroll
-      for (int u = 0; u < kG4Nct; ++u) bq[c][u] = bload(bp[u], c);
-    lookup(i1, i1.o < 8 ? __ldg(&T.rt[i1.r].x) : 0, pd);
-    while (i0.o < 8) {
-      // instance i1: its cones are resolved now (requested one instance ago);
-      // instance i2: request its bitmap words; instance i3: its child gamma
-      const double2* bpn[kG4Nct];
-      resolve(pd, bpn);
-      lookup(i2, g2, pd);
-      Inst i3 = i2;
-      if (i3.o < 8) advance(i3);
-      g2 = i3.o < 8 ? __ldg(&T.rt[i3.r].x) : 0;
-      const WgRow recn = rtab[(size_t)(i1.o < 8 ? i1.r : i0.r) * 8 + nn];
-      // basis of this lane's node: Ts and the theta-phi products
-      double Ts[PS], WP[PT * PP];
-      {
-        double Tt[PT], Tp[PP];
-        cheb_basis<PS>(rec.ts, Ts);
-        cheb_basis<PT>(rec.tt, Tt);
-        cheb_basis<PP>(rec.tp, Tp);
-        if (rec.m < 0) {
-#pragma unroll
-          for (int k2 = 0; k2 < PS; ++k2) Ts[k2] = 0.0;
-        }
-#pragma unroll
-        for (int t = 0; t < PT; ++t)
-#pragma unroll
-          for (int p2 = 0; p2 < PP; ++p2) WP[t * PP + p2] = Tt[t] * Tp[p2];
-      }
-      double dr[kG4Nct][2], di[kG4Nct][2];
-#pragma unroll
-      for (int u = 0; u < kG4Nct; ++u) dr[u][0] = dr[u][1] = di[u][0] = di[u][1] = 0.0;
-#pragma unroll
-      for (int c = 0; c < NCH; ++c) {
-        // A fragments of the chunk: the lane's two coefficients
-        double a[2];
-#pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          double wv[4], sv[4];
-#pragma unroll
-          for (int k2 = 0; k2 < 4; ++k2) {
-            const int e = 8 * c + 2 * k2 + h;
-            const bool real = e < BL::Pst && e % BL::PL < PT * PP;
-            wv[k2] = real ? WP[real ? e % BL::PL : 0] : 0.0;
-            sv[k2] = real ? Ts[real ? e / BL::PL : 0] : 0.0;
+    // NU column tiles: units of <= 8 cones skip the second tile
+    auto run_stream = [&](auto NUc) {
+      constexpr int NU = decltype(NUc)::value;
+      struct Pend {  // find_cone in flight: bitmap word, rank, bit (64: absent child)
+        uint64_t wd;
+        uint32_t rk, bit;
+      };
+      auto lookup = [&](const Inst& it, uint32_t gc, Pend (&pd)[NU]) {
+  #pragma unroll
+        for (int u = 0; u < NU; ++u) {
+          const uint32_t cb = it.o < 8 ? s_cb[w][it.o][u * 8 + nn] : kNone;
+          pd[u].wd = 0;
+          pd[u].rk = 0;
+          pd[u].bit = 64;
+          if (cb != kNone) {
+            const uint64_t idx = (uint64_t)cb * L.G + gc;
+            pd[u].wd = __ldg(&L.bits[idx >> 6]);
+            pd[u].rk = __ldg(&L.rank[idx >> 6]);
+            pd[u].bit = (uint32_t)(idx & 63);
           }
-          a[h] = sel4(kq, sv[0], sv[1], sv[2], sv[3]) * sel4(kq, wv[0], wv[1], wv[2], wv[3]);
         }
-        double4 b[kG4Nct];
-#pragma unroll
-        for (int u = 0; u < kG4Nct; ++u) b[u] = bq[c % PF][u];
-#pragma unroll
-        for (int u = 0; u < kG4Nct; ++u) {
-          dmma(dr[u][0], dr[u][1], a[0], b[u].x);
-          dmma(di[u][0], di[u][1], a[0], b[u].y);
+      };
+      auto resolve = [&](const Pend (&pd)[NU], const double2* (&bpo)[NU]) {
+  #pragma unroll
+        for (int u = 0; u < NU; ++u) {
+          const double2* p = zblock;
+          if (pd[u].bit < 64) {
+            const uint64_t bit = 1ull << pd[u].bit;
+            if (pd[u].wd & bit)
+              p = child + (size_t)(pd[u].rk + (uint32_t)__popcll(pd[u].wd & (bit - 1))) * BL::Pst;
+            else
+              raise_err(err, kErrPropCover);
+          }
+          bpo[u] = p + 2 * kq;
         }
-#pragma unroll
-        for (int u = 0; u < kG4Nct; ++u) {
-          dmma(dr[u][0], dr[u][1], a[1], b[u].z);
-          dmma(di[u][0], di[u][1], a[1], b[u].w);
-          bq[c % PF][u] = c + PF < NCH ? bload(bp[u], c + PF) : bload(bpn[u], c + PF - NCH);
-        }
+      };
+      Inst i0 = {-1, 0, 0};
+      advance(i0);
+      Inst i1 = i0;
+      if (i1.o < 8) advance(i1);
+      Inst i2 = i1;
+      if (i2.o < 8) advance(i2);
+      uint32_t g2 = i2.o < 8 ? __ldg(&T.rt[i2.r].x) : 0;
+      const double2* bp[NU];
+      double4 bq[PF][NU];
+      Pend pd[NU];
+      WgRow rec = {0.0, 0.0, 0.0, 0.0, 0.0, -1};
+      if (i0.o < 8) {
+        lookup(i0, __ldg(&T.rt[i0.r].x), pd);
+        rec = rtab[(size_t)i0.r * 8 + nn];
+      } else {
+        lookup(i0, 0, pd);
       }
-      // epilogue: D row nn = node m, columns 2 kq + h = cones of the tile
-      if (rec.m >= 0) {
-        const int m = (int)rec.m;
-#pragma unroll
-        for (int u = 0; u < kG4Nct; ++u)
-#pragma unroll
+      resolve(pd, bp);
+  #pragma unroll
+      for (int c = 0; c < PF; ++c)
+  #pragma unroll
+        for (int u = 0; u < NU; ++u) bq[c][u] = bload(bp[u], c);
+      lookup(i1, i1.o < 8 ? __ldg(&T.rt[i1.r].x) : 0, pd);
+      while (i0.o < 8) {
+        // instance i1: its cones are resolved now (requested one instance ago);
+        // instance i2: request its bitmap words; instance i3: its child gamma
+        const double2* bpn[NU];
+        resolve(pd, bpn);
+        lookup(i2, g2, pd);
+        Inst i3 = i2;
+        if (i3.o < 8) advance(i3);
+        g2 = i3.o < 8 ? __ldg(&T.rt[i3.r].x) : 0;
+        const WgRow recn = rtab[(size_t)(i1.o < 8 ? i1.r : i0.r) * 8 + nn];
+        // basis of this lane's node: Ts and the theta-phi products
+        double Ts[PS], WP[PT * PP];
+        {
+          double Tt[PT], Tp[PP];
+          cheb_basis<PS>(rec.ts, Ts);
+          cheb_basis<PT>(rec.tt, Tt);
+          cheb_basis<PP>(rec.tp, Tp);
+          if (rec.m < 0) {
+  #pragma unroll
+            for (int k2 = 0; k2 < PS; ++k2) Ts[k2] = 0.0;
+          }
+  #pragma unroll
+          for (int t = 0; t < PT; ++t)
+  #pragma unroll
+            for (int p2 = 0; p2 < PP; ++p2) WP[t * PP + p2] = Tt[t] * Tp[p2];
+        }
+        double dr[NU][2], di[NU][2];
+  #pragma unroll
+        for (int u = 0; u < NU; ++u) dr[u][0] = dr[u][1] = di[u][0] = di[u][1] = 0.0;
+  #pragma unroll
+        for (int c = 0; c < NCH; ++c) {
+          // A fragments of the chunk: the lane's two coefficients
+          double a[2];
+  #pragma unroll
           for (int h = 0; h < 2; ++h) {
-            const double vr = dr[u][h], vi = di[u][h];
-            double2* p = acc + (size_t)(u * 8 + 2 * kq + h) * P + m;
-            double2 v = *p;
-            if (LAP) {
-              v.x = fma(vr, rec.tfx, v.x);
-              v.y = fma(vi, rec.tfx, v.y);
-            } else {
-              v.x = fma(vr, rec.tfx, fma(-vi, rec.tfy, v.x));
-              v.y = fma(vr, rec.tfy, fma(vi, rec.tfx, v.y));
+            double wv[4], sv[4];
+  #pragma unroll
+            for (int k2 = 0; k2 < 4; ++k2) {
+              const int e = 8 * c + 2 * k2 + h;
+              const bool real = e < BL::Pst && e % BL::PL < PT * PP;
+              wv[k2] = real ? WP[real ? e % BL::PL : 0] : 0.0;
+              sv[k2] = real ? Ts[real ? e / BL::PL : 0] : 0.0;
             }
-            *p = v;
+            a[h] = sel4(kq, sv[0], sv[1], sv[2], sv[3]) * sel4(kq, wv[0], wv[1], wv[2], wv[3]);
           }
+          double4 b[NU];
+  #pragma unroll
+          for (int u = 0; u < NU; ++u) b[u] = bq[c % PF][u];
+  #pragma unroll
+          for (int u = 0; u < NU; ++u) {
+            dmma(dr[u][0], dr[u][1], a[0], b[u].x);
+            dmma(di[u][0], di[u][1], a[0], b[u].y);
+          }
+  #pragma unroll
+          for (int u = 0; u < NU; ++u) {
+            dmma(dr[u][0], dr[u][1], a[1], b[u].z);
+            dmma(di[u][0], di[u][1], a[1], b[u].w);
+            bq[c % PF][u] = c + PF < NCH ? bload(bp[u], c + PF) : bload(bpn[u], c + PF - NCH);
+          }
+        }
+        // epilogue: D row nn = node m, columns 2 kq + h = cones of the tile
+        if (rec.m >= 0) {
+          const int m = (int)rec.m;
+  #pragma unroll
+          for (int u = 0; u < NU; ++u)
+  #pragma unroll
+            for (int h = 0; h < 2; ++h) {
+              if (kG4Cones < kG4Cols && u * 8 + 2 * kq + h >= kG4Cones) continue;
+              const double vr = dr[u][h], vi = di[u][h];
+              double2* p = acc + (size_t)(u * 8 + 2 * kq + h) * P + m;
+              double2 v = *p;
+              if (LAP) {
+                v.x = fma(vr, rec.tfx, v.x);
+                v.y = fma(vi, rec.tfx, v.y);
+              } else {
+                v.x = fma(vr, rec.tfx, fma(-vi, rec.tfy, v.x));
+                v.y = fma(vr, rec.tfy, fma(vi, rec.tfx, v.y));
+              }
+              *p = v;
+            }
+        }
+        // the next octant's row tiles touch the same (cone, node) slots from other lanes
+        if (i1.o != i0.o) __syncwarp();
+        i0 = i1;
+        i1 = i2;
+        i2 = i3;
+        rec = recn;
+  #pragma unroll
+        for (int u = 0; u < NU; ++u) bp[u] = bpn[u];
       }
-      // the next octant's row tiles touch the same (cone, node) slots from other lanes
-      if (i1.o != i0.o) __syncwarp();
-      i0 = i1;
-      i1 = i2;
-      i2 = i3;
-      rec = recn;
-#pragma unroll
-      for (int u = 0; u < kG4Nct; ++u) bp[u] = bpn[u];
-    }
+    };
+    if (kG4Nct == 2 && nq <= 8) run_stream(std::integral_constant<int, 1>{});
+    else run_stream(std::integral_constant<int, kG4Nct>{});
     __syncwarp();
     // flagged nodes: per-box exact locate + evaluation (rare), after the MMA
     // contributions, octants in Morton order
@@ -1454,8 +1468,11 @@ bool launch_propagation_mma(ifgf_plan* P, int d, uint32_t qb, uint32_t qe, const
       const char* v = std::getenv("IFGF_G4_MIN_SHARE");
       return v ? std::atof(v) : 100.0;
     }();
+    // ... and enough cones for several units per resident warp (C1's
+    // 44,522-cone level: rows 0.30 ms, warp GEMM 0.36)
     const bool want = P->prop_kernel == IFGF_PROP_DMMA ||
-                      (double)P->lv[d - 1].nc >= min_share * (double)T.ngamma;
+                      ((double)(qe - qb) >= min_share * (double)T.ngamma &&
+                       (size_t)(qe - qb) >= (size_t)4 * 148 * kG4Warps * kG4Cones);
     bool ok = false;
     dispatch_mma_orders(P->K.ps, P->K.pt, P->K.pp, [&](auto A, auto B, auto C) {
       ok = G4Shape<decltype(A)::value, decltype(B)::value, decltype(C)::value>::ok;
