@@ -1464,15 +1464,18 @@ bool launch_propagation_mma(ifgf_plan* P, int d, uint32_t qb, uint32_t qe, const
   // fill the units (C2: d = 8, 7, 6 with 12,280 / 1,679 / 216 cones per gamma;
   // d = 5 with 23 stays with the rows: 12 cones per unit, 7.4 ms against 6.8)
   if (P->prop_kernel == IFGF_PROP_DMMA || P->prop_kernel == IFGF_PROP_AUTO) {
-    static const double min_share = [] {
-      const char* v = std::getenv("IFGF_G4_MIN_SHARE");
-      return v ? std::atof(v) : 100.0;
-    }();
-    // ... and enough cones for several units per resident warp (C1's
-    // 44,522-cone level: rows 0.30 ms, warp GEMM 0.36)
+    // (the level's totals, not the range's: every rank plan of a group takes
+    // the same kernel as the single-GPU plan, so their blocks agree bitwise).
+    // IFGF_G4_MIN_SHARE / IFGF_G4_MIN_CONES override the thresholds (tests).
+    const char* ev = std::getenv("IFGF_G4_MIN_SHARE");
+    const double min_share = ev ? std::atof(ev) : 100.0;
+    ev = std::getenv("IFGF_G4_MIN_CONES");
+    // several units per resident warp (C1's 44,522-cone level: rows 0.30 ms,
+    // warp GEMM 0.36)
+    const double min_cones = ev ? std::atof(ev) : 4.0 * 148 * kG4Warps * kG4Cones;
+    const double lnc = (double)P->lv[d - 1].nc;
     const bool want = P->prop_kernel == IFGF_PROP_DMMA ||
-                      ((double)(qe - qb) >= min_share * (double)T.ngamma &&
-                       (size_t)(qe - qb) >= (size_t)4 * 148 * kG4Warps * kG4Cones);
+                      (lnc >= min_share * (double)T.ngamma && lnc >= min_cones);
     bool ok = false;
     dispatch_mma_orders(P->K.ps, P->K.pt, P->K.pp, [&](auto A, auto B, auto C) {
       ok = G4Shape<decltype(A)::value, decltype(B)::value, decltype(C)::value>::ok;

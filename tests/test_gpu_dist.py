@@ -11,7 +11,7 @@ import math
 import numpy as np
 import pytest
 
-from bindings import Params
+from bindings import Params, rel_l2
 
 pytestmark = pytest.mark.gpu
 
@@ -67,6 +67,26 @@ def test_rank_group_bitwise_equal_single_gpu(gpu, case, R):
             sum(i.levels[k]["halo_cones"] for i in infos)
     if R == 1:
         assert all(lv["halo_cones"] == 0 for lv in infos[0].levels)
+
+
+@pytest.mark.parametrize("R", [2, 3])
+def test_rank_group_bitwise_equal_with_warp_gemm(gpu, case, R, monkeypatch):
+    """With the warp GEMM taken at every level that has the precomputed
+    geometry (thresholds lifted), rank plans -- whose units cover only their
+    cone intervals -- still reproduce the single-GPU blocks bitwise: a cone's
+    result does not depend on the unit it is batched into."""
+    from paper_2112_15198_b200.dist import run_distributed
+    monkeypatch.setenv("IFGF_G4_MIN_SHARE", "0")
+    monkeypatch.setenv("IFGF_G4_MIN_CONES", "0")
+    pc, cfg = case
+    s_re, s_im, _ = _single(gpu, pc, cfg)
+    q = pc.copy()
+    run_distributed(q, cfg, gpu.EngineParams(), R)
+    assert np.array_equal(q.i_re, s_re) and np.array_equal(q.i_im, s_im)
+    monkeypatch.delenv("IFGF_G4_MIN_SHARE")
+    monkeypatch.delenv("IFGF_G4_MIN_CONES")
+    r_re, r_im, _ = _single(gpu, pc, cfg)
+    assert rel_l2(s_re, s_im, r_re, r_im) <= 1e-13
 
 
 def test_rank_group_counters_match_reference(gpu, ref, case):
