@@ -316,11 +316,14 @@ __global__ void k_mark_points(const __grid_constant__ LevelDev L, const uint32_t
   const double x = xs[i], y = ys[i], z = zs[i];
   for (uint32_t ci = L.cous_off[b]; ci < L.cous_off[b + 1]; ++ci) {
     const uint32_t cb = L.cous[ci];
+    const double cx = L.cx[cb], cy = L.cy[cb], cz = L.cz[cb];
     uint32_t g;
-    const int e = cone_of_point_fast(L, trig, L.cx[cb], L.cy[cb], L.cz[cb], x, y, z, g);
-    if (e) {
-      raise_err(err, e);
-      return;
+    if (!cone_index_f32(L, cx, cy, cz, x, y, z, g)) {
+      const int e = cone_of_point_fast(L, trig, cx, cy, cz, x, y, z, g);
+      if (e) {
+        raise_err(err, e);
+        return;
+      }
     }
     set_bit_warp(bits, (uint64_t)cb * L.G + g);
   }
@@ -343,11 +346,14 @@ __global__ void k_mark_nodes(const __grid_constant__ LevelDev L, const __grid_co
   double x, y, z;
   node_position(sm, U.rad, U.cx[pb], U.cy[pb], U.cz[pb], K.ns[js], K.nt[jt], K.np[jp], x, y, z);
   for (uint32_t cb = U.child_begin[pb]; cb < U.child_begin[pb + 1]; ++cb) {
+    const double cx = L.cx[cb], cy = L.cy[cb], cz = L.cz[cb];
     uint32_t g;
-    const int e = cone_of_point_fast(L, trig, L.cx[cb], L.cy[cb], L.cz[cb], x, y, z, g);
-    if (e) {
-      raise_err(err, e);
-      return;
+    if (!cone_index_f32(L, cx, cy, cz, x, y, z, g)) {
+      const int e = cone_of_point_fast(L, trig, cx, cy, cz, x, y, z, g);
+      if (e) {
+        raise_err(err, e);
+        return;
+      }
     }
     set_bit_warp(bits, (uint64_t)cb * L.G + g);
   }
