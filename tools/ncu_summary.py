@@ -17,6 +17,10 @@ METRICS = {
     "dram_read_bytes": "dram__bytes_read.sum",
     "dram_write_bytes": "dram__bytes_write.sum",
     "fp64_pipe_active_pct": "sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active",
+    "tensor_pipe_active_pct": "sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active",
+    "l2_throughput_pct": "lts__throughput.avg.pct_of_peak_sustained_elapsed",
+    "l2_hit_pct": "lts__t_sector_hit_rate.pct",
+    "l2_to_l1_read_bytes": "l1tex__m_xbar2l1tex_read_bytes.sum",
     "l1_lsu_wavefronts_pct": "l1tex__data_pipe_lsu_wavefronts.avg.pct_of_peak_sustained_elapsed",
     "l1_hit_pct": "l1tex__t_sector_pipe_lsu_mem_global_op_ld_hit_rate.pct",
     "issue_active_pct": "sm__inst_issued.avg.pct_of_peak_sustained_active",
@@ -54,7 +58,7 @@ def main(rep, out_prefix):
                 if k == "duration_us" and v is not None:
                     v = v * {"ns": 1e-3, "nsecond": 1e-3, "ms": 1e3, "msecond": 1e3,
                              "s": 1e6, "second": 1e6}.get(u, 1.0)
-                if k.startswith("dram_") and v is not None:
+                if (k.startswith("dram_") or k.endswith("_bytes")) and v is not None:
                     scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9,
                              "KB": 1e3, "MB": 1e6, "GB": 1e9}.get(u, 1)
                     v = v * scale
