@@ -423,8 +423,11 @@ def run_ours(args):
                 # transfer factor precomputed and K4/K1 use the 12-op table sincos,
                 # so the FP64 work actually executed per propagation evaluation
                 # is ~380 flop (186 FMA contraction + 4 FMA transfer), not 430.
+                # The warp GEMM (fine levels) executes 2 x 80 MMA FMAs per node
+                # slot, 89 % of the slots filled: ~360 flop + transfer per
+                # evaluation, the same ballpark.
                 "flop_model": "algorithmic (SURVEY.md 8(d)); executed ~380 of the 430 "
-                              "flop per propagation evaluation",
+                              "flop per propagation evaluation (rows; warp GEMM ~370)",
                 "frac_executed_estimate": (dk["frac_fp64"] * 380.0 / 430.0
                                            if dom == "propagation" else None)}
 
