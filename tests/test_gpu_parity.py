@@ -20,6 +20,10 @@ CASES = [
     ("helm_oblate", 6000, 1, 0.25, 0, 2 * math.pi * 2.0, 0, 13, (3, 5, 5)),
     ("helm_high_order", 3456, 0, 1.0, 0, 2 * math.pi * 2.0, 0, 14, (5, 7, 7)),
     ("helm_mid_order", 3456, 0, 1.0, 0, 2 * math.pi * 2.0, 0, 14, (4, 6, 6)),
+    # the other orders the warp GEMM serves (blocks of 30 and 64 coefficients:
+    # a short last K chunk, and K chunks that tile the block exactly)
+    ("helm_order_333", 3000, 0, 1.0, 0, 2 * math.pi * 1.5, 0, 15, (3, 3, 3)),
+    ("laplace_order_444", 3000, 0, 1.0, 1, 0.0, 1, 16, (4, 4, 4)),
 ]
 
 
