@@ -457,9 +457,9 @@ __device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b)
                : "d"(a), "d"(b));
 }
 
-// ---------------------------------------------------------------- K3 v4
-// Warp GEMM.  A warp owns a unit of <= 8 * kG4Nct parent cones that share
-// gamma (and the octants of their children) from start to finish: node values
+// ------------------------------------------------------------ K3 warp GEMM
+// A warp owns a unit of <= 8 * kG4Nct parent cones that share gamma (and,
+// mostly, the octants of their children) from start to finish: node values
 // in its own shared-memory accumulator, children in Morton order, then the
 // fit.  No CTA barriers and no work shared between warps, so a warp's stalls
 // are its own.  Per child octant and row tile (<= 8 nodes sharing a child
@@ -470,11 +470,14 @@ __device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b)
 // coefficients (a quad covers 128 contiguous bytes of one block, so a warp's
 // load touches 8 lines for 1 KB -- the 128-bit version touched 8 lines for
 // 512 B and was bound by L1 wavefronts), feeding four MMAs (2 K steps x re,
-// im).  The loads run kPF chunks ahead in a register ring that continues into
+// im).  The loads run PF chunks ahead in a register ring that continues into
 // the next row tile.  A (basis products of the lane's node at its own 2
 // coefficients per chunk) is formed in registers per row tile: the 25
 // theta-phi products once, then a 4-way select by the lane's position in the
 // quad -- no table, no memory traffic.
+// Measured at C2 (DESIGN.md sections 3 and 9): 8 warps x 2 column tiles is the
+// optimum (12 warps x 15 cones at 168 registers, 16 warps x 1 tile, 6 and 4
+// warps are all slower); the macros below exist for those sweeps.
 #ifndef IFGF_G4_WARPS
 #define IFGF_G4_WARPS 8
 #endif
@@ -489,7 +492,7 @@ constexpr int kG4Nct = IFGF_G4_NCT;       // column tiles (of 8 cones) per warp 
 constexpr int kG4Cones = IFGF_G4_CONES;   // cones per unit (<= 8 * kG4Nct)
 constexpr int kG4Cols = 8 * kG4Nct;
 #ifndef IFGF_G4_PF
-#define IFGF_G4_PF 6
+#define IFGF_G4_PF 6   // largest ring depth tried; the ring takes a divisor of the chunk count
 #endif
 
 constexpr int g4_prefetch(int nch) {
