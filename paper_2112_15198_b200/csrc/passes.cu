@@ -328,7 +328,8 @@ __global__ void __launch_bounds__(320)
     sv[c * P + m] = make_double2(sr, si);
   }
   __syncthreads();
-  fit_cones<PS, PT, PP>(K, sv, st, ncon, out + (size_t)q0 * BlockLayout<PS, PT, PP>::Pst, err);
+  fit_cones_inplace<PS, PT, PP, true>(K, sv, ncon, out + (size_t)q0 * BlockLayout<PS, PT, PP>::Pst,
+                                      err);
 }
 
 // ------------------------------------------------------------ K3 propagation
