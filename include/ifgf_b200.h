@@ -128,9 +128,13 @@ void ifgf_plan_destroy(ifgf_plan* plan);
  *   IFGF_NEAR_BOX   (1, default) warp per target box, the box's neighbour
  *                       sources staged in shared memory and split across
  *                       lanes, several targets per pass.
- *   Both agree to rounding. */
+ *   Both agree to rounding.
+ * IFGF_OPT_K4_RECORDS = 0: the interpolation pass locates every (point,
+ *   cousin) pair again instead of reading the plan's locate records (kept by
+ *   single-GPU plans whose records fit in 15 % of the device memory; same
+ *   result bitwise).  Default 1. */
 enum { IFGF_OPT_SERIAL = 1, IFGF_OPT_PROP_KERNEL = 2, IFGF_OPT_NEAR_KERNEL = 3,
-       IFGF_OPT_PARTITION = 4 };
+       IFGF_OPT_PARTITION = 4, IFGF_OPT_K4_RECORDS = 5 };
 enum { IFGF_NEAR_POINT = 0, IFGF_NEAR_BOX = 1 };
 /* IFGF_OPT_PARTITION selects the rank layout of ifgf_plan_partition and
  * ifgf_plan_exchange_set:

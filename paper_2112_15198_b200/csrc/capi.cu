@@ -235,6 +235,14 @@ void plan_free(ifgf_plan* P) {
   delete P;
 }
 
+// Plans of a rank group keep no K4 locate records (each would hold the whole
+// cloud's; several rank plans share one device in the in-process groups).
+thread_local bool tl_rank_plan = false;
+struct RankPlanScope {
+  RankPlanScope() { tl_rank_plan = true; }
+  ~RankPlanScope() { tl_rank_plan = false; }
+};
+
 ifgf_plan* new_plan(size_t n, int kind, double wavenumber, const ifgf_params* p) {
   if (n < 1) throw Error(IFGF_EINVAL, "empty point cloud");
   if (n > 0xffffffffull) throw Error(IFGF_EINVAL, "more than 2^32 points");
@@ -254,6 +262,7 @@ ifgf_plan* new_plan(size_t n, int kind, double wavenumber, const ifgf_params* p)
     throw Error(IFGF_EINVAL, "unknown partition mode");
   P->partition_mode = p->partition;
   P->mem_budget = device_memory_budget(P->device);
+  P->k4_records = !tl_rank_plan;
   try {
     P->s_main = take_stream(P->device);
     P->s_aux = take_stream(P->device);
@@ -717,6 +726,8 @@ int ifgf_plan_set_option(ifgf_plan* P, int option, int value) {
       if (value < IFGF_NEAR_POINT || value > IFGF_NEAR_BOX)
         throw Error(IFGF_EINVAL, "unknown near-field kernel");
       P->near_kernel = value;
+    } else if (option == IFGF_OPT_K4_RECORDS) {
+      P->k4_records = value != 0;
     } else {
       throw Error(IFGF_EINVAL, "unknown option");
     }
@@ -1212,6 +1223,7 @@ int ifgf_dist_plan_create_device(ifgf_comm* comm, const double* dx, const double
     if (!p) throw Error(IFGF_EINVAL, "null params");
     ifgf_params q = *p;
     q.device = comm->device;
+    RankPlanScope rank_scope;
     ifgf_plan* P = new_plan(n, kind, k, &q);
     try {
       cudaEvent_t e;
@@ -1269,6 +1281,7 @@ int ifgf_run_distributed(size_t n, const double* x1, const double* x2, const dou
       }
     } fr{G};
     const auto t0 = clk::now();
+    RankPlanScope rank_scope;
     for (int r = 0; r < R; ++r) {
       ifgf_params q = *p;
       q.device = devices ? devices[r] : p->device;

@@ -518,6 +518,336 @@ __global__ void __launch_bounds__(128, IFGF_INTERP_MINB)
     }
 }
 
+// K4 from the plan's locate records (LevelDev::rec / rec_g, setup.cu
+// k_locate_points + k_rec_cones): the same work items, cousin order and sums
+// as k_interp with the cone ordinal, the local coordinates and the kernel
+// factor of every (point, cousin) pair read back instead of recomputed --
+// bitwise the same result.
+//
+// k_interp_rec: blocks streamed per thread from global memory (any orders).
+// k_interp_stg: blocks staged in shared memory.  Without the locate K4 is
+// bound by the L1 tag stage: every lane streams its own 1.2 KB block, ~30
+// different lines per warp load (ncu: L1 wavefronts 74 %, FP64 pipe 28 %).
+// Neighbouring points mostly see the same few cones of a cousin, so per
+// cousin step the warp finds the distinct blocks among its 64 (lane, point)
+// pairs (match.any), copies each once with coalesced cp.async into one of S
+// padded slots (slot stride = block + 16 B, so the lanes' reads of different
+// slots fall into different banks), one step ahead of the evaluation (two
+// slot sets per warp), and every lane evaluates from its slot.  Pairs beyond
+// S distinct blocks read from global memory as before.  No CTA barriers.
+// The records of one work item and cousin: R slots per plane, read with one
+// aligned vector load per plane for R = 2.
+template <int R, bool LAP>
+struct RecSet {
+  uint32_t g[R];
+  double ts[R], tt[R], tp[R], gr[R], gi[R];
+  __device__ __forceinline__ void load(const uint32_t* __restrict__ rec_g,
+                                       const double* __restrict__ rec, uint64_t np, uint64_t idx) {
+    if constexpr (R == 2) {
+      const uint2 q = *reinterpret_cast<const uint2*>(rec_g + idx);
+      g[0] = q.x, g[1] = q.y;
+      double2 v = *reinterpret_cast<const double2*>(rec + idx);
+      ts[0] = v.x, ts[1] = v.y;
+      v = *reinterpret_cast<const double2*>(rec + np + idx);
+      tt[0] = v.x, tt[1] = v.y;
+      v = *reinterpret_cast<const double2*>(rec + 2 * np + idx);
+      tp[0] = v.x, tp[1] = v.y;
+      v = *reinterpret_cast<const double2*>(rec + 3 * np + idx);
+      gr[0] = v.x, gr[1] = v.y;
+      if (!LAP) {
+        v = *reinterpret_cast<const double2*>(rec + 4 * np + idx);
+        gi[0] = v.x, gi[1] = v.y;
+      } else {
+        gi[0] = gi[1] = 0.0;
+      }
+    } else {
+#pragma unroll
+      for (int j = 0; j < R; ++j) {
+        g[j] = rec_g[idx + j];
+        ts[j] = rec[idx + j];
+        tt[j] = rec[np + idx + j];
+        tp[j] = rec[2 * np + idx + j];
+        gr[j] = rec[3 * np + idx + j];
+        gi[j] = LAP ? 0.0 : rec[4 * np + idx + j];
+      }
+    }
+  }
+  __device__ __forceinline__ void get(int slot, uint32_t& g_, double& ts_, double& tt_, double& tp_,
+                                      double& gr_, double& gi_) const {
+    g_ = g[0], ts_ = ts[0], tt_ = tt[0], tp_ = tp[0], gr_ = gr[0], gi_ = gi[0];
+#pragma unroll
+    for (int j = 1; j < R; ++j)
+      if (slot == j) g_ = g[j], ts_ = ts[j], tt_ = tt[j], tp_ = tp[j], gr_ = gr[j], gi_ = gi[j];
+  }
+};
+
+#ifndef IFGF_INTERP_REC_MINB
+#define IFGF_INTERP_REC_MINB 3
+#endif
+template <int PS, int PT, int PP, bool LAP, int R>
+__global__ void __launch_bounds__(128, IFGF_INTERP_REC_MINB)
+    k_interp_rec(const __grid_constant__ LevelDev L, const uint2* __restrict__ chunk,
+                 const uint32_t* __restrict__ nchunk, size_t b0, size_t e0,
+                 const double2* __restrict__ blocks, double* ir, double* ii, int* err) {
+  using BL = BlockLayout<PS, PT, PP>;
+  const size_t t = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
+  if (t >= *nchunk) return;
+  const uint2 ch = chunk[t];
+  const uint32_t b = ch.y;
+  const uint32_t fb = L.first[b], cnt = L.count[b];
+  const size_t lo = max((size_t)ch.x, b0);
+  const size_t hi = min(min((size_t)ch.x + R, (size_t)fb + cnt), e0);
+  if (lo >= hi) return;
+  const int n = (int)(hi - lo);
+  const uint32_t k0 = L.cous_off[b], k1 = L.cous_off[b + 1];
+  if (k0 == k1) return;
+  const uint64_t np = L.npairs;
+  const double* __restrict__ rec = L.rec;
+  const uint32_t* __restrict__ rec_g = L.rec_g;
+  const uint32_t cntp = (cnt + R - 1) / R * R;
+  uint64_t idx = L.pair_off[b] + (ch.x - fb);
+  // record slot of evaluation j: the item's points from lo on, the first repeated
+  int off[R];
+#pragma unroll
+  for (int j = 0; j < R; ++j) off[j] = (int)(lo - ch.x) + (j < n ? j : 0);
+  double acr[R], aci[R];
+#pragma unroll
+  for (int j = 0; j < R; ++j) acr[j] = aci[j] = 0.0;
+  RecSet<R, LAP> nx;
+  nx.load(rec_g, rec, np, idx);
+  for (uint32_t k = k0; k < k1; ++k) {
+    uint32_t g[R];
+    double ts[R], tt[R], tp[R], gr[R], gi[R], vr[R], vi[R];
+#pragma unroll
+    for (int j = 0; j < R; ++j) nx.get(off[j], g[j], ts[j], tt[j], tp[j], gr[j], gi[j]);
+    if (k + 1 < k1) {
+      idx += cntp;
+      nx.load(rec_g, rec, np, idx);
+    }
+    eval_block_multi<PS, PT, PP, R>(blocks + (size_t)g[0] * BL::Pst, ts, tt, tp, vr, vi);
+#pragma unroll
+    for (int j = 1; j < R; ++j)
+      if (j < n && g[j] != g[0])  // another cone of this cousin
+        eval_block<PS, PT, PP>(blocks + (size_t)g[j] * BL::Pst, ts[j], tt[j], tp[j], vr[j], vi[j]);
+#pragma unroll
+    for (int j = 0; j < R; ++j) {
+      if (LAP) {
+        acr[j] = fma(vr[j], gr[j], acr[j]);
+        aci[j] = fma(vi[j], gr[j], aci[j]);
+      } else {
+        acr[j] = fma(vr[j], gr[j], fma(-vi[j], gi[j], acr[j]));
+        aci[j] = fma(vr[j], gi[j], fma(vi[j], gr[j], aci[j]));
+      }
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < R; ++j)
+    if (j < n) {
+      ir[lo + j] += acr[j];
+      ii[lo + j] += aci[j];
+    }
+}
+
+__device__ __forceinline__ void cp_async16(void* dst_smem, const void* src) {
+  const uint32_t d = (uint32_t)__cvta_generic_to_shared(dst_smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(d), "l"(src) : "memory");
+}
+
+#ifndef IFGF_STG_WARPS
+#define IFGF_STG_WARPS 2
+#endif
+#ifndef IFGF_STG_MINB
+#define IFGF_STG_MINB 5
+#endif
+constexpr int kStgWarps = IFGF_STG_WARPS;
+// slots per set: 8 blocks of <= 80 coefficients, 4 of <= 160
+constexpr int stg_slots(int Pst) { return Pst <= 80 ? 8 : (Pst <= 160 ? 4 : 0); }
+
+template <int PS, int PT, int PP, bool LAP>
+__global__ void __launch_bounds__(kStgWarps * 32, IFGF_STG_MINB)
+    k_interp_stg(const __grid_constant__ LevelDev L, const uint2* __restrict__ chunk,
+                 const uint32_t* __restrict__ nchunk, size_t b0, size_t e0,
+                 const double2* __restrict__ blocks, double* ir, double* ii) {
+  using BL = BlockLayout<PS, PT, PP>;
+  constexpr int R = 2;
+  constexpr int S = stg_slots(BL::Pst);
+  constexpr int ST = BL::Pst + 1;  // slot stride (double2): odd, so slots start in different banks
+  constexpr unsigned FULL = 0xffffffffu;
+  constexpr uint32_t NONE = 0xffffffffu;
+  extern __shared__ double2 stg_smem[];
+  const int lane = threadIdx.x & 31;
+  double2* const buf = stg_smem + (size_t)(threadIdx.x >> 5) * 2 * S * ST;
+  const size_t t = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
+  const uint32_t nch = *nchunk;
+  if (t - lane >= nch) return;  // whole warp past the work list
+  // lanes without work stay for the cooperative copies
+  uint32_t cntp = 0, len = 0;
+  size_t lo = 0;
+  int n = 0;
+  bool sel0 = false, sel1 = false;  // record slot (0 / 1) of the two evaluations
+  uint64_t idx = 0;
+  if (t < nch) {
+    const uint2 ch = chunk[t];
+    const uint32_t b = ch.y;
+    const uint32_t fb = L.first[b], cnt = L.count[b];
+    cntp = (cnt + 1u) & ~1u;
+    lo = max((size_t)ch.x, b0);
+    const size_t hi = min(min((size_t)ch.x + R, (size_t)fb + cnt), e0);
+    if (lo < hi) {
+      n = (int)(hi - lo);
+      len = L.cous_off[b + 1] - L.cous_off[b];
+      idx = L.pair_off[b] + (ch.x - fb);
+      sel0 = lo > ch.x;
+      sel1 = sel0 || n > 1;
+    }
+  }
+  const uint32_t maxlen = __reduce_max_sync(FULL, len);
+  if (maxlen == 0) return;
+  const uint64_t np = L.npairs;
+  const double* __restrict__ rec = L.rec;
+  const uint32_t* __restrict__ rec_g = L.rec_g;
+  double acr[R] = {0.0, 0.0}, aci[R] = {0.0, 0.0};
+
+  // cone ordinals of step kk (NONE: no work), from the records
+  auto load_q = [&](uint32_t kk, uint32_t& q0, uint32_t& q1) {
+    q0 = q1 = NONE;
+    if (kk < len) {
+      const uint2 v = *reinterpret_cast<const uint2*>(rec_g + idx + (uint64_t)kk * cntp);
+      q0 = sel0 ? v.y : v.x;
+      q1 = sel1 ? v.y : v.x;
+    }
+  };
+  // slots of the step's distinct blocks, and their copies into slot set `set`
+  auto stage = [&](uint32_t q0, uint32_t q1, int set, int& s0, int& s1) {
+    const bool act = q0 != NONE;
+    const unsigned pa = __match_any_sync(FULL, q0);
+    const int la = __ffs(pa) - 1;
+    const unsigned leadA = __ballot_sync(FULL, act && la == lane);
+    s0 = __popc(leadA & ((1u << la) - 1u));
+    const int nA = __popc(leadA);
+    const bool diff = act && q1 != q0;
+    const unsigned dm = __ballot_sync(FULL, diff);
+    s1 = s0;
+    unsigned leadB = 0;
+    if (dm) {  // warp-uniform
+      const uint32_t v = diff ? q1 : q0;
+      const unsigned pb = __match_any_sync(FULL, v);
+      const unsigned same0 = pb & ~dm;  // lanes whose first block is this one
+      const int src = same0 ? __ffs(same0) - 1 : lane;
+      const int sfrom = __shfl_sync(FULL, s0, src);
+      const int lb = __ffs(pb & dm) - 1;
+      leadB = __ballot_sync(FULL, diff && !same0 && lb == lane);
+      if (diff) s1 = same0 ? sfrom : nA + __popc(leadB & ((1u << lb) - 1u));
+    }
+    const int ntot = min(nA + __popc(leadB), S);
+    double2* const dst0 = buf + (size_t)set * S * ST;
+    for (int s = 0; s < ntot; ++s) {
+      const bool fromA = s < nA;
+      const int src = (int)__fns(fromA ? leadA : leadB, 0, (fromA ? s : s - nA) + 1);
+      const uint32_t q = __shfl_sync(FULL, fromA ? q0 : q1, src);
+      const double2* g = blocks + (size_t)q * BL::Pst;
+      double2* d = dst0 + (size_t)s * ST;
+#pragma unroll
+      for (int c = 0; c < (BL::Pst + 31) / 32; ++c)
+        if (c * 32 + lane < BL::Pst) cp_async16(d + c * 32 + lane, g + c * 32 + lane);
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  };
+
+  // The cone ordinals run three steps ahead of the evaluation through a
+  // per-lane ring in shared memory (cp.async with the block copies: a
+  // register prefetch leaves the loop's register rotation waiting on the load)
+  uint2* const qring = reinterpret_cast<uint2*>(stg_smem + (size_t)kStgWarps * 2 * S * ST) +
+                       (size_t)(threadIdx.x >> 5) * 4 * 32 + lane;
+  auto fetch_q = [&](uint32_t kk) {  // async: lands with the next committed group
+    uint2* dst = qring + (kk & 3) * 32;
+    if (kk < len) {
+      const uint32_t d = (uint32_t)__cvta_generic_to_shared(dst);
+      asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(d),
+                   "l"(rec_g + idx + (uint64_t)kk * cntp)
+                   : "memory");
+    } else {
+      *dst = make_uint2(NONE, NONE);
+    }
+  };
+  auto read_q = [&](uint32_t kk, uint32_t& q0, uint32_t& q1) {
+    const uint2 v = qring[(kk & 3) * 32];
+    q0 = sel0 ? v.y : v.x;
+    q1 = sel1 ? v.y : v.x;
+  };
+  uint32_t q0, q1, q0n, q1n;
+  int s0, s1, s0n = 0, s1n = 0;
+  load_q(0, q0, q1);
+  fetch_q(1);
+  fetch_q(2);
+  stage(q0, q1, 0, s0, s1);  // commits group 0 (blocks of step 0, ordinals of steps 1 and 2)
+  double ts[R], tt[R], tp[R], gr[R], gi[R];
+  auto load_rec = [&](uint32_t kk) {
+    if (kk < len) {
+      const double* r = rec + idx + (uint64_t)kk * cntp;
+      auto pick = [&](const double* p, double* out) {
+        const double2 v = *reinterpret_cast<const double2*>(p);
+        out[0] = sel0 ? v.y : v.x;
+        out[1] = sel1 ? v.y : v.x;
+      };
+      pick(r, ts);
+      pick(r + np, tt);
+      pick(r + 2 * np, tp);
+      pick(r + 3 * np, gr);
+      if (!LAP) pick(r + 4 * np, gi);
+      else gi[0] = gi[1] = 0.0;
+    }
+  };
+  load_rec(0);
+  asm volatile("cp.async.wait_group 0;" ::: "memory");
+  for (uint32_t kk = 0; kk < maxlen; ++kk) {
+    // next step's blocks into the other slot set (its readers finished at the
+    // __syncwarp that closed the previous iteration), ordinals of step kk + 3
+    read_q(kk + 1, q0n, q1n);
+    fetch_q(kk + 3);
+    if (kk + 1 < maxlen) stage(q0n, q1n, (kk + 1) & 1, s0n, s1n);
+    else asm volatile("cp.async.commit_group;" ::: "memory");
+    asm volatile("cp.async.wait_group 1;" ::: "memory");
+    __syncwarp();
+    if (q0 != NONE) {
+      const double2* const set = buf + (size_t)(kk & 1) * S * ST;
+      double vr[R], vi[R];
+      if (s0 < S)
+        eval_block_multi<PS, PT, PP, R, true>(set + (size_t)s0 * ST, ts, tt, tp, vr, vi);
+      else
+        eval_block_multi<PS, PT, PP, R>(blocks + (size_t)q0 * BL::Pst, ts, tt, tp, vr, vi);
+      if (q1 != q0) {  // the second point sees another cone of this cousin
+        if (s1 < S)
+          eval_block<PS, PT, PP, true>(set + (size_t)s1 * ST, ts[1], tt[1], tp[1], vr[1], vi[1]);
+        else
+          eval_block<PS, PT, PP>(blocks + (size_t)q1 * BL::Pst, ts[1], tt[1], tp[1], vr[1], vi[1]);
+      }
+#pragma unroll
+      for (int j = 0; j < R; ++j) {
+        if (LAP) {
+          acr[j] = fma(vr[j], gr[j], acr[j]);
+          aci[j] = fma(vi[j], gr[j], aci[j]);
+        } else {
+          acr[j] = fma(vr[j], gr[j], fma(-vi[j], gi[j], acr[j]));
+          aci[j] = fma(vr[j], gi[j], fma(vi[j], gr[j], aci[j]));
+        }
+      }
+    }
+    load_rec(kk + 1);
+    __syncwarp();
+    q0 = q0n;
+    q1 = q1n;
+    s0 = s0n;
+    s1 = s1n;
+  }
+#pragma unroll
+  for (int j = 0; j < R; ++j)
+    if (j < n) {
+      ir[lo + j] += acr[j];
+      ii[lo + j] += aci[j];
+    }
+}
+
 // --------------------------------------------------------------- K6 permutes
 __global__ void k_gather_density(const uint32_t* __restrict__ perm, const double* __restrict__ a_re,
                                  const double* __restrict__ a_im, size_t n, double* ar, double* ai,
@@ -687,6 +1017,37 @@ void launch_interpolation(ifgf_plan* P, int d, size_t b, size_t e, const double2
     using O = decltype(o);
     constexpr int R = interp_points(O::P);
     const unsigned g = blocks_for(L.chunk_cap, 128);
+    if (L.rec && P->k4_records) {
+      using BL = BlockLayout<O::PS, O::PT, O::PP>;
+      static const bool no_stage = [] {
+        const char* v = std::getenv("IFGF_K4_STAGE");
+        return v && std::atoi(v) == 0;
+      }();
+      if constexpr (R == 2 && stg_slots(BL::Pst) > 0) {
+        if (!no_stage) {
+          auto kern = P->kappa == 0.0 ? k_interp_stg<O::PS, O::PT, O::PP, true>
+                                      : k_interp_stg<O::PS, O::PT, O::PP, false>;
+          const size_t smem =
+              (size_t)kStgWarps * 2 * stg_slots(BL::Pst) * (BL::Pst + 1) * sizeof(double2) +
+              (size_t)kStgWarps * 4 * 32 * sizeof(uint2);  // slot sets + ordinal rings
+          static bool attr_set = false;  // per instantiation (orders, kernel kind share the size)
+          if (!attr_set) {
+            IFGF_CUDA(cudaFuncSetAttribute(k_interp_stg<O::PS, O::PT, O::PP, true>,
+                                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+            IFGF_CUDA(cudaFuncSetAttribute(k_interp_stg<O::PS, O::PT, O::PP, false>,
+                                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+            attr_set = true;
+          }
+          kern<<<blocks_for(L.chunk_cap, kStgWarps * 32), kStgWarps * 32, smem, s>>>(
+              L.dev(), L.chunk, L.nchunk, b, e, blocks, P->ir, P->ii);
+          return;
+        }
+      }
+      auto kern = P->kappa == 0.0 ? k_interp_rec<O::PS, O::PT, O::PP, true, R>
+                                  : k_interp_rec<O::PS, O::PT, O::PP, false, R>;
+      kern<<<g, 128, 0, s>>>(L.dev(), L.chunk, L.nchunk, b, e, blocks, P->ir, P->ii, P->err);
+      return;
+    }
     auto kern = P->kappa == 0.0 ? k_interp<O::PS, O::PT, O::PP, true, R>
                                 : k_interp<O::PS, O::PT, O::PP, false, R>;
     kern<<<g, 128, 0, s>>>(L.dev(), L.chunk, L.nchunk, P->xs, P->ys, P->zs, P->kappa, b, e,

@@ -74,6 +74,11 @@ struct Level {
   uint32_t* rank = nullptr;
   size_t nwords = 0;
   const double2* trig = nullptr;
+  // K4 records (null unless the plan keeps them for this level)
+  uint64_t* pair_off = nullptr;
+  uint32_t* rec_g = nullptr;
+  double* rec = nullptr;
+  uint64_t npairs = 0;
 
   LevelDev dev() const {
     LevelDev v;
@@ -110,6 +115,10 @@ struct Level {
     v.bits = bits;
     v.rank = rank;
     v.trig = trig;
+    v.pair_off = pair_off;
+    v.rec_g = rec_g;
+    v.rec = rec;
+    v.npairs = npairs;
     return v;
   }
 };
@@ -202,6 +211,7 @@ struct ifgf_plan {
   int near_kernel = IFGF_NEAR_BOX;   // IFGF_OPT_NEAR_KERNEL
   int partition_mode = IFGF_PARTITION_COUNT;  // IFGF_OPT_PARTITION
   size_t setup_launches = 0;
+  bool k4_records = true;  // IFGF_OPT_K4_RECORDS: K4 reads the stored locate records where a level has them
   size_t mem_budget = 0;  // device memory available when the plan was created (capi.cu)
   ifgf_b200::DistState* dist = nullptr;  // rank plans of a multi-GPU group (dist.cu)
 
@@ -237,6 +247,7 @@ void launch_propagation(ifgf_plan* P, int d, uint32_t qb, uint32_t qe, const dou
                         double2* parent, cudaStream_t s);
 void launch_interpolation(ifgf_plan* P, int d, size_t b, size_t e, const double2* blocks,
                           cudaStream_t s);
+void launch_locate_points(ifgf_plan* P, int d, cudaStream_t s);
 void launch_pack(ifgf_plan* P, const double2* blocks, const uint32_t* cones, size_t m,
                  uint32_t nc, double* buf, int unpack, double2* blocks_out, cudaStream_t s);
 bool orders_supported(int ps, int pt, int pp);

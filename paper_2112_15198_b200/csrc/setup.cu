@@ -329,6 +329,176 @@ __global__ void k_mark_points(const __grid_constant__ LevelDev L, const uint32_t
   }
 }
 
+// Clause 1 for plans that keep K4 records: the apply-side locate
+// (engine.cpp:29-51) of every (point, cousin) pair in full precision, once.
+// Thread = one K4 work item (<= R consecutive points of a box, Level::chunk).
+// Per pair it marks the segment (clause 1) and stores what K4 needs from the
+// locate: the segment, the local Chebyshev coordinates and the kernel factor
+// e^{i kappa r} / (4 pi r) (LevelDev::rec).  K4 then only looks up the cone
+// and evaluates; the interpolation pass of every later apply skips the locate
+// (more than half of its time), and this kernel, free of the evaluation's
+// registers, runs it at four times K4's occupancy.
+__global__ void k_pair_count(const uint32_t* __restrict__ count,
+                             const uint32_t* __restrict__ ncous, uint32_t nb, uint32_t R,
+                             uint64_t* out) {
+  const uint32_t b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b < nb) out[b] = (uint64_t)((count[b] + R - 1) / R * R) * ncous[b];
+  else if (b == nb) out[b] = 0;
+}
+
+// R values of one record plane of a work item (the item's pair index is a
+// multiple of R: one aligned vector store for R = 2)
+template <int R, class T>
+__device__ __forceinline__ void rec_store(T* __restrict__ p, uint64_t idx, const T* v) {
+  if constexpr (R == 2 && sizeof(T) == 8) {
+    *reinterpret_cast<double2*>(p + idx) = make_double2(v[0], v[1]);
+  } else if constexpr (R == 2 && sizeof(T) == 4) {
+    *reinterpret_cast<uint2*>(p + idx) = make_uint2(v[0], v[1]);
+  } else {
+#pragma unroll
+    for (int j = 0; j < R; ++j) p[idx + j] = v[j];
+  }
+}
+
+template <bool LAP, int R>
+__global__ void __launch_bounds__(256)
+    k_locate_points(const __grid_constant__ LevelDev L, const uint2* __restrict__ chunk,
+                    const uint32_t* __restrict__ nchunk, const double* __restrict__ xs,
+                    const double* __restrict__ ys, const double* __restrict__ zs, double kappa,
+                    uint64_t* bits, uint32_t* __restrict__ rec_g, double* __restrict__ rec,
+                    int* err) {
+  __shared__ double2 trig[kTrigEntries];
+  __shared__ double2 ptab[LAP ? 1 : kPhaseEntries];
+  stage_trig(trig, L.trig);
+  if (!LAP)
+    for (int k = threadIdx.x; k < kPhaseEntries; k += blockDim.x) ptab[k] = L.trig[kTrigEntries + k];
+  __syncthreads();
+  const double ks = kappa * kPhaseScale;
+  const size_t t = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
+  if (t >= *nchunk) return;
+  const uint2 ch = chunk[t];
+  const uint32_t b = ch.y;
+  const uint32_t fb = L.first[b], cnt = L.count[b];
+  const uint32_t cntp = (cnt + R - 1) / R * R;
+  const int n = (int)min((uint32_t)R, fb + cnt - ch.x);
+  double px[R], py[R], pz[R];
+#pragma unroll
+  for (int j = 0; j < R; ++j) {  // slots past the box's last point repeat the item's first point
+    const size_t i = (size_t)ch.x + (j < n ? j : 0);
+    px[j] = xs[i];
+    py[j] = ys[i];
+    pz[j] = zs[i];
+  }
+  const uint32_t k0 = L.cous_off[b], k1 = L.cous_off[b + 1];
+  uint64_t idx = L.pair_off[b] + (ch.x - fb);
+  const uint64_t np = L.npairs;
+  // cousin index two steps ahead, centre one step ahead
+  uint32_t cb1 = k0 < k1 ? L.cous[k0] : 0;
+  uint32_t cb2 = k0 + 1 < k1 ? L.cous[k0 + 1] : 0;
+  double cxn = L.cx[cb1], cyn = L.cy[cb1], czn = L.cz[cb1];
+  for (uint32_t k = k0; k < k1; ++k, idx += cntp) {
+    const uint32_t cb = cb1;
+    const double cx = cxn, cy = cyn, cz = czn;
+    cb1 = cb2;
+    if (k + 2 < k1) cb2 = L.cous[k + 2];
+    if (k + 1 < k1) {
+      cxn = L.cx[cb1];
+      cyn = L.cy[cb1];
+      czn = L.cz[cb1];
+    }
+    Loc o[R];
+    int e = 0;
+#pragma unroll
+    for (int j = 0; j < R; ++j) {
+      const int ej = locate_fast(L, trig, cx, cy, cz, px[j], py[j], pz[j], o[j]);
+      e = e ? e : ej;
+    }
+    if (e) {
+      raise_err(err, e);
+      return;
+    }
+    // clause 1: the bitmap words are requested here and tested after the
+    // factor and the stores (a set bit -- the common case -- needs no atomic)
+    uint64_t bi[R], bw[R];
+    uint32_t g[R];
+#pragma unroll
+    for (int j = 0; j < R; ++j) {
+      g[j] = o[j].gamma;
+      bi[j] = (uint64_t)cb * L.G + g[j];
+      bw[j] = bits[bi[j] >> 6];
+    }
+    double v[R];
+    rec_store<R>(rec_g, idx, g);
+#pragma unroll
+    for (int j = 0; j < R; ++j) v[j] = o[j].ts;
+    rec_store<R>(rec, idx, v);
+#pragma unroll
+    for (int j = 0; j < R; ++j) v[j] = o[j].tt;
+    rec_store<R>(rec + np, idx, v);
+#pragma unroll
+    for (int j = 0; j < R; ++j) v[j] = o[j].tp;
+    rec_store<R>(rec + 2 * np, idx, v);
+    double gi[R];
+#pragma unroll
+    for (int j = 0; j < R; ++j) {
+      const double inv = kQuarterInvPi * o[j].rinv;
+      v[j] = inv;
+      gi[j] = 0.0;
+      if (!LAP) {
+        double sn, cn;
+        sincos_tab(ptab, ks * o[j].r, sn, cn);
+        v[j] = cn * inv;
+        gi[j] = sn * inv;
+      }
+    }
+    rec_store<R>(rec + 3 * np, idx, v);
+    if (!LAP) rec_store<R>(rec + 4 * np, idx, gi);
+#pragma unroll
+    for (int j = 0; j < R; ++j) {
+      const uint64_t m = 1ull << (bi[j] & 63);
+      if (!(bw[j] & m) && (j == 0 || bi[j] != bi[0]))
+        atomicOr((unsigned long long*)(bits + (bi[j] >> 6)), (unsigned long long)m);
+    }
+  }
+}
+
+// K4 records, second step (after the level's cones are numbered): the stored
+// segment of every pair becomes the ordinal of its cone (find_cone), so the
+// apply reads the block address without touching the bitmap.
+template <int R>
+__global__ void __launch_bounds__(256)
+    k_rec_cones(const __grid_constant__ LevelDev L, const uint2* __restrict__ chunk,
+                const uint32_t* __restrict__ nchunk, uint32_t* __restrict__ rec_g, int* err) {
+  const size_t t = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
+  if (t >= *nchunk) return;
+  const uint2 ch = chunk[t];
+  const uint32_t b = ch.y;
+  const uint32_t fb = L.first[b], cnt = L.count[b];
+  const uint32_t cntp = (cnt + R - 1) / R * R;
+  uint64_t idx = L.pair_off[b] + (ch.x - fb);
+  for (uint32_t k = L.cous_off[b]; k < L.cous_off[b + 1]; ++k, idx += cntp) {
+    const uint32_t cb = L.cous[k];
+    uint32_t g[R];
+    if constexpr (R == 2) {
+      const uint2 v = *reinterpret_cast<const uint2*>(rec_g + idx);
+      g[0] = v.x;
+      g[1] = v.y;
+    } else {
+#pragma unroll
+      for (int j = 0; j < R; ++j) g[j] = rec_g[idx + j];
+    }
+#pragma unroll
+    for (int j = 0; j < R; ++j) {
+      g[j] = find_cone(L, cb, g[j]);
+      if (g[j] == 0xffffffffu) {
+        raise_err(err, kErrInterpCover);
+        return;
+      }
+    }
+    rec_store<R>(rec_g, idx, g);
+  }
+}
+
 // Clause 2 (cones.cpp:108-119): nodes of every relevant cone of the parent box
 // mark the containing segment of each child box.
 __global__ void k_mark_nodes(const __grid_constant__ LevelDev L, const __grid_constant__ LevelDev U,
@@ -433,6 +603,23 @@ void check_device_error(ifgf_plan* P) {
     default:
       throw Error(IFGF_ERUNTIME, "unknown device error " + std::to_string(e));
   }
+}
+
+void launch_locate_points(ifgf_plan* P, int d, cudaStream_t s) {
+  const Level& L = P->lv[d];
+  const unsigned g = (unsigned)((L.chunk_cap + 255) / 256);
+  auto go = [&](auto kern) {
+    kern<<<g, 256, 0, s>>>(L.dev(), L.chunk, L.nchunk, P->xs, P->ys, P->zs, P->kappa, L.bits,
+                           L.rec_g, L.rec, P->err);
+  };
+  const bool lap = P->kappa == 0.0;
+  switch (interp_points(P->K.P)) {
+    case 1: lap ? go(k_locate_points<true, 1>) : go(k_locate_points<false, 1>); break;
+    case 2: lap ? go(k_locate_points<true, 2>) : go(k_locate_points<false, 2>); break;
+    case 3: lap ? go(k_locate_points<true, 3>) : go(k_locate_points<false, 3>); break;
+    default: lap ? go(k_locate_points<true, 4>) : go(k_locate_points<false, 4>); break;
+  }
+  ++P->launches;
 }
 
 void build_plan(ifgf_plan* P, const double* d_x, const double* d_y, const double* d_z) {
@@ -621,6 +808,19 @@ void build_plan(ifgf_plan* P, const double* d_x, const double* d_y, const double
   }
   // cousin CSR for d = 3..D
   std::vector<uint32_t> cous_total(D + 1, 0);
+  // K4 records (k_locate_points): kept when all levels' records fit in
+  // IFGF_K4_REC_FRAC (default 0.15) of the plan's memory budget;
+  // IFGF_K4_RECORDS=0 turns them off.
+  static const bool rec_env = [] {
+    const char* v = std::getenv("IFGF_K4_RECORDS");
+    return !v || std::atoi(v) != 0;
+  }();
+  static const double rec_frac = [] {
+    const char* v = std::getenv("IFGF_K4_REC_FRAC");
+    return v ? std::atof(v) : 0.15;
+  }();
+  const bool want_records = P->k4_records && rec_env && D >= 3;
+  std::vector<unsigned long long> pair_total(D + 1, 0);
   for (int d = 3; d <= D; ++d) {
     Level& L = P->lv[d];
     uint32_t* cnt = P->alloc<uint32_t>(L.nb + 1);
@@ -634,6 +834,19 @@ void build_plan(ifgf_plan* P, const double* d_x, const double* d_y, const double
         cub::DeviceScan::ExclusiveSum(scratch.get(tb), tb, cnt, L.cous_off, (int)(L.nb + 1), s));
     IFGF_CUDA(cudaMemcpyAsync(&cous_total[d], L.cous_off + L.nb, sizeof(uint32_t),
                               cudaMemcpyDeviceToHost, s));
+    if (want_records) {
+      // K4 record offsets: exclusive sum of points x cousins per box
+      uint64_t* pc = P->alloc<uint64_t>(L.nb + 1);
+      L.pair_off = P->alloc<uint64_t>(L.nb + 1);
+      k_pair_count<<<grid_for(L.nb + 1), kT, 0, s>>>(L.count, cnt, L.nb,
+                                                     (uint32_t)interp_points(P->K.P), pc);
+      ++P->launches;
+      cub::DeviceScan::ExclusiveSum(nullptr, tb, pc, L.pair_off, (int)(L.nb + 1), s);
+      IFGF_CUDA(
+          cub::DeviceScan::ExclusiveSum(scratch.get(tb), tb, pc, L.pair_off, (int)(L.nb + 1), s));
+      IFGF_CUDA(cudaMemcpyAsync(&pair_total[d], L.pair_off + L.nb, sizeof(uint64_t),
+                                cudaMemcpyDeviceToHost, s));
+    }
   }
   // neighbour-list totals (ifgf_plan_info), read back with the cousin totals
   std::vector<unsigned long long> nbr_total(D + 1, 0);
@@ -673,6 +886,20 @@ void build_plan(ifgf_plan* P, const double* d_x, const double* d_y, const double
   IFGF_CUDA(cudaStreamSynchronize(s));
   mark("cousin sync");
   for (int d = 1; d <= D; ++d) P->lv[d].n_nbr = (size_t)nbr_total[d];
+  if (want_records) {
+    const int planes = P->kappa == 0.0 ? 4 : 5;
+    unsigned long long pairs = 0;
+    for (int d = 3; d <= D; ++d) pairs += pair_total[d];
+    const double need = (double)pairs * (planes * sizeof(double) + sizeof(uint32_t));
+    if (pairs > 0 && need <= rec_frac * (double)mem_available(P)) {
+      for (int d = 3; d <= D; ++d) {
+        Level& L = P->lv[d];
+        L.npairs = pair_total[d];
+        L.rec = P->alloc<double>((size_t)planes * L.npairs + 1);
+        L.rec_g = P->alloc<uint32_t>(L.npairs + 1);
+      }
+    }
+  }
   for (int d = 3; d <= D; ++d) {
     Level& L = P->lv[d];
     L.n_cous = cous_total[d];
@@ -714,9 +941,13 @@ void build_plan(ifgf_plan* P, const double* d_x, const double* d_y, const double
   for (int d = 3; d <= D; ++d) {
     Level& L = P->lv[d];
     IFGF_CUDA(cudaMemsetAsync(L.bits, 0, L.nwords * sizeof(uint64_t), sa));
-    k_mark_points<<<grid_for(n), kT, 0, sa>>>(L.dev(), L.ptbox, P->xs, P->ys, P->zs, n, L.bits,
-                                              P->err);
-    ++P->launches;
+    if (L.rec) {
+      launch_locate_points(P, d, sa);
+    } else {
+      k_mark_points<<<grid_for(n), kT, 0, sa>>>(L.dev(), L.ptbox, P->xs, P->ys, P->zs, n, L.bits,
+                                                P->err);
+      ++P->launches;
+    }
     IFGF_CUDA(cudaEventCreateWithFlags(&ev_pts[d], cudaEventDisableTiming));
     IFGF_CUDA(cudaEventRecord(ev_pts[d], sa));
   }
@@ -757,8 +988,24 @@ void build_plan(ifgf_plan* P, const double* d_x, const double* d_y, const double
     k_compact<<<grid_for(L.nwords), kT, 0, s>>>(L.dev(), L.nwords, L.cone_box, L.cone_gamma);
     k_box_cone<<<grid_for(L.nb + 1), kT, 0, s>>>(L.dev(), L.box_cone);
     P->launches += 2;
+    if (L.rec) {  // records: segment -> cone ordinal, on the aux stream
+      IFGF_CUDA(cudaEventRecord(ev_pts[d], s));
+      IFGF_CUDA(cudaStreamWaitEvent(sa, ev_pts[d], 0));
+      auto conv = [&](auto kern) {
+        kern<<<grid_for(L.chunk_cap), kT, 0, sa>>>(L.dev(), L.chunk, L.nchunk, L.rec_g, P->err);
+      };
+      switch (interp_points(P->K.P)) {
+        case 1: conv(k_rec_cones<1>); break;
+        case 2: conv(k_rec_cones<2>); break;
+        case 3: conv(k_rec_cones<3>); break;
+        default: conv(k_rec_cones<4>); break;
+      }
+      ++P->launches;
+    }
     mark("  compact");
   }
+  IFGF_CUDA(cudaEventRecord(ev_tree, sa));
+  IFGF_CUDA(cudaStreamWaitEvent(s, ev_tree, 0));
   IFGF_CUDA(cudaStreamSynchronize(s));
   cudaEventDestroy(ev_tree);
   for (int d = 3; d <= D; ++d) cudaEventDestroy(ev_pts[d]);

@@ -294,8 +294,15 @@ class Plan:
     def set_option(self, option: int, value: int):
         """IFGF_OPT_* (include/ifgf_b200.h): 1 serial streams, 2 propagation
         kernel (PROP_NODE, PROP_DMMA, PROP_ROWS, PROP_FLY, PROP_AUTO default), 3 near-field kernel (NEAR_POINT, NEAR_BOX default),
-        4 rank layout (PARTITION_COUNT default, PARTITION_WORK)."""
+        4 rank layout (PARTITION_COUNT default, PARTITION_WORK), 5 K4 reads the
+        plan's locate records (default 1; 0 locates every pair again)."""
         check(lib.ifgf_plan_set_option(self._h, option, value))
+
+    def set_k4_records(self, on: bool = True):
+        """K4 from the plan's stored locate records (default, when the plan
+        keeps them) or with a fresh locate per (point, cousin) pair; the
+        results are bitwise equal."""
+        self.set_option(5, 1 if on else 0)
 
     def set_prop_kernel(self, kind: int):
         self.set_option(2, kind)
