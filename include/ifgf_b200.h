@@ -192,6 +192,8 @@ typedef struct ifgf_plan_info {
   size_t device_bytes;
   size_t setup_launches; /* our kernels launched by the plan's setup */
   size_t launches;       /* our kernels launched by the plan so far (setup + passes) */
+  size_t k4_record_pairs; /* (point, cousin) pairs whose locate the plan keeps (0: none) */
+  size_t k4_record_bytes; /* device bytes of those records */
 } ifgf_plan_info;
 
 int ifgf_plan_get_info(const ifgf_plan* plan, ifgf_plan_info* info);

@@ -42,7 +42,8 @@ class CPlanInfo(C.Structure):
                 ("cousin_entries", C.c_size_t * MAX_LEVELS), ("h", C.c_double * MAX_LEVELS),
                 ("setup_seconds", C.c_double), ("device_bytes", C.c_size_t),
                 ("setup_launches", C.c_size_t),
-                ("launches", C.c_size_t)]
+                ("launches", C.c_size_t), ("k4_record_pairs", C.c_size_t),
+                ("k4_record_bytes", C.c_size_t)]
 
 
 class CDistLevel(C.Structure):

@@ -900,6 +900,11 @@ int ifgf_plan_get_info(const ifgf_plan* P, ifgf_plan_info* info) {
     info->device_bytes = P->bytes;
     info->setup_launches = P->setup_launches;
     info->launches = P->launches;
+    info->k4_record_pairs = 0;
+    for (int d = 3; d <= P->depth; ++d)
+      if (P->lv[d].rec) info->k4_record_pairs += (size_t)P->lv[d].npairs;
+    info->k4_record_bytes = info->k4_record_pairs *
+                            ((P->kappa == 0.0 ? 4 : 5) * sizeof(double) + sizeof(uint32_t));
   });
 }
 

@@ -661,7 +661,10 @@ __device__ __forceinline__ void cp_async16(void* dst_smem, const void* src) {
 #endif
 constexpr int kStgWarps = IFGF_STG_WARPS;
 // slots per set: 8 blocks of <= 80 coefficients, 4 of <= 160
-constexpr int stg_slots(int Pst) { return Pst <= 80 ? 8 : (Pst <= 160 ? 4 : 0); }
+#ifndef IFGF_STG_SLOTS
+#define IFGF_STG_SLOTS 8
+#endif
+constexpr int stg_slots(int Pst) { return Pst <= 80 ? IFGF_STG_SLOTS : (Pst <= 160 ? IFGF_STG_SLOTS / 2 : 0); }
 
 template <int PS, int PT, int PP, bool LAP>
 __global__ void __launch_bounds__(kStgWarps * 32, IFGF_STG_MINB)
@@ -781,21 +784,17 @@ __global__ void __launch_bounds__(kStgWarps * 32, IFGF_STG_MINB)
   fetch_q(1);
   fetch_q(2);
   stage(q0, q1, 0, s0, s1);  // commits group 0 (blocks of step 0, ordinals of steps 1 and 2)
-  double ts[R], tt[R], tp[R], gr[R], gi[R];
+  // the step's record pairs as loaded (the slot selects wait until the
+  // evaluation, a whole step after the loads were issued)
+  double2 raw[5];
+#pragma unroll
+  for (int i = 0; i < 5; ++i) raw[i] = make_double2(0.0, 0.0);
   auto load_rec = [&](uint32_t kk) {
     if (kk < len) {
       const double* r = rec + idx + (uint64_t)kk * cntp;
-      auto pick = [&](const double* p, double* out) {
-        const double2 v = *reinterpret_cast<const double2*>(p);
-        out[0] = sel0 ? v.y : v.x;
-        out[1] = sel1 ? v.y : v.x;
-      };
-      pick(r, ts);
-      pick(r + np, tt);
-      pick(r + 2 * np, tp);
-      pick(r + 3 * np, gr);
-      if (!LAP) pick(r + 4 * np, gi);
-      else gi[0] = gi[1] = 0.0;
+#pragma unroll
+      for (int i = 0; i < (LAP ? 4 : 5); ++i)
+        raw[i] = *reinterpret_cast<const double2*>(r + i * np);
     }
   };
   load_rec(0);
@@ -812,6 +811,11 @@ __global__ void __launch_bounds__(kStgWarps * 32, IFGF_STG_MINB)
     if (q0 != NONE) {
       const double2* const set = buf + (size_t)(kk & 1) * S * ST;
       double vr[R], vi[R];
+      const double ts[R] = {sel0 ? raw[0].y : raw[0].x, sel1 ? raw[0].y : raw[0].x};
+      const double tt[R] = {sel0 ? raw[1].y : raw[1].x, sel1 ? raw[1].y : raw[1].x};
+      const double tp[R] = {sel0 ? raw[2].y : raw[2].x, sel1 ? raw[2].y : raw[2].x};
+      const double gr[R] = {sel0 ? raw[3].y : raw[3].x, sel1 ? raw[3].y : raw[3].x};
+      const double gi[R] = {sel0 ? raw[4].y : raw[4].x, sel1 ? raw[4].y : raw[4].x};
       if (s0 < S)
         eval_block_multi<PS, PT, PP, R, true>(set + (size_t)s0 * ST, ts, tt, tp, vr, vi);
       else

@@ -360,8 +360,11 @@ __device__ __forceinline__ void rec_store(T* __restrict__ p, uint64_t idx, const
   }
 }
 
+#ifndef IFGF_LOCATE_MINB
+#define IFGF_LOCATE_MINB 3
+#endif
 template <bool LAP, int R>
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(256, IFGF_LOCATE_MINB)
     k_locate_points(const __grid_constant__ LevelDev L, const uint2* __restrict__ chunk,
                     const uint32_t* __restrict__ nchunk, const double* __restrict__ xs,
                     const double* __restrict__ ys, const double* __restrict__ zs, double kappa,

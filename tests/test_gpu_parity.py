@@ -108,6 +108,31 @@ def test_interpolation_pass(built):
     assert rel_l2(*g, *o) <= 1e-12
 
 
+def test_interpolation_records_bitwise(built):
+    """K4 from the plan's locate records (k_locate_points at setup, blocks staged
+    in shared memory where the orders allow it) equals the K4 that locates
+    every (point, cousin) pair again, bitwise: whole applies, and pass ranges
+    that cut through a two-point work item."""
+    case, pc, cfg, ep, op, plan, prob = built
+    D, n = plan.depth, pc.size()
+    cre, cim = prob.level_d()
+    plan.write_blocks(D, cre, cim)
+    res = {}
+    for rec in (True, False):
+        plan.set_k4_records(rec)
+        whole = plan.apply(pc.a_re, pc.a_im)[:2]
+        plan.write_blocks(D, cre, cim)
+        plan.zero_result()
+        for b, e in ((0, 1), (1, n // 3 + 1), (n // 3 + 1, n - 1), (n - 1, n)):
+            plan.interpolation_pass(D, b, e)
+        res[rec] = (whole, plan.read_result(sorted_order=True))
+    plan.set_k4_records(True)
+    for a, b in zip(res[True], res[False]):
+        assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1])
+    o = prob.interpolation(D, cre, cim)
+    assert rel_l2(*res[True][1], *o) <= 1e-12
+
+
 def test_apply_parity_and_error(built, oracle):
     case, pc, cfg, ep, op, plan, prob = built
     g_re, g_im, rep = plan.apply(pc.a_re, pc.a_im)
