@@ -503,7 +503,7 @@ __global__ void __launch_bounds__(128, IFGF_INTERP_MINB)
         aci[j] = fma(vi[j], inv, aci[j]);
       } else {
         double sn, cn;
-        sincos_tab(ptab, ks * o[j].r, sn, cn);
+        sincos_tab<true>(ptab, ks * o[j].r, sn, cn);
         const double gr = cn * inv, gi = sn * inv;
         acr[j] = fma(vr[j], gr, fma(-vi[j], gi, acr[j]));
         aci[j] = fma(vr[j], gi, fma(vi[j], gr, aci[j]));

@@ -449,7 +449,7 @@ __global__ void __launch_bounds__(256, IFGF_LOCATE_MINB)
       gi[j] = 0.0;
       if (!LAP) {
         double sn, cn;
-        sincos_tab(ptab, ks * o[j].r, sn, cn);
+        sincos_tab<true>(ptab, ks * o[j].r, sn, cn);
         v[j] = cn * inv;
         gi[j] = sn * inv;
       }

@@ -26,4 +26,16 @@ timeout 900 ncu --set full --import-source on --clock-control none -k regex:k_pr
   -c 1 -f -o gpurun_out/ncu_c2_k3_rows python tools/profile_step.py C2 1 > gpurun_out/ncu_c2_k3_rows.log 2>&1
 timeout 900 ncu --set full --import-source on --clock-control none -k regex:k_interp \
   --launch-skip 2 -c 1 -f -o gpurun_out/ncu_c2_k4 python tools/profile_step.py C2 1 > gpurun_out/ncu_c2_k4.log 2>&1
+# 5. the setup's locate kernel (K4 records), two of its six launches
+timeout 900 ncu --set full --import-source on --clock-control none -k regex:k_locate_points \
+  --launch-skip 6 -c 2 -f -o gpurun_out/ncu_c2_locate python tools/profile_step.py C2 1 --setups 2 > gpurun_out/ncu_c2_locate.log 2>&1
+# 6. K4 from the records against the locate-per-pair K4 (bitwise, per-level times)
+python tools/k4_records.py C2 > gpurun_out/k4_records_c2.log 2>&1
+# 7. summaries here (the reports themselves exceed what gpurun_out/ brings back)
+for tag in ncu_c2_k3_wgemm ncu_c2_k3_rows ncu_c2_k4 ncu_c2_locate; do
+  python tools/ncu_summary.py gpurun_out/$tag.ncu-rep gpurun_out/$tag > /dev/null 2>&1
+  ncu -i gpurun_out/$tag.ncu-rep --page source --csv > gpurun_out/$tag.src.csv 2> /dev/null
+  python tools/ncu_stalls.py gpurun_out/$tag.src.csv > gpurun_out/${tag}_stalls.txt 2>&1
+  rm -f gpurun_out/$tag.src.csv gpurun_out/$tag.ncu-rep
+done
 echo done > gpurun_out/profiles_done
