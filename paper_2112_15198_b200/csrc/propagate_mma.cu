@@ -616,13 +616,10 @@ __global__ void __launch_bounds__(kG4Warps * 32, 1)
           }
         }
       };
-      // act[u]: some cone of column tile u has this octant's child (else the
-      // tile's MMAs of the instance are skipped: its B operand is all zero)
-      auto resolve = [&](const Pend (&pd)[NU], const double2* (&bpo)[NU], bool (&act)[NU]) {
+      auto resolve = [&](const Pend (&pd)[NU], const double2* (&bpo)[NU]) {
   #pragma unroll
         for (int u = 0; u < NU; ++u) {
           const double2* p = zblock;
-          act[u] = __any_sync(0xffffffffu, pd[u].bit < 64);
           if (pd[u].bit < 64) {
             const uint64_t bit = 1ull << pd[u].bit;
             if (pd[u].wd & bit)
@@ -650,8 +647,7 @@ __global__ void __launch_bounds__(kG4Warps * 32, 1)
       } else {
         lookup(i0, 0, pd);
       }
-      bool act[NU];
-      resolve(pd, bp, act);
+      resolve(pd, bp);
   #pragma unroll
       for (int c = 0; c < PF; ++c)
   #pragma unroll
@@ -661,8 +657,7 @@ __global__ void __launch_bounds__(kG4Warps * 32, 1)
         // instance i1: its cones are resolved now (requested one instance ago);
         // instance i2: request its bitmap words; instance i3: its child gamma
         const double2* bpn[NU];
-        bool actn[NU];
-        resolve(pd, bpn, actn);
+        resolve(pd, bpn);
         lookup(i2, g2, pd);
         Inst i3 = i2;
         if (i3.o < 8) advance(i3);
@@ -708,17 +703,13 @@ __global__ void __launch_bounds__(kG4Warps * 32, 1)
           for (int u = 0; u < NU; ++u) b[u] = bq[c % PF][u];
   #pragma unroll
           for (int u = 0; u < NU; ++u) {
-            if (act[u]) {
-              dmma(dr[u][0], dr[u][1], a[0], b[u].x);
-              dmma(di[u][0], di[u][1], a[0], b[u].y);
-            }
+            dmma(dr[u][0], dr[u][1], a[0], b[u].x);
+            dmma(di[u][0], di[u][1], a[0], b[u].y);
           }
   #pragma unroll
           for (int u = 0; u < NU; ++u) {
-            if (act[u]) {
-              dmma(dr[u][0], dr[u][1], a[1], b[u].z);
-              dmma(di[u][0], di[u][1], a[1], b[u].w);
-            }
+            dmma(dr[u][0], dr[u][1], a[1], b[u].z);
+            dmma(di[u][0], di[u][1], a[1], b[u].w);
             bq[c % PF][u] = c + PF < NCH ? bload(bp[u], c + PF) : bload(bpn[u], c + PF - NCH);
           }
         }
@@ -750,10 +741,7 @@ __global__ void __launch_bounds__(kG4Warps * 32, 1)
         i2 = i3;
         rec = recn;
   #pragma unroll
-        for (int u = 0; u < NU; ++u) {
-          bp[u] = bpn[u];
-          act[u] = actn[u];
-        }
+        for (int u = 0; u < NU; ++u) bp[u] = bpn[u];
       }
     };
     if (kG4Nct == 2 && nq <= 8) run_stream(std::integral_constant<int, 1>{});

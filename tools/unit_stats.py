@@ -41,7 +41,7 @@ for d in range(plan.depth, 4, -1):
     ideal = POPC[msk].sum()
     starts = np.flatnonzero(np.r_[True, gam[1:] != gam[:-1]])
     ends = np.r_[starts[1:], len(gam)]
-    c0 = c1 = c2 = 0
+    c0 = c1 = c2 = ct = 0
     nu0 = nu1 = 0
     for a, b in zip(starts, ends):
         m = msk[a:b]
@@ -50,6 +50,10 @@ for d in range(plan.depth, 4, -1):
         cuts = list(range(0, n, 16))
         c0 += cost_units(m, cuts)
         nu0 += len(cuts)
+        # S0 with a column tile's MMAs skipped for octants none of its 8 cones
+        # has (the kernel's predicate): every tile pays only its own union
+        for t in range(0, n, 8):
+            ct += 8 * POPC[np.bitwise_or.reduce(m[t:t + 8])]
         # S1: new unit at a mask change once the unit holds >= 8 cones
         cuts, size = [0], 0
         for i in range(n):
@@ -109,5 +113,6 @@ for d in range(plan.depth, 4, -1):
     for a, b in zip(s4, e4):
         c4 += cost_units(m4[a:b], list(range(0, b - a, 16)))
     print(f"   Morton order within gamma, every 16: {c4 / ideal:.3f}")
+    print(f"   every 16, MMAs per column tile's own octants: {ct / ideal:.3f}")
     print(f"d={d}: cones {len(gam)} gammas {len(starts)} ideal {ideal}  every-16 {c0 / ideal:.3f} ({nu0} units)  "
           f"cut-at-mask>=8 {c1 / ideal:.3f} ({nu1} units)  optimal contiguous {c2 / ideal:.3f}", flush=True)
