@@ -376,12 +376,20 @@ void apply_device(ifgf_plan* P, const double* a_re, const double* a_im, double* 
   IFGF_CUDA(cudaEventRecord(t_ld.b, sm));
   blk_ready[D] = t_ld.b;
 
+  // K4 from the locate records stages its blocks in 212 KB of shared memory
+  // per SM: next to K3 on a second stream it costs both kernels their L1
+  // (C2 apply 50.1 ms on two streams against 48.4 ms in line), so it runs on
+  // the main stream between the propagation levels; K1 keeps the aux stream.
+  const bool k4_staged = P->k4_records && P->lv[D].rec != nullptr;
+  cudaStream_t s4 = k4_staged ? sm : sa;
+  // K1 and K4 both add into the result: K4 starts after K1 on either stream
+  if (s4 != sa) IFGF_CUDA(cudaStreamWaitEvent(s4, t_sing.b, 0));
   for (int d = D; d >= 3; --d) {
-    IFGF_CUDA(cudaStreamWaitEvent(sa, blk_ready[d], 0));
+    IFGF_CUDA(cudaStreamWaitEvent(s4, blk_ready[d], 0));
     t_int[d] = {mk(true), mk(true)};
-    IFGF_CUDA(cudaEventRecord(t_int[d].a, sa));
-    launch_interpolation(P, d, 0, P->n, P->slots[d], sa);
-    IFGF_CUDA(cudaEventRecord(t_int[d].b, sa));
+    IFGF_CUDA(cudaEventRecord(t_int[d].a, s4));
+    launch_interpolation(P, d, 0, P->n, P->slots[d], s4);
+    IFGF_CUDA(cudaEventRecord(t_int[d].b, s4));
     int_done[d] = t_int[d].b;
     if (d > 3) {
       const int prev = d - 1 + P->n_slots;  // previous occupant of level d-1's slot
@@ -394,6 +402,7 @@ void apply_device(ifgf_plan* P, const double* a_re, const double* a_im, double* 
     }
   }
   IFGF_CUDA(cudaStreamWaitEvent(sm, int_done[3], 0));
+  IFGF_CUDA(cudaStreamWaitEvent(sm, t_sing.b, 0));
   launch_scatter_result(P, i_re, i_im, sm);
   cudaEvent_t done = mk(false);
   IFGF_CUDA(cudaEventRecord(done, sm));

@@ -905,11 +905,39 @@ void build_plan(ifgf_plan* P, const double* d_x, const double* d_y, const double
     for (int d = 3; d <= D; ++d) pairs += pair_total[d];
     const double need = (double)pairs * (planes * sizeof(double) + sizeof(uint32_t));
     if (pairs > 0 && need <= rec_frac * (double)mem_available(P)) {
-      for (int d = 3; d <= D; ++d) {
+      // an allocation failure (memory taken by others since the budget's
+      // sample) only costs the records: the levels fall back to k_interp
+      bool ok = true;
+      std::vector<void*> got;
+      size_t got_bytes = 0;
+      for (int d = 3; d <= D && ok; ++d) {
         Level& L = P->lv[d];
+        const size_t b[2] = {((size_t)planes * pair_total[d] + 1) * sizeof(double) + 16,
+                             ((size_t)pair_total[d] + 1) * sizeof(uint32_t) + 16};
+        void* p[2] = {nullptr, nullptr};
+        for (int i = 0; i < 2 && ok; ++i) {
+          if (cudaMallocAsync(&p[i], b[i], s) != cudaSuccess) {
+            cudaGetLastError();
+            ok = false;
+          } else {
+            got.push_back(p[i]);
+            got_bytes += b[i];
+          }
+        }
         L.npairs = pair_total[d];
-        L.rec = P->alloc<double>((size_t)planes * L.npairs + 1);
-        L.rec_g = P->alloc<uint32_t>(L.npairs + 1);
+        L.rec = static_cast<double*>(p[0]);
+        L.rec_g = static_cast<uint32_t*>(p[1]);
+      }
+      if (ok) {
+        P->allocs.insert(P->allocs.end(), got.begin(), got.end());
+        P->bytes += got_bytes;
+      } else {  // all or nothing (the blocks keep their room)
+        for (void* q : got) cudaFreeAsync(q, s);
+        for (int d = 3; d <= D; ++d) {
+          P->lv[d].rec = nullptr;
+          P->lv[d].rec_g = nullptr;
+          P->lv[d].npairs = 0;
+        }
       }
     }
   }
