@@ -314,9 +314,6 @@ __global__ void k_mark_points(const __grid_constant__ LevelDev L, const uint32_t
   if (i >= n) return;
   const uint32_t b = ptbox[i];
   const double x = xs[i], y = ys[i], z = zs[i];
-  // a segment's bitmap word is requested when the segment is known and
-  // tested one cousin later (a set bit -- the common case -- needs no atomic)
-  uint64_t pidx = 0, pw = ~0ull;
   for (uint32_t ci = L.cous_off[b]; ci < L.cous_off[b + 1]; ++ci) {
     const uint32_t cb = L.cous[ci];
     const double cx = L.cx[cb], cy = L.cy[cb], cz = L.cz[cb];
@@ -328,15 +325,8 @@ __global__ void k_mark_points(const __grid_constant__ LevelDev L, const uint32_t
         return;
       }
     }
-    const uint64_t idx = (uint64_t)cb * L.G + g;
-    const uint64_t w = bits[idx >> 6];
-    if (!((pw >> (pidx & 63)) & 1ull))
-      atomicOr((unsigned long long*)(bits + (pidx >> 6)), 1ull << (pidx & 63));
-    pidx = idx;
-    pw = w;
+    set_bit_warp(bits, (uint64_t)cb * L.G + g);
   }
-  if (!((pw >> (pidx & 63)) & 1ull))
-    atomicOr((unsigned long long*)(bits + (pidx >> 6)), 1ull << (pidx & 63));
 }
 
 // Clause 1 for plans that keep K4 records: the apply-side locate
