@@ -130,9 +130,9 @@ void ifgf_plan_destroy(ifgf_plan* plan);
  *                       lanes, several targets per pass.
  *   Both agree to rounding.
  * IFGF_OPT_K4_RECORDS = 0: the interpolation pass locates every (point,
- *   cousin) pair again instead of reading the plan's locate records (kept by
- *   single-GPU plans whose records fit in 15 % of the device memory; same
- *   result bitwise).  Default 1. */
+ *   cousin) pair again instead of reading the plan's locate records (kept
+ *   when they fit in 15 % of the device memory -- a rank plan keeps only its
+ *   own points'; same result bitwise).  Default 1. */
 enum { IFGF_OPT_SERIAL = 1, IFGF_OPT_PROP_KERNEL = 2, IFGF_OPT_NEAR_KERNEL = 3,
        IFGF_OPT_PARTITION = 4, IFGF_OPT_K4_RECORDS = 5 };
 enum { IFGF_NEAR_POINT = 0, IFGF_NEAR_BOX = 1 };

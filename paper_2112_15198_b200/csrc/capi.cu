@@ -235,8 +235,8 @@ void plan_free(ifgf_plan* P) {
   delete P;
 }
 
-// Plans of a rank group keep no K4 locate records (each would hold the whole
-// cloud's; several rank plans share one device in the in-process groups).
+// Plans of a rank group keep K4 locate records for their own points only
+// (build_rank_records, after dist_prepare), not the whole cloud's.
 thread_local bool tl_rank_plan = false;
 struct RankPlanScope {
   RankPlanScope() { tl_rank_plan = true; }
@@ -262,7 +262,7 @@ ifgf_plan* new_plan(size_t n, int kind, double wavenumber, const ifgf_params* p)
     throw Error(IFGF_EINVAL, "unknown partition mode");
   P->partition_mode = p->partition;
   P->mem_budget = device_memory_budget(P->device);
-  P->k4_records = !tl_rank_plan;
+  P->rank_plan = tl_rank_plan;
   try {
     P->s_main = take_stream(P->device);
     P->s_aux = take_stream(P->device);

@@ -404,6 +404,8 @@ void dist_prepare(ifgf_plan* P, int R, int rank) {
     P->lv[d].bits = S->lv[d].lbits;
     P->lv[d].rank = S->lv[d].lrank;
   }
+  // K4 locate records of the rank's own points (ordinals = local block slots)
+  build_rank_records(P, p0, p1);
 }
 
 namespace {

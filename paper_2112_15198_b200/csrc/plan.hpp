@@ -212,6 +212,7 @@ struct ifgf_plan {
   int partition_mode = IFGF_PARTITION_COUNT;  // IFGF_OPT_PARTITION
   size_t setup_launches = 0;
   bool k4_records = true;  // IFGF_OPT_K4_RECORDS: K4 reads the stored locate records where a level has them
+  bool rank_plan = false;  // plan of a rank group: records only for its own points (build_rank_records)
   size_t mem_budget = 0;  // device memory available when the plan was created (capi.cu)
   ifgf_b200::DistState* dist = nullptr;  // rank plans of a multi-GPU group (dist.cu)
 
@@ -248,6 +249,7 @@ void launch_propagation(ifgf_plan* P, int d, uint32_t qb, uint32_t qe, const dou
 void launch_interpolation(ifgf_plan* P, int d, size_t b, size_t e, const double2* blocks,
                           cudaStream_t s);
 void launch_locate_points(ifgf_plan* P, int d, cudaStream_t s);
+void build_rank_records(ifgf_plan* P, uint32_t p0, uint32_t p1);
 void launch_pack(ifgf_plan* P, const double2* blocks, const uint32_t* cones, size_t m,
                  uint32_t nc, double* buf, int unpack, double2* blocks_out, cudaStream_t s);
 bool orders_supported(int ps, int pt, int pp);

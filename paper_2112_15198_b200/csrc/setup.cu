@@ -363,13 +363,16 @@ __device__ __forceinline__ void rec_store(T* __restrict__ p, uint64_t idx, const
 #ifndef IFGF_LOCATE_MINB
 #define IFGF_LOCATE_MINB 3
 #endif
-template <bool LAP, int R>
+// Rank plans (MARK = false: their cone set is final) keep the records of the
+// boxes [b_lo, b_hi] that hold their points; rec / rec_g then point b_lo's
+// pair offset before the window and L.npairs is the window's pair count.
+template <bool LAP, int R, bool MARK>
 __global__ void __launch_bounds__(256, IFGF_LOCATE_MINB)
     k_locate_points(const __grid_constant__ LevelDev L, const uint2* __restrict__ chunk,
                     const uint32_t* __restrict__ nchunk, const double* __restrict__ xs,
                     const double* __restrict__ ys, const double* __restrict__ zs, double kappa,
                     uint64_t* bits, uint32_t* __restrict__ rec_g, double* __restrict__ rec,
-                    int* err) {
+                    uint32_t b_lo, uint32_t b_hi, int* err) {
   __shared__ double2 trig[kTrigEntries];
   __shared__ double2 ptab[LAP ? 1 : kPhaseEntries];
   stage_trig(trig, L.trig);
@@ -381,6 +384,7 @@ __global__ void __launch_bounds__(256, IFGF_LOCATE_MINB)
   if (t >= *nchunk) return;
   const uint2 ch = chunk[t];
   const uint32_t b = ch.y;
+  if (b < b_lo || b > b_hi) return;
   const uint32_t fb = L.first[b], cnt = L.count[b];
   const uint32_t cntp = (cnt + R - 1) / R * R;
   const int n = (int)min((uint32_t)R, fb + cnt - ch.x);
@@ -428,7 +432,7 @@ __global__ void __launch_bounds__(256, IFGF_LOCATE_MINB)
     for (int j = 0; j < R; ++j) {
       g[j] = o[j].gamma;
       bi[j] = (uint64_t)cb * L.G + g[j];
-      bw[j] = bits[bi[j] >> 6];
+      bw[j] = MARK ? bits[bi[j] >> 6] : ~0ull;
     }
     double v[R];
     rec_store<R>(rec_g, idx, g);
@@ -456,11 +460,13 @@ __global__ void __launch_bounds__(256, IFGF_LOCATE_MINB)
     }
     rec_store<R>(rec + 3 * np, idx, v);
     if (!LAP) rec_store<R>(rec + 4 * np, idx, gi);
+    if (MARK) {
 #pragma unroll
-    for (int j = 0; j < R; ++j) {
-      const uint64_t m = 1ull << (bi[j] & 63);
-      if (!(bw[j] & m) && (j == 0 || bi[j] != bi[0]))
-        atomicOr((unsigned long long*)(bits + (bi[j] >> 6)), (unsigned long long)m);
+      for (int j = 0; j < R; ++j) {
+        const uint64_t m = 1ull << (bi[j] & 63);
+        if (!(bw[j] & m) && (j == 0 || bi[j] != bi[0]))
+          atomicOr((unsigned long long*)(bits + (bi[j] >> 6)), (unsigned long long)m);
+      }
     }
   }
 }
@@ -471,12 +477,22 @@ __global__ void __launch_bounds__(256, IFGF_LOCATE_MINB)
 template <int R>
 __global__ void __launch_bounds__(256)
     k_rec_cones(const __grid_constant__ LevelDev L, const uint2* __restrict__ chunk,
-                const uint32_t* __restrict__ nchunk, uint32_t* __restrict__ rec_g, int* err) {
+                const uint32_t* __restrict__ nchunk, uint32_t* __restrict__ rec_g, uint32_t b_lo,
+                uint32_t b_hi, uint32_t p_lo, uint32_t p_hi, int* err) {
   const size_t t = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
   if (t >= *nchunk) return;
   const uint2 ch = chunk[t];
   const uint32_t b = ch.y;
+  if (b < b_lo || b > b_hi) return;
   const uint32_t fb = L.first[b], cnt = L.count[b];
+  // a rank plan's window holds whole boxes: points of [b_lo, b_hi] outside the
+  // rank's [p_lo, p_hi) may see cones the rank does not store (never read)
+  bool mine[R];
+#pragma unroll
+  for (int j = 0; j < R; ++j) {
+    const uint32_t i = ch.x + ((uint32_t)j < fb + cnt - ch.x ? j : 0);
+    mine[j] = i >= p_lo && i < p_hi;
+  }
   const uint32_t cntp = (cnt + R - 1) / R * R;
   uint64_t idx = L.pair_off[b] + (ch.x - fb);
   for (uint32_t k = L.cous_off[b]; k < L.cous_off[b + 1]; ++k, idx += cntp) {
@@ -493,7 +509,7 @@ __global__ void __launch_bounds__(256)
 #pragma unroll
     for (int j = 0; j < R; ++j) {
       g[j] = find_cone(L, cb, g[j]);
-      if (g[j] == 0xffffffffu) {
+      if (g[j] == 0xffffffffu && mine[j]) {
         raise_err(err, kErrInterpCover);
         return;
       }
@@ -608,21 +624,132 @@ void check_device_error(ifgf_plan* P) {
   }
 }
 
-void launch_locate_points(ifgf_plan* P, int d, cudaStream_t s) {
+namespace {
+
+template <bool MARK>
+void launch_locate_range(ifgf_plan* P, int d, uint32_t b_lo, uint32_t b_hi, cudaStream_t s) {
   const Level& L = P->lv[d];
   const unsigned g = (unsigned)((L.chunk_cap + 255) / 256);
   auto go = [&](auto kern) {
     kern<<<g, 256, 0, s>>>(L.dev(), L.chunk, L.nchunk, P->xs, P->ys, P->zs, P->kappa, L.bits,
-                           L.rec_g, L.rec, P->err);
+                           L.rec_g, L.rec, b_lo, b_hi, P->err);
   };
   const bool lap = P->kappa == 0.0;
   switch (interp_points(P->K.P)) {
-    case 1: lap ? go(k_locate_points<true, 1>) : go(k_locate_points<false, 1>); break;
-    case 2: lap ? go(k_locate_points<true, 2>) : go(k_locate_points<false, 2>); break;
-    case 3: lap ? go(k_locate_points<true, 3>) : go(k_locate_points<false, 3>); break;
-    default: lap ? go(k_locate_points<true, 4>) : go(k_locate_points<false, 4>); break;
+    case 1: lap ? go(k_locate_points<true, 1, MARK>) : go(k_locate_points<false, 1, MARK>); break;
+    case 2: lap ? go(k_locate_points<true, 2, MARK>) : go(k_locate_points<false, 2, MARK>); break;
+    case 3: lap ? go(k_locate_points<true, 3, MARK>) : go(k_locate_points<false, 3, MARK>); break;
+    default: lap ? go(k_locate_points<true, 4, MARK>) : go(k_locate_points<false, 4, MARK>); break;
   }
   ++P->launches;
+}
+
+void launch_rec_cones(ifgf_plan* P, int d, uint32_t b_lo, uint32_t b_hi, uint32_t p_lo,
+                      uint32_t p_hi, cudaStream_t s) {
+  const Level& L = P->lv[d];
+  auto conv = [&](auto kern) {
+    kern<<<grid_for(L.chunk_cap), kT, 0, s>>>(L.dev(), L.chunk, L.nchunk, L.rec_g, b_lo, b_hi,
+                                              p_lo, p_hi, P->err);
+  };
+  switch (interp_points(P->K.P)) {
+    case 1: conv(k_rec_cones<1>); break;
+    case 2: conv(k_rec_cones<2>); break;
+    case 3: conv(k_rec_cones<3>); break;
+    default: conv(k_rec_cones<4>); break;
+  }
+  ++P->launches;
+}
+
+// Record storage of levels 3..D: `pairs[d]` pairs per level, all levels or
+// none.  An allocation failure (memory taken by others since the budget's
+// sample) only costs the records: K4 falls back to k_interp.
+bool alloc_records(ifgf_plan* P, const std::vector<unsigned long long>& pairs, cudaStream_t s) {
+  const int D = P->depth, planes = P->kappa == 0.0 ? 4 : 5;
+  bool ok = true;
+  std::vector<void*> got;
+  size_t got_bytes = 0;
+  for (int d = 3; d <= D && ok; ++d) {
+    Level& L = P->lv[d];
+    const size_t b[2] = {((size_t)planes * pairs[d] + 2) * sizeof(double) + 16,
+                         ((size_t)pairs[d] + 2) * sizeof(uint32_t) + 16};
+    void* p[2] = {nullptr, nullptr};
+    for (int i = 0; i < 2 && ok; ++i) {
+      if (cudaMallocAsync(&p[i], b[i], s) != cudaSuccess) {
+        cudaGetLastError();
+        ok = false;
+      } else {
+        got.push_back(p[i]);
+        got_bytes += b[i];
+      }
+    }
+    L.npairs = pairs[d];
+    L.rec = static_cast<double*>(p[0]);
+    L.rec_g = static_cast<uint32_t*>(p[1]);
+  }
+  if (ok) {
+    P->allocs.insert(P->allocs.end(), got.begin(), got.end());
+    P->bytes += got_bytes;
+  } else {
+    for (void* q : got) cudaFreeAsync(q, s);
+    for (int d = 3; d <= D; ++d) {
+      P->lv[d].rec = nullptr;
+      P->lv[d].rec_g = nullptr;
+      P->lv[d].npairs = 0;
+    }
+  }
+  return ok;
+}
+
+double records_fraction() {
+  static const double f = [] {
+    const char* v = std::getenv("IFGF_K4_REC_FRAC");
+    return v ? std::atof(v) : 0.15;
+  }();
+  return f;
+}
+
+}  // namespace
+
+void launch_locate_points(ifgf_plan* P, int d, cudaStream_t s) {
+  launch_locate_range<true>(P, d, 0u, 0xffffffffu, s);
+}
+
+// K4 records of a rank plan: for the boxes that hold the rank's points
+// [p0, p1) at every level (1/R of the single-GPU plan's records), built after
+// dist_prepare has made the level bitmaps rank-local, so the stored ordinals
+// are the rank's block slots.
+void build_rank_records(ifgf_plan* P, uint32_t p0, uint32_t p1) {
+  const int D = P->depth;
+  if (p1 <= p0 || D < 3 || !P->lv[D].pair_off) return;
+  cudaStream_t s = P->s_main;
+  std::vector<uint32_t> blo(D + 1, 0), bhi(D + 1, 0);
+  std::vector<unsigned long long> off(D + 1, 0), end(D + 1, 0);
+  for (int d = 3; d <= D; ++d) {
+    IFGF_CUDA(cudaMemcpyAsync(&blo[d], P->lv[d].ptbox + p0, 4, cudaMemcpyDeviceToHost, s));
+    IFGF_CUDA(cudaMemcpyAsync(&bhi[d], P->lv[d].ptbox + (p1 - 1), 4, cudaMemcpyDeviceToHost, s));
+  }
+  IFGF_CUDA(cudaStreamSynchronize(s));
+  for (int d = 3; d <= D; ++d) {
+    IFGF_CUDA(cudaMemcpyAsync(&off[d], P->lv[d].pair_off + blo[d], 8, cudaMemcpyDeviceToHost, s));
+    IFGF_CUDA(cudaMemcpyAsync(&end[d], P->lv[d].pair_off + bhi[d] + 1, 8, cudaMemcpyDeviceToHost, s));
+  }
+  IFGF_CUDA(cudaStreamSynchronize(s));
+  const int planes = P->kappa == 0.0 ? 4 : 5;
+  std::vector<unsigned long long> win(D + 1, 0);
+  unsigned long long pairs = 0;
+  for (int d = 3; d <= D; ++d) pairs += (win[d] = end[d] - off[d]);
+  const double need = (double)pairs * (planes * sizeof(double) + sizeof(uint32_t));
+  if (pairs == 0 || need > records_fraction() * (double)mem_available(P)) return;
+  if (!alloc_records(P, win, s)) return;
+  for (int d = 3; d <= D; ++d) {
+    Level& L = P->lv[d];
+    L.rec -= off[d];  // indexed by the level's global pair offsets
+    L.rec_g -= off[d];
+    launch_locate_range<false>(P, d, blo[d], bhi[d], s);
+    launch_rec_cones(P, d, blo[d], bhi[d], p0, p1, s);
+  }
+  IFGF_CUDA(cudaStreamSynchronize(s));
+  check_device_error(P);
 }
 
 void build_plan(ifgf_plan* P, const double* d_x, const double* d_y, const double* d_z) {
@@ -818,11 +945,9 @@ void build_plan(ifgf_plan* P, const double* d_x, const double* d_y, const double
     const char* v = std::getenv("IFGF_K4_RECORDS");
     return !v || std::atoi(v) != 0;
   }();
-  static const double rec_frac = [] {
-    const char* v = std::getenv("IFGF_K4_REC_FRAC");
-    return v ? std::atof(v) : 0.15;
-  }();
-  const bool want_records = P->k4_records && rec_env && D >= 3;
+  const double rec_frac = records_fraction();
+  // rank plans get the offsets here and their records from build_rank_records
+  const bool want_records = rec_env && D >= 3;
   std::vector<unsigned long long> pair_total(D + 1, 0);
   for (int d = 3; d <= D; ++d) {
     Level& L = P->lv[d];
@@ -894,42 +1019,8 @@ void build_plan(ifgf_plan* P, const double* d_x, const double* d_y, const double
     unsigned long long pairs = 0;
     for (int d = 3; d <= D; ++d) pairs += pair_total[d];
     const double need = (double)pairs * (planes * sizeof(double) + sizeof(uint32_t));
-    if (pairs > 0 && need <= rec_frac * (double)mem_available(P)) {
-      // an allocation failure (memory taken by others since the budget's
-      // sample) only costs the records: the levels fall back to k_interp
-      bool ok = true;
-      std::vector<void*> got;
-      size_t got_bytes = 0;
-      for (int d = 3; d <= D && ok; ++d) {
-        Level& L = P->lv[d];
-        const size_t b[2] = {((size_t)planes * pair_total[d] + 1) * sizeof(double) + 16,
-                             ((size_t)pair_total[d] + 1) * sizeof(uint32_t) + 16};
-        void* p[2] = {nullptr, nullptr};
-        for (int i = 0; i < 2 && ok; ++i) {
-          if (cudaMallocAsync(&p[i], b[i], s) != cudaSuccess) {
-            cudaGetLastError();
-            ok = false;
-          } else {
-            got.push_back(p[i]);
-            got_bytes += b[i];
-          }
-        }
-        L.npairs = pair_total[d];
-        L.rec = static_cast<double*>(p[0]);
-        L.rec_g = static_cast<uint32_t*>(p[1]);
-      }
-      if (ok) {
-        P->allocs.insert(P->allocs.end(), got.begin(), got.end());
-        P->bytes += got_bytes;
-      } else {  // all or nothing (the blocks keep their room)
-        for (void* q : got) cudaFreeAsync(q, s);
-        for (int d = 3; d <= D; ++d) {
-          P->lv[d].rec = nullptr;
-          P->lv[d].rec_g = nullptr;
-          P->lv[d].npairs = 0;
-        }
-      }
-    }
+    if (!P->rank_plan && pairs > 0 && need <= rec_frac * (double)mem_available(P))
+      alloc_records(P, pair_total, s);
   }
   for (int d = 3; d <= D; ++d) {
     Level& L = P->lv[d];
@@ -1022,16 +1113,7 @@ void build_plan(ifgf_plan* P, const double* d_x, const double* d_y, const double
     if (L.rec) {  // records: segment -> cone ordinal, on the aux stream
       IFGF_CUDA(cudaEventRecord(ev_pts[d], s));
       IFGF_CUDA(cudaStreamWaitEvent(sa, ev_pts[d], 0));
-      auto conv = [&](auto kern) {
-        kern<<<grid_for(L.chunk_cap), kT, 0, sa>>>(L.dev(), L.chunk, L.nchunk, L.rec_g, P->err);
-      };
-      switch (interp_points(P->K.P)) {
-        case 1: conv(k_rec_cones<1>); break;
-        case 2: conv(k_rec_cones<2>); break;
-        case 3: conv(k_rec_cones<3>); break;
-        default: conv(k_rec_cones<4>); break;
-      }
-      ++P->launches;
+      launch_rec_cones(P, d, 0u, 0xffffffffu, 0u, 0xffffffffu, sa);
     }
     mark("  compact");
   }
